@@ -1,0 +1,195 @@
+/*
+ * csflow_b200.h -- C ABI of the B200-native implicit pseudo-time iteration of
+ * arXiv 2403.03440 (component-splitting, CS, and coupled, CI, LU-SGS).
+ *
+ * The reference (/root/reference/pkg/src/csflow) has no FFI: its boundary is
+ * a set of Python functions.  Each entry point below replaces one of them and
+ * cites it as <file>:<line>.  The drop-in Python package
+ * paper_2403_03440_b200 binds these symbols with ctypes.
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers to FP64 data unless stated.
+ *  - Cell fields are SoA, component-major: x[c * N + cell], with
+ *    cell = (i * nj + j) * nk + k (the reference's C order, component axis
+ *    moved to the front) and N = ni * nj * nk.
+ *  - Face fields of direction d are SoA over the face-shaped grid
+ *    (n_d + 1 along axis d): S_d[x * NF_d + f], f = (i * nj' + j) * nk' + k.
+ *  - Padded primitive layout (fields.py:1-20): [rho, u, v, w, p, Y_1..Y_ns, T].
+ *  - `stream` is a cudaStream_t passed as void*; every call is stream-ordered
+ *    and asynchronous.  Errors inside kernels are recorded in a device flag
+ *    word; csb_status() synchronises the stream and reports them.
+ *  - Return value: CSB_OK or a CSB_E* code (csb_last_error() has the text).
+ */
+#ifndef CSFLOW_B200_H
+#define CSFLOW_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return / status codes (errors.py:4-75) */
+#define CSB_OK 0
+#define CSB_E_NONPHYSICAL 1   /* NonPhysicalState (mixture.py:169-193, spatial.py:54, 269; driver.py:223, 250) */
+#define CSB_E_SINGULAR 2      /* SingularDiagonal (implicit.py:406-408, lusgs.py:253, 267) */
+#define CSB_E_ZEROWAVE 3      /* ZeroWavespeed (implicit.py:42-43) */
+#define CSB_E_DIVERGED 4      /* Diverged (driver.py:259-262, 282-283) */
+#define CSB_E_MISSINGBC 5     /* MissingBC (boundary.py:60-70) */
+#define CSB_E_BADARG 10
+#define CSB_E_CUDA 11
+#define CSB_E_STATE 12        /* call order (model/grid/bc/workspace not set) */
+
+/* device flag bits reported by csb_status (see csb_common.cuh ErrBit) */
+#define CSB_F_DECODE (1u << 0)
+#define CSB_F_FACE_T (1u << 1)
+#define CSB_F_RES_NONFINITE (1u << 2)
+#define CSB_F_ZERO_WAVE (1u << 3)
+#define CSB_F_SINGULAR (1u << 4)
+#define CSB_F_GATE (1u << 5)
+#define CSB_F_KSKIP (1u << 6)
+#define CSB_F_BLOCK (1u << 7)
+#define CSB_F_GATE_DECODE (1u << 8)
+
+/* schemes (implicit.py:30 MODES) */
+#define CSB_CI 0
+#define CSB_CS1 1
+#define CSB_CS2 2
+
+/* boundary kinds (boundary.py:22) */
+#define CSB_BC_FARFIELD 0
+#define CSB_BC_OUTFLOW 1
+#define CSB_BC_WALL 2
+#define CSB_BC_SYMMETRY 3
+#define CSB_BC_PERIODIC 4
+
+typedef struct csb_ctx csb_ctx;
+
+/* ---------------------------------------------------------------- context */
+int csb_create(csb_ctx** out);
+void csb_destroy(csb_ctx* ctx);
+const char* csb_last_error(const csb_ctx* ctx);
+int csb_version(void);
+
+/* Species table, host arrays of length ns (MixtureModel, mixture.py:58-104). */
+int csb_set_model(csb_ctx* ctx, int ns, const double* M, const double* cp, const double* hf,
+                  const double* Tref, const double* mu_ref, const double* T_mu,
+                  const double* S_mu, double Pr, double Sc);
+
+/* Mechanism (Mechanism/Reaction, chemistry.py:21-43), host arrays:
+ * nu_r, nu_p: [nrx][ns] stoichiometry; fwd: [nrx][3] (A_f, b_f, Ea_f);
+ * bwd: [nrx][3] (A_b, b_b, Ea_b) with NaN A_b for irreversible reactions.
+ * enabled = 0 or nrx = 0 freezes the chemistry. */
+int csb_set_mechanism(csb_ctx* ctx, int nrx, const double* nu_r, const double* nu_p,
+                      const double* fwd, const double* bwd, int enabled);
+
+/* Grid metrics (StructuredGrid, grid.py:20-48), DEVICE SoA arrays owned by
+ * the caller: Si [3][ni+1][nj][nk], Sj [3][ni][nj+1][nk], Sk [3][ni][nj][nk+1],
+ * vol [ni][nj][nk]. */
+int csb_set_grid(csb_ctx* ctx, int ni, int nj, int nk, const double* Si, const double* Sj,
+                 const double* Sk, const double* vol);
+
+/* Boundary condition of face 0..5 = imin, imax, jmin, jmax, kmin, kmax
+ * (BoundaryCondition, boundary.py:25-38).  fs_prim: HOST padded-layout
+ * freestream vector (6 + ns) for farfield, else NULL; axis = -1 for none. */
+int csb_set_bc(csb_ctx* ctx, int face, int kind, double T_wall, int axis, const double* fs_prim);
+
+/* Workspace: bytes needed for the current model/grid (with_block != 0 adds
+ * the CI+chemistry ns x ns blocks), then hand over a device buffer of at
+ * least that size.  No allocation happens on the hot path. */
+size_t csb_workspace_bytes(const csb_ctx* ctx, int with_block);
+int csb_set_workspace(csb_ctx* ctx, void* dev, size_t bytes);
+
+/* Read and clear the device flag word (synchronises `stream`).  flags: bit
+ * set; first_cell: first offending cell of the lowest set bit; gate_count:
+ * number of cells that failed the post-update gate. */
+int csb_status(csb_ctx* ctx, unsigned long long* flags, long long* first_cell,
+               long long* gate_count, void* stream);
+
+/* ---------------------------------------------------------------- stages */
+
+/* assemble_residual (spatial.py:207-274): q [nv][N] -> R [nv][N].
+ * P (nullable): padded primitives [6+ns][(ni+4)(nj+4)(nk+4)] (return_padded). */
+int csb_residual(csb_ctx* ctx, const double* q, double* R, double* P, int first_order,
+                 void* stream);
+
+/* Grid-free entry points take the cell count N explicitly (N <= 0: the
+ * grid's N); they use only the context's model, mechanism and flag word. */
+
+/* cons_to_prim (mixture.py:287-307): q [nv][N] -> out [12+ns][N] =
+ * rho, u, v, w, p, T, c, gamma, h, Ek, R, cp, Y_1..Y_ns. */
+int csb_cons_to_prim(csb_ctx* ctx, long long N, const double* q, double* out, void* stream);
+
+/* production_rates (chemistry.py:68-73): omega [ns][N]. */
+int csb_production_rates(csb_ctx* ctx, long long N, const double* q, double* omega, void* stream);
+
+/* source_jacobian + source_spectral_radius (chemistry.py:76-104):
+ * dOm [ns*ns][N] (entry (s, r) at (s*ns + r)), lamS [N] (nullable). */
+int csb_source_jacobian(csb_ctx* ctx, long long N, const double* q, double* dOm, double* lamS,
+                        void* stream);
+
+/* cell_spectral_radii (implicit.py:152-163): lam_inv, lam_vis [3][N]. */
+int csb_spectral_radii(csb_ctx* ctx, const double* q, double* lam_inv, double* lam_vis,
+                       void* stream);
+
+/* local_time_step on given radii (implicit.py:33-44): lam_inv, lam_vis
+ * AoS [N][3]; lamS [N] or NULL with lamS_scalar; J [N]. */
+int csb_local_time_step(csb_ctx* ctx, long long N, const double* lam_inv, const double* lam_vis,
+                        const double* lamS, double lamS_scalar, double cfl, const double* J,
+                        double* dtau, void* stream);
+
+/* dtau of one implicit step as _implicit_step computes it (driver.py:235-239):
+ * radii + (chemistry) source radius -> dtau [N].  dOm_in (nullable): inject
+ * the source Jacobian [ns*ns][N] instead of computing it. */
+int csb_time_step(csb_ctx* ctx, const double* q, double cfl, const double* dOm_in, double* dtau,
+                  void* stream);
+
+/* assemble_lhs (implicit.py:329-403) into the context's operator buffers.
+ * offdiag_paper: species_offdiag == "paper"; theta/dt: dual-time diagonal
+ * (dt <= 0 or non-finite = steady).  dOm_in as above. */
+int csb_assemble(csb_ctx* ctx, const double* q, const double* dtau, int scheme,
+                 int offdiag_paper, double theta, double dt, const double* dOm_in, void* stream);
+
+/* Copy one field of the assembled operator (ImplicitOperator, implicit.py:210-241)
+ * into dst (device).  which: 0 w [nv][N], 1 b [nv][N], 2 sp_lower [3][N],
+ * 3 sp_upper [3][N], 4 d_scal [N], 5 d_species [ns][N] (broadcast when
+ * frozen), 6+d lam_face[d], 9+d lam_face_sp[d] (face-shaped), 12 dinv
+ * [ns*ns][N], 13 vdom [ns*ns][N].  q must be the state assembled. */
+int csb_operator_field(csb_ctx* ctx, const double* q, int which, double* dst, void* stream);
+
+/* lusgs_solve (lusgs.py:250-274) with the assembled operator: rhs [nv][N] ->
+ * dq [nv][N]; dq_star (nullable) receives the forward-sweep result. */
+int csb_lusgs(csb_ctx* ctx, const double* rhs, double* dq, double* dq_star, void* stream);
+
+/* _apply_update + admissibility gate (driver.py:216-229, 250): q, dq -> q_new. */
+int csb_apply_update(csb_ctx* ctx, long long N, const double* q, const double* dq, int scheme,
+                     double* q_new, void* stream);
+
+/* correct_increment_cs1 (mode 1) / correct_normalize_cs2 (mode 2)
+ * (implicit.py:113-135) on row-major [rows][ns] arrays. */
+int csb_correct(csb_ctx* ctx, int mode, long long rows, int ns, const double* rho_s,
+                const double* d_rho_s, const double* d_rho, double* out, void* stream);
+
+/* residual_norms (driver.py:85-90): out3 (device) = flow, species, density. */
+int csb_residual_norms(csb_ctx* ctx, long long N, const double* R, double* out3, void* stream);
+
+/* _implicit_step (driver.py:232-251), steady: q, R -> q_new (dq kept in the
+ * workspace).  dOm_in as above. */
+int csb_implicit_step(csb_ctx* ctx, const double* q, const double* R, double cfl, int scheme,
+                      int offdiag_paper, const double* dOm_in, double* q_new, void* stream);
+
+/* One steady iteration (driver.py:279-308 without the retry/stop logic):
+ * R = residual(q) (R_out nullable: internal), norms -> norms3 (device,
+ * nullable), q_new = implicit step. */
+int csb_iteration(csb_ctx* ctx, const double* q, double cfl, int scheme, int offdiag_paper,
+                  int first_order, double* q_new, double* R_out, double* norms3, void* stream);
+
+/* AoS [N][nv] <-> SoA [nv][N] (device). */
+int csb_transpose(long long N, int nv, const double* src, double* dst, int to_soa, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CSFLOW_B200_H */

@@ -1,0 +1,619 @@
+// csflow-b200: C-ABI entry points (include/csflow_b200.h).
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/csflow_b200.h"
+#include "csb_common.cuh"
+#include "csb_kernels.cuh"
+
+using namespace csb;
+
+struct csb_ctx {
+  int ns = 0;
+  bool has_model = false, has_grid = false, has_ws = false;
+  Model host_model{};
+  Model* d_model = nullptr;
+  std::vector<Reaction> rx;
+  Reaction* d_rx = nullptr;
+  int nrx_active = 0;
+  GridDev g{};
+  int geom2d_ok = 0;
+  int k2d_disabled = 0;
+  int bc_kind[6] = {-1, -1, -1, -1, -1, -1};
+  int bc_axis[6] = {-1, -1, -1, -1, -1, -1};
+  double bc_Tw[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<double> fs;  // [6][nc]
+  double* d_fs = nullptr;
+  bool fs_dirty = true;
+  // workspace carve
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  bool ws_block = false;
+  unsigned long long* flags = nullptr;
+  OpDev op{};
+  double *dtau = nullptr, *R = nullptr, *dq = nullptr, *partial = nullptr, *norms = nullptr;
+  double* dom_scratch = nullptr;
+  int assembled_scheme = -1;
+  std::string err;
+};
+
+namespace {
+
+int fail(csb_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  return code;
+}
+
+int cuda_check(csb_ctx* c, cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return CSB_OK;
+  return fail(c, CSB_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+Mech mech_of(const csb_ctx* c) {
+  Mech m;
+  m.nrx = c->nrx_active;
+  m.rx = c->d_rx;
+  return m;
+}
+
+BCDev bc_of(const csb_ctx* c) {
+  BCDev b;
+  for (int f = 0; f < 6; ++f) {
+    b.kind[f] = c->bc_kind[f];
+    b.axis[f] = c->bc_axis[f];
+    b.Tw[f] = c->bc_Tw[f];
+  }
+  b.fs = c->d_fs;
+  return b;
+}
+
+bool bcs_ready(const csb_ctx* c) {
+  for (int f = 0; f < 6; ++f)
+    if (c->bc_kind[f] < 0) return false;
+  return true;
+}
+
+int check_bcs(csb_ctx* c) {
+  static const char* names[6] = {"imin", "imax", "jmin", "jmax", "kmin", "kmax"};
+  for (int f = 0; f < 6; ++f)
+    if (c->bc_kind[f] < 0)
+      return fail(c, CSB_E_MISSINGBC, std::string("no boundary condition for face '") + names[f] + "'");
+  for (int f = 0; f < 6; ++f) {
+    if (c->bc_kind[f] == CSB_BC_PERIODIC && c->bc_kind[f ^ 1] != CSB_BC_PERIODIC)
+      return fail(c, CSB_E_MISSINGBC, std::string("periodic face '") + names[f] +
+                                          "' requires periodic '" + names[f ^ 1] + "'");
+  }
+  return CSB_OK;
+}
+
+bool use_k2d(const csb_ctx* c) {
+  if (c->g.nk != 1 || !c->geom2d_ok || c->k2d_disabled) return false;
+  const int a = c->bc_kind[4], b = c->bc_kind[5];
+  if (a != b) return false;
+  if (a == CSB_BC_OUTFLOW || a == CSB_BC_PERIODIC) return true;
+  if (a == CSB_BC_SYMMETRY) {
+    const bool ax_ok = (c->bc_axis[4] < 0 || c->bc_axis[4] == 2) &&
+                       (c->bc_axis[5] < 0 || c->bc_axis[5] == 2);
+    return ax_ok;
+  }
+  return false;
+}
+
+int sync_fs(csb_ctx* c) {
+  if (!c->fs_dirty) return CSB_OK;
+  const int nc = 6 + c->ns;
+  if (!c->d_fs) {
+    if (cudaMalloc(&c->d_fs, sizeof(double) * 6 * (size_t)(6 + csb::MAXNS)) != cudaSuccess)
+      return fail(c, CSB_E_CUDA, "cudaMalloc(freestream)");
+  }
+  if (c->fs.size() != (size_t)6 * nc) c->fs.assign((size_t)6 * nc, NAN);
+  cudaError_t e = cudaMemcpy(c->d_fs, c->fs.data(), sizeof(double) * 6 * nc, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_check(c, e, "upload freestream");
+  c->fs_dirty = false;
+  return CSB_OK;
+}
+
+int ready(csb_ctx* c, bool need_ws = true) {
+  if (!c) return CSB_E_BADARG;
+  if (!c->has_model) return fail(c, CSB_E_STATE, "model not set");
+  if (!c->has_grid) return fail(c, CSB_E_STATE, "grid not set");
+  if (need_ws && !c->has_ws) return fail(c, CSB_E_STATE, "workspace not set");
+  return CSB_OK;
+}
+
+GridDev with_n(const csb_ctx* c, long long N) {
+  GridDev g = c->g;
+  if (N > 0) g.N = N;
+  return g;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Carve {
+  size_t off = 0;
+  char* base;
+  template <class T>
+  T* take(size_t count) {
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off = align_up(off + count * sizeof(T));
+    return p;
+  }
+};
+
+size_t carve(csb_ctx* c, char* base, bool with_block) {
+  Carve k{0, base};
+  const long long N = c->g.N;
+  const int ns = c->ns, nv = 5 + ns;
+  c->flags = k.take<unsigned long long>(FLAG_WORDS);
+  c->op.st = k.take<double>((size_t)NST * N);
+  c->op.Y = k.take<double>((size_t)ns * N);
+  c->op.d = k.take<double>((size_t)N);
+  c->op.dsp = k.take<double>((size_t)ns * N);
+  c->op.dinv_sp = k.take<double>((size_t)ns * N);
+  for (int d = 0; d < 3; ++d) c->op.lam[d] = k.take<double>((size_t)c->g.NF[d]);
+  for (int d = 0; d < 3; ++d) c->op.lamsp[d] = k.take<double>((size_t)c->g.NF[d]);
+  c->op.dom = k.take<double>((size_t)(with_block ? ns * ns : ns) * N);
+  c->op.lamS = k.take<double>((size_t)N);
+  c->op.dinv = with_block ? k.take<double>((size_t)ns * ns * N) : nullptr;
+  c->dtau = k.take<double>((size_t)N);
+  c->R = k.take<double>((size_t)nv * N);
+  c->dq = k.take<double>((size_t)nv * N);
+  c->partial = k.take<double>(3 * 512);
+  c->norms = k.take<double>(4);
+  return k.off;
+}
+
+int reset_flags(csb_ctx* c, cudaStream_t st) {
+  unsigned long long h[FLAG_WORDS];
+  for (int i = 0; i < FLAG_WORDS; ++i) h[i] = 0ull;
+  for (int b = 0; b < EB_COUNT; ++b) h[1 + b] = ~0ull;
+  return cuda_check(c, cudaMemcpyAsync(c->flags, h, sizeof(h), cudaMemcpyHostToDevice, st),
+                    "reset flags");
+}
+
+}  // namespace
+
+extern "C" {
+
+int csb_version(void) { return 1; }
+
+int csb_create(csb_ctx** out) {
+  if (!out) return CSB_E_BADARG;
+  *out = new csb_ctx();
+  return CSB_OK;
+}
+
+void csb_destroy(csb_ctx* c) {
+  if (!c) return;
+  if (c->d_model) cudaFree(c->d_model);
+  if (c->d_rx) cudaFree(c->d_rx);
+  if (c->d_fs) cudaFree(c->d_fs);
+  delete c;
+}
+
+const char* csb_last_error(const csb_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int csb_set_model(csb_ctx* c, int ns, const double* M, const double* cp, const double* hf,
+                  const double* Tref, const double* mu_ref, const double* T_mu,
+                  const double* S_mu, double Pr, double Sc) {
+  if (!c) return CSB_E_BADARG;
+  if (ns < 1 || ns > MAXNS) return fail(c, CSB_E_BADARG, "ns must be in [1, 64]");
+  Model m{};
+  m.ns = ns;
+  m.Pr = Pr;
+  m.Sc = Sc;
+  for (int s = 0; s < ns; ++s) {
+    m.M[s] = M[s];
+    m.cp[s] = cp[s];
+    m.Rs[s] = R_U / M[s];
+    m.bs[s] = hf[s] - cp[s] * Tref[s];
+    m.mu_ref[s] = mu_ref[s];
+    m.T_mu[s] = T_mu[s];
+    m.S_mu[s] = S_mu[s];
+    m.TS[s] = T_mu[s] + S_mu[s];
+  }
+  if (!c->d_model && cudaMalloc(&c->d_model, sizeof(Model)) != cudaSuccess)
+    return fail(c, CSB_E_CUDA, "cudaMalloc(model)");
+  cudaError_t e = cudaMemcpy(c->d_model, &m, sizeof(Model), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_check(c, e, "upload model");
+  if (c->has_model && c->ns != ns) {
+    c->has_ws = false;
+    c->fs.clear();
+  }
+  c->host_model = m;
+  c->ns = ns;
+  c->has_model = true;
+  c->fs_dirty = true;
+  return CSB_OK;
+}
+
+int csb_set_mechanism(csb_ctx* c, int nrx, const double* nu_r, const double* nu_p,
+                      const double* fwd, const double* bwd, int enabled) {
+  if (!c || !c->has_model) return fail(c, CSB_E_STATE, "set the model before the mechanism");
+  const int ns = c->ns;
+  std::vector<Reaction> v;
+  for (int r = 0; r < nrx; ++r) {
+    Reaction x{};
+    x.Af = fwd[3 * r];
+    x.bf = fwd[3 * r + 1];
+    x.Eaf = fwd[3 * r + 2];
+    x.has_back = bwd && !std::isnan(bwd[3 * r]);
+    if (x.has_back) {
+      x.Ab = bwd[3 * r];
+      x.bb = bwd[3 * r + 1];
+      x.Eab = bwd[3 * r + 2];
+    }
+    for (int s = 0; s < ns; ++s) {
+      const double a = nu_r[(size_t)r * ns + s], b = nu_p[(size_t)r * ns + s];
+      if (a != 0.0) {
+        if (x.nr >= MAXTERM) return fail(c, CSB_E_BADARG, "too many reactant terms");
+        x.rs[x.nr] = s;
+        x.rn[x.nr++] = a;
+      }
+      if (b != 0.0) {
+        if (x.np >= MAXTERM) return fail(c, CSB_E_BADARG, "too many product terms");
+        x.ps[x.np] = s;
+        x.pn[x.np++] = b;
+      }
+      if (b - a != 0.0) {
+        x.ds[x.nd] = s;
+        x.dn[x.nd++] = b - a;
+      }
+    }
+    v.push_back(x);
+  }
+  if (c->d_rx) {
+    cudaFree(c->d_rx);
+    c->d_rx = nullptr;
+  }
+  if (!v.empty()) {
+    if (cudaMalloc(&c->d_rx, sizeof(Reaction) * v.size()) != cudaSuccess)
+      return fail(c, CSB_E_CUDA, "cudaMalloc(reactions)");
+    cudaError_t e = cudaMemcpy(c->d_rx, v.data(), sizeof(Reaction) * v.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_check(c, e, "upload reactions");
+  }
+  c->rx = v;
+  c->nrx_active = (enabled && nrx > 0) ? nrx : 0;
+  return CSB_OK;
+}
+
+int csb_set_grid(csb_ctx* c, int ni, int nj, int nk, const double* Si, const double* Sj,
+                 const double* Sk, const double* vol) {
+  if (!c) return CSB_E_BADARG;
+  if (ni < 1 || nj < 1 || nk < 1) return fail(c, CSB_E_BADARG, "grid dims must be positive");
+  const bool changed = !c->has_grid || c->g.ni != ni || c->g.nj != nj || c->g.nk != nk;
+  GridDev g{};
+  g.ni = ni;
+  g.nj = nj;
+  g.nk = nk;
+  g.N = (long long)ni * nj * nk;
+  g.S[0] = Si;
+  g.S[1] = Sj;
+  g.S[2] = Sk;
+  g.NF[0] = (long long)(ni + 1) * nj * nk;
+  g.NF[1] = (long long)ni * (nj + 1) * nk;
+  g.NF[2] = (long long)ni * nj * (nk + 1);
+  g.vol = vol;
+  c->g = g;
+  c->has_grid = true;
+  if (changed) c->has_ws = false;
+  c->geom2d_ok = 0;
+  c->k2d_disabled = 0;
+  if (nk == 1) {
+    int* d_ok = nullptr;
+    if (cudaMalloc(&d_ok, sizeof(int)) != cudaSuccess) return fail(c, CSB_E_CUDA, "cudaMalloc");
+    int one = 1;
+    cudaMemcpy(d_ok, &one, sizeof(int), cudaMemcpyHostToDevice);
+    launch_check_2d(g, d_ok, 0);
+    cudaError_t e = cudaMemcpy(&one, d_ok, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(d_ok);
+    if (e != cudaSuccess) return cuda_check(c, e, "check 2-D geometry");
+    c->geom2d_ok = one;
+  }
+  return CSB_OK;
+}
+
+int csb_set_bc(csb_ctx* c, int face, int kind, double T_wall, int axis, const double* fs_prim) {
+  if (!c || !c->has_model) return fail(c, CSB_E_STATE, "set the model before boundary conditions");
+  if (face < 0 || face > 5 || kind < 0 || kind > 4) return fail(c, CSB_E_BADARG, "bad face/kind");
+  if (kind == CSB_BC_FARFIELD && !fs_prim)
+    return fail(c, CSB_E_MISSINGBC, "farfield boundary requires a freestream state");
+  if (kind == CSB_BC_WALL && !(T_wall > 0.0))
+    return fail(c, CSB_E_MISSINGBC, "isothermal wall requires T_wall > 0");
+  c->bc_kind[face] = kind;
+  c->bc_axis[face] = axis;
+  c->bc_Tw[face] = T_wall;
+  const int nc = 6 + c->ns;
+  if (c->fs.size() != (size_t)6 * nc) c->fs.assign((size_t)6 * nc, NAN);
+  for (int k = 0; k < nc; ++k) c->fs[(size_t)face * nc + k] = fs_prim ? fs_prim[k] : NAN;
+  c->fs_dirty = true;
+  c->k2d_disabled = 0;
+  return CSB_OK;
+}
+
+size_t csb_workspace_bytes(const csb_ctx* c, int with_block) {
+  if (!c || !c->has_model || !c->has_grid) return 0;
+  csb_ctx tmp = *c;
+  return carve(&tmp, nullptr, with_block != 0) + 256;
+}
+
+int csb_set_workspace(csb_ctx* c, void* dev, size_t bytes) {
+  int r = ready(c, false);
+  if (r) return r;
+  const size_t need_plain = csb_workspace_bytes(c, 0);
+  const size_t need_block = csb_workspace_bytes(c, 1);
+  if (bytes < need_plain) return fail(c, CSB_E_BADARG, "workspace too small");
+  char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<size_t>(dev)));
+  c->ws_block = bytes >= need_block;
+  carve(c, base, c->ws_block);
+  c->ws = reinterpret_cast<char*>(dev);
+  c->ws_bytes = bytes;
+  c->has_ws = true;
+  c->assembled_scheme = -1;
+  return reset_flags(c, 0) ? CSB_E_CUDA : (cudaDeviceSynchronize() == cudaSuccess ? CSB_OK : CSB_E_CUDA);
+}
+
+int csb_status(csb_ctx* c, unsigned long long* flags, long long* first_cell, long long* gate_count,
+               void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  cudaStream_t st = S(stream);
+  unsigned long long h[FLAG_WORDS];
+  cudaError_t e = cudaMemcpyAsync(h, c->flags, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_check(c, e, "read status");
+  if (flags) *flags = h[0];
+  if (first_cell) {
+    *first_cell = -1;
+    for (int b = 0; b < EB_COUNT; ++b)
+      if (h[0] & (1ull << b)) {
+        *first_cell = (long long)h[1 + b];
+        break;
+      }
+  }
+  if (gate_count) *gate_count = (long long)h[FLAG_GATE_COUNT];
+  if (h[0] & (1ull << EB_KSKIP)) c->k2d_disabled = 1;
+  return reset_flags(c, st);
+}
+
+int csb_residual(csb_ctx* c, const double* q, double* R, double* P, int first_order,
+                 void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  if ((r = check_bcs(c))) return r;
+  if ((r = sync_fs(c))) return r;
+  cudaStream_t st = S(stream);
+  const bool k2d = use_k2d(c);
+  cudaError_t e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
+                                  k2d, c->flags, st);
+  if (e == cudaSuccess && P) e = launch_padded(c->d_model, c->ns, c->g, bc_of(c), q, P, c->flags, st);
+  return cuda_check(c, e, "residual");
+}
+
+int csb_cons_to_prim(csb_ctx* c, long long N, const double* q, double* out, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  return cuda_check(c, launch_decode(c->d_model, c->ns, with_n(c, N), q, out, c->flags, S(stream)),
+                    "decode");
+}
+
+int csb_production_rates(csb_ctx* c, long long N, const double* q, double* omega, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  return cuda_check(c, launch_production(c->d_model, c->ns, with_n(c, N), mech_of(c), q, omega, c->flags,
+                                         S(stream)),
+                    "production");
+}
+
+int csb_source_jacobian(csb_ctx* c, long long N, const double* q, double* dOm, double* lamS,
+                        void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  const GridDev g = with_n(c, N);
+  if (mech_of(c).nrx == 0) {
+    cudaStream_t st = S(stream);
+    cudaError_t e = cudaMemsetAsync(dOm, 0, sizeof(double) * c->ns * c->ns * g.N, st);
+    if (e == cudaSuccess && lamS) e = cudaMemsetAsync(lamS, 0, sizeof(double) * g.N, st);
+    return cuda_check(c, e, "source jacobian (frozen)");
+  }
+  return cuda_check(c, launch_source_jacobian(c->d_model, c->ns, g, mech_of(c), q, dOm, 1, lamS,
+                                              nullptr, c->flags, S(stream)),
+                    "source jacobian");
+}
+
+int csb_spectral_radii(csb_ctx* c, const double* q, double* lam_inv, double* lam_vis,
+                       void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  return cuda_check(c, launch_time_step(c->d_model, c->ns, c->g, q, 1.0, nullptr, nullptr, lam_inv,
+                                        lam_vis, c->flags, S(stream)),
+                    "spectral radii");
+}
+
+int csb_local_time_step(csb_ctx* c, long long N, const double* lam_inv, const double* lam_vis,
+                        const double* lamS, double lamS_scalar, double cfl, const double* J,
+                        double* dtau, void* stream) {
+  if (!c || !c->has_ws) return fail(c, CSB_E_STATE, "workspace (flags) not set");
+  return cuda_check(c, launch_dtau_arrays(N, lam_inv, lam_vis, lamS, lamS_scalar, cfl, J, dtau,
+                                          c->flags, S(stream)),
+                    "local_time_step");
+}
+
+static int time_step_impl(csb_ctx* c, const double* q, double cfl, const double* dOm_in,
+                          double* dtau, bool full_dom, cudaStream_t st) {
+  const bool chem = mech_of(c).nrx > 0;
+  const double* lamS = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (chem) {
+    e = launch_source_jacobian(c->d_model, c->ns, c->g, mech_of(c), q, c->op.dom, full_dom ? 1 : 0,
+                               c->op.lamS, dOm_in, c->flags, st);
+    lamS = c->op.lamS;
+  }
+  if (e == cudaSuccess)
+    e = launch_time_step(c->d_model, c->ns, c->g, q, cfl, lamS, dtau, nullptr, nullptr, c->flags,
+                         st);
+  return cuda_check(c, e, "time step");
+}
+
+int csb_time_step(csb_ctx* c, const double* q, double cfl, const double* dOm_in, double* dtau,
+                  void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  return time_step_impl(c, q, cfl, dOm_in, dtau, c->ws_block, S(stream));
+}
+
+static int assemble_impl(csb_ctx* c, const double* q, const double* dtau, int scheme,
+                         int offdiag_paper, double theta, double dt, const double* dOm_in,
+                         bool dom_ready, cudaStream_t st) {
+  if (scheme < 0 || scheme > 2) return fail(c, CSB_E_BADARG, "unknown scheme");
+  const bool chem = mech_of(c).nrx > 0;
+  if (chem && scheme == SCH_CI && !c->ws_block)
+    return fail(c, CSB_E_STATE, "CI with chemistry needs a workspace with blocks");
+  OpDev& op = c->op;
+  op.mode = scheme;
+  op.sp_scale = offdiag_paper ? 1.0 : 0.5;
+  op.chem = chem ? 1 : 0;
+  op.dsp_per_species = chem ? 1 : 0;
+  op.dom_full = (chem && c->ws_block) ? 1 : 0;
+  cudaError_t e = cudaSuccess;
+  if (chem && !dom_ready)
+    e = launch_source_jacobian(c->d_model, c->ns, c->g, mech_of(c), q, op.dom, op.dom_full,
+                               op.lamS, dOm_in, c->flags, st);
+  if (e == cudaSuccess)
+    e = launch_assemble(c->d_model, c->ns, c->g, q, dtau, theta, dt, op, c->flags, st);
+  c->assembled_scheme = scheme;
+  return cuda_check(c, e, "assemble");
+}
+
+int csb_assemble(csb_ctx* c, const double* q, const double* dtau, int scheme, int offdiag_paper,
+                 double theta, double dt, const double* dOm_in, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  return assemble_impl(c, q, dtau, scheme, offdiag_paper, theta, dt, dOm_in, false, S(stream));
+}
+
+int csb_operator_field(csb_ctx* c, const double* q, int which, double* dst, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  if (c->assembled_scheme < 0) return fail(c, CSB_E_STATE, "no operator assembled");
+  cudaStream_t st = S(stream);
+  const long long N = c->g.N;
+  const int ns = c->ns;
+  cudaError_t e = cudaSuccess;
+  auto cp = [&](const double* src, size_t n) {
+    return cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  };
+  if (which <= 3) {
+    e = launch_export_op(c->d_model, ns, c->g, c->op, q, which, dst, st);
+  } else if (which == 4) {
+    e = cp(c->op.d, N);
+  } else if (which == 5) {
+    if (c->op.dsp_per_species) e = cp(c->op.dsp, (size_t)ns * N);
+    else
+      for (int s = 0; s < ns && e == cudaSuccess; ++s)
+        e = cudaMemcpyAsync(dst + (size_t)s * N, c->op.dsp, N * sizeof(double),
+                            cudaMemcpyDeviceToDevice, st);
+  } else if (which >= 6 && which <= 8) {
+    e = cp(c->op.lam[which - 6], c->g.NF[which - 6]);
+  } else if (which >= 9 && which <= 11) {
+    e = cp(c->op.lamsp[which - 9], c->g.NF[which - 9]);
+  } else if (which == 12) {
+    if (!c->op.dinv || !(c->op.chem && c->op.mode == SCH_CI))
+      return fail(c, CSB_E_STATE, "no CI species block inverse");
+    e = cp(c->op.dinv, (size_t)ns * ns * N);
+  } else if (which == 13) {
+    if (!c->op.dom_full) return fail(c, CSB_E_STATE, "full dOmega not stored");
+    e = cp(c->op.dom, (size_t)ns * ns * N);
+  } else {
+    return fail(c, CSB_E_BADARG, "unknown operator field");
+  }
+  return cuda_check(c, e, "operator field");
+}
+
+int csb_lusgs(csb_ctx* c, const double* rhs, double* dq, double* dq_star, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  if (c->assembled_scheme < 0) return fail(c, CSB_E_STATE, "no operator assembled");
+  cudaStream_t st = S(stream);
+  cudaError_t e = cudaMemsetAsync(dq, 0, sizeof(double) * (5 + c->ns) * c->g.N, st);
+  c->op.neg_rhs = 0;
+  if (e == cudaSuccess)
+    e = launch_sweeps(c->d_model, c->ns, c->g, c->op, rhs, dq, dq_star, c->flags, st);
+  return cuda_check(c, e, "lusgs");
+}
+
+int csb_apply_update(csb_ctx* c, long long N, const double* q, const double* dq, int scheme,
+                     double* q_new, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  return cuda_check(c, launch_update(c->d_model, c->ns, with_n(c, N), scheme, q, dq, q_new, c->flags,
+                                     S(stream)),
+                    "apply update");
+}
+
+int csb_correct(csb_ctx* c, int mode, long long rows, int ns, const double* rho_s,
+                const double* d_rho_s, const double* d_rho, double* out, void* stream) {
+  if (!c || !c->has_ws) return fail(c, CSB_E_STATE, "workspace (flags) not set");
+  if (mode != 1 && mode != 2) return fail(c, CSB_E_BADARG, "mode must be 1 (CS1) or 2 (CS2)");
+  return cuda_check(c, launch_correct(mode, rows, ns, rho_s, d_rho_s, d_rho, out, c->flags, S(stream)),
+                    "correct");
+}
+
+int csb_residual_norms(csb_ctx* c, long long N, const double* R, double* out3, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  return cuda_check(c, launch_norms(c->ns, N > 0 ? N : c->g.N, R, c->partial, out3, S(stream)),
+                    "norms");
+}
+
+static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cfl, int scheme,
+                         int offdiag_paper, const double* dOm_in, double* q_new, cudaStream_t st) {
+  const bool chem = mech_of(c).nrx > 0;
+  const bool full = chem && scheme == SCH_CI;
+  if (full && !c->ws_block) return fail(c, CSB_E_STATE, "CI with chemistry needs block workspace");
+  int r = time_step_impl(c, q, cfl, dOm_in, c->dtau, full, st);
+  if (r) return r;
+  OpDev& op = c->op;
+  op.dom_full = full ? 1 : 0;
+  r = assemble_impl(c, q, c->dtau, scheme, offdiag_paper, 0.0, 0.0, dOm_in, true, st);
+  if (r) return r;
+  // rhs = -R: the sweeps negate on load (exact)
+  cudaError_t e = cudaMemsetAsync(c->dq, 0, sizeof(double) * (5 + c->ns) * c->g.N, st);
+  op.neg_rhs = 1;
+  if (e == cudaSuccess) e = launch_sweeps(c->d_model, c->ns, c->g, op, R, c->dq, nullptr, c->flags, st);
+  op.neg_rhs = 0;
+  if (e == cudaSuccess) e = launch_update(c->d_model, c->ns, c->g, scheme, q, c->dq, q_new, c->flags, st);
+  return cuda_check(c, e, "implicit step");
+}
+
+int csb_implicit_step(csb_ctx* c, const double* q, const double* R, double cfl, int scheme,
+                      int offdiag_paper, const double* dOm_in, double* q_new, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  return implicit_impl(c, q, R, cfl, scheme, offdiag_paper, dOm_in, q_new, S(stream));
+}
+
+int csb_iteration(csb_ctx* c, const double* q, double cfl, int scheme, int offdiag_paper,
+                  int first_order, double* q_new, double* R_out, double* norms3, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  if ((r = check_bcs(c))) return r;
+  if ((r = sync_fs(c))) return r;
+  cudaStream_t st = S(stream);
+  double* R = R_out ? R_out : c->R;
+  cudaError_t e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
+                                  use_k2d(c), c->flags, st);
+  if (e == cudaSuccess) e = launch_norms(c->ns, c->g.N, R, c->partial, norms3 ? norms3 : c->norms, st);
+  if (e != cudaSuccess) return cuda_check(c, e, "iteration residual");
+  return implicit_impl(c, q, R, cfl, scheme, offdiag_paper, nullptr, q_new, st);
+}
+
+int csb_transpose(long long N, int nv, const double* src, double* dst, int to_soa, void* stream) {
+  return launch_transpose(N, nv, src, dst, to_soa, S(stream)) == cudaSuccess ? CSB_OK : CSB_E_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,253 @@
+// csflow-b200: shared device types and closures (sm_100a, FP64).
+//
+// Layout contract (see include/csflow_b200.h): every cell field is SoA,
+// component-major, cell index c = (i*nj + j)*nk + k (the reference's C order
+// with the component axis moved to the front).  Face arrays of direction d are
+// SoA over the face-shaped grid (n_d + 1 along axis d).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define CSB_DEV __device__ __forceinline__
+
+namespace csb {
+
+constexpr int MAXNS = 64;
+constexpr int NG = 2;  // ghost layers (reference fields.py:14)
+constexpr double R_U = 8.314462618;  // mixture.py:26
+constexpr double EPS_NEG = 1e-10;    // mixture.py:30
+
+// Error bits of the device flag word.  The host maps them onto the
+// reference's exception classes in pipeline order (csflow_b200.h).
+enum ErrBit : int {
+  EB_DECODE = 0,       // cons_to_prim on the input state (NonPhysicalState)
+  EB_FACE_T = 1,       // face temperature <= 0 (spatial.py:54-55)
+  EB_RES_NONFINITE = 2,// non-finite residual (spatial.py:269-271)
+  EB_ZERO_WAVE = 3,    // local_time_step denominator <= 0 (implicit.py:42-43)
+  EB_SINGULAR = 4,     // _check_diag / lusgs underflow (implicit.py:406-408)
+  EB_GATE = 5,         // post-update admissibility (driver.py:223-224, 250; implicit.py:138-141)
+  EB_KSKIP = 6,        // 2-D fast-path precondition violated (internal)
+  EB_BLOCK = 7,        // CI species block not invertible (implicit.py:365-368)
+  EB_GATE_DECODE = 8,  // post-update cons_to_prim gate (driver.py:250)
+  EB_COUNT = 9
+};
+// flag buffer layout (unsigned long long): [0] bits, [1+b] first cell of bit b,
+// [15] gate-failure count
+constexpr int FLAG_WORDS = 16;
+constexpr int FLAG_GATE_COUNT = 15;
+
+struct Model {
+  int ns;
+  double Pr, Sc;
+  double M[MAXNS], cp[MAXNS], Rs[MAXNS], bs[MAXNS];
+  double mu_ref[MAXNS], T_mu[MAXNS], S_mu[MAXNS], TS[MAXNS];  // TS = T_mu + S_mu
+};
+
+// Reactions in the reference's order; stoichiometry kept as (species, nu)
+// pairs in ascending species order (chemistry.py:56-62 iterates np.nonzero).
+constexpr int MAXTERM = 6;
+struct Reaction {
+  double Af, bf, Eaf, Ab, bb, Eab;
+  int has_back;
+  int nr, np;
+  int rs[MAXTERM], ps[MAXTERM];
+  double rn[MAXTERM], pn[MAXTERM];
+  int nd;                       // species with nonzero (nu'' - nu')
+  int ds[2 * MAXTERM];
+  double dn[2 * MAXTERM];
+};
+
+struct Mech {
+  int nrx;  // 0 = frozen
+  const Reaction* rx;
+};
+
+struct GridDev {
+  int ni, nj, nk;
+  long long N;
+  const double* S[3];   // SoA face vectors, S[d][x*NF_d + f]
+  long long NF[3];
+  const double* vol;
+};
+
+enum BcKind : int { BC_FARFIELD = 0, BC_OUTFLOW = 1, BC_WALL = 2, BC_SYMMETRY = 3, BC_PERIODIC = 4 };
+
+struct BCDev {
+  int kind[6];
+  int axis[6];
+  double Tw[6];
+  const double* fs;  // [6][nc] padded-layout freestream vectors (device)
+};
+
+CSB_DEV long long cell_index(const GridDev& g, int i, int j, int k) {
+  return ((long long)i * g.nj + j) * g.nk + k;
+}
+
+CSB_DEV long long face_index(const GridDev& g, int d, int i, int j, int k) {
+  // (i, j, k) with index d ranging over [0, n_d]
+  if (d == 0) return ((long long)i * g.nj + j) * g.nk + k;
+  if (d == 1) return ((long long)i * (g.nj + 1) + j) * g.nk + k;
+  return ((long long)i * g.nj + j) * (g.nk + 1) + k;
+}
+
+CSB_DEV void load_S(const GridDev& g, int d, long long f, double S[3]) {
+  const double* p = g.S[d];
+  const long long nf = g.NF[d];
+  S[0] = __ldg(p + f);
+  S[1] = __ldg(p + nf + f);
+  S[2] = __ldg(p + 2 * nf + f);
+}
+
+// numpy.maximum: NaN-propagating
+CSB_DEV double npmax(double a, double b) {
+  if (a != a) return a;
+  if (b != b) return b;
+  return a > b ? a : (b > a ? b : a);
+}
+
+// minmod with numpy's np.where semantics (spatial.py:22-27): a NaN operand
+// fails both comparisons, exactly as in the reference.
+CSB_DEV double minmod(double a, double b) {
+  double out = (fabs(a) < fabs(b)) ? a : b;
+  return (a * b <= 0.0) ? 0.0 : out;
+}
+
+CSB_DEV bool finite(double x) { return isfinite(x); }
+
+CSB_DEV void raise_flag(unsigned long long* fl, int bit, long long cell) {
+  atomicOr(fl, 1ull << bit);
+  atomicMin(fl + 1 + bit, (unsigned long long)cell);
+}
+
+// Sutherland viscosity of species s (mixture.py:368); (T/T_mu)^1.5 as x*sqrt(x)
+CSB_DEV double mu_species(const Model& m, int s, double T) {
+  const double x = T / m.T_mu[s];
+  return m.mu_ref[s] * (x * sqrt(x)) * m.TS[s] / (T + m.S_mu[s]);
+}
+
+// Decoded cell state (mixture.py:287-307 cons_to_prim with clipping).
+template <int NSB>
+struct Cell {
+  double rho, u[3], p, T, Y[NSB], c, gamma, h, Ek, R, cp;
+};
+
+// Decode conservative vector q[c*stride] into primitives.  Returns false on
+// the reference's NonPhysicalState conditions (rho, Y < -eps, T).
+template <int NSB>
+CSB_DEV bool decode(const Model& m, const double* __restrict__ q, long long stride, Cell<NSB>& o) {
+  const int ns = m.ns;
+  const double rho = q[0];
+  bool ok = (rho > 0.0) && finite(rho);
+  const double ir = rho;
+  o.rho = rho;
+#pragma unroll
+  for (int x = 0; x < 3; ++x) o.u[x] = q[(1 + x) * stride] / ir;
+  double sum = 0.0;
+#pragma unroll
+  for (int s = 0; s < NSB; ++s) {
+    if (s < ns) {
+      double y = q[(5 + s) * stride] / ir;
+      if (y < -EPS_NEG) ok = false;
+      if (y < 0.0) y = 0.0;
+      o.Y[s] = y;
+      sum += y;
+    } else {
+      o.Y[s] = 0.0;
+    }
+  }
+  double R = 0.0, cp = 0.0, yb = 0.0;
+#pragma unroll
+  for (int s = 0; s < NSB; ++s) {
+    if (s < ns) {
+      const double y = o.Y[s] / sum;
+      o.Y[s] = y;
+      R += y * m.Rs[s];
+      cp += y * m.cp[s];
+      yb += y * m.bs[s];
+    }
+  }
+  o.Ek = 0.5 * ((o.u[0] * o.u[0] + o.u[1] * o.u[1]) + o.u[2] * o.u[2]);
+  const double cv = cp - R;
+  const double e_int = q[4 * stride] / rho - o.Ek;
+  o.T = (e_int - yb) / cv;
+  if (!(o.T > 0.0) || !finite(o.T)) ok = false;
+  o.R = R;
+  o.cp = cp;
+  o.p = rho * R * o.T;
+  o.gamma = cp / cv;
+  o.c = sqrt(o.gamma * R * o.T);
+  o.h = yb + cp * o.T + o.Ek;
+  return ok;
+}
+
+// Transport (mixture.py:354-372): mu, k, D (D identical for all species).
+template <int NSB>
+CSB_DEV void transport(const Model& m, double T, const double* Y, double rho, double& mu, double& k,
+                       double& D) {
+  double acc = 0.0, cp = 0.0;
+#pragma unroll
+  for (int s = 0; s < NSB; ++s) {
+    if (s < m.ns) {
+      acc += Y[s] * mu_species(m, s, T);
+      cp += Y[s] * m.cp[s];
+    }
+  }
+  mu = acc;
+  k = mu * cp / m.Pr;
+  D = mu / (rho * m.Sc);
+}
+
+// Diffusivities (implicit.py:144-149).
+CSB_DEV void diffusivities(double mu, double k, double D, double rho, double cv, double& nf,
+                           double& nsp, double& nu) {
+  nf = npmax(4.0 * mu / (3.0 * rho), k / (rho * cv));
+  nsp = D;
+  nu = npmax(nf, nsp);
+}
+
+// Deterministic block reduction helper (sum of doubles over a CTA).
+template <int NT>
+CSB_DEV double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NT / 32; ++i) r += sh[i];
+  }
+  return r;
+}
+
+// ns bucket dispatch: NSB is the compile-time register-array bound.  The
+// templated kernels are instantiated once per bucket in separate translation
+// units (csb_bucket.cu compiled with -DCSB_BUCKET=<b>); their launchers are
+// named <name>_b<b> there (CSB_BK) and routed by csb_dispatch.cu.
+#define CSB_BUCKET_LIST(X) X(2) X(4) X(6) X(8) X(12) X(16) X(24) X(32) X(48) X(64)
+#define CSB_CAT2(a, b) a##_b##b
+#define CSB_CAT(a, b) CSB_CAT2(a, b)
+#ifdef CSB_BUCKET
+#define CSB_BK(name) CSB_CAT(name, CSB_BUCKET)
+#define CSB_NS_DISPATCH(ns, ...)            \
+  do {                                      \
+    (void)(ns);                             \
+    constexpr int NSB = CSB_BUCKET;         \
+    __VA_ARGS__;                            \
+  } while (0)
+#endif
+
+static inline int bucket_of(int ns) {
+  return ns <= 2 ? 2 : ns <= 4 ? 4 : ns <= 6 ? 6 : ns <= 8 ? 8 : ns <= 12 ? 12 : ns <= 16 ? 16
+       : ns <= 24 ? 24 : ns <= 32 ? 32 : ns <= 48 ? 48 : 64;
+}
+
+static inline int grid_for(long long n, int bs) {
+  long long b = (n + bs - 1) / bs;
+  if (b < 1) b = 1;
+  if (b > 148LL * 32) b = 148LL * 32;
+  return (int)b;
+}
+
+}  // namespace csb

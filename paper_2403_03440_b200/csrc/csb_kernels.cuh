@@ -1,0 +1,81 @@
+// csflow-b200: internal launcher declarations shared by the .cu files.
+#pragma once
+
+#include <algorithm>
+
+#include "csb_common.cuh"
+
+namespace csb {
+
+// per-cell operator state written by the assembly, read by the sweeps
+enum StIdx : int {
+  ST_RHO = 0, ST_U0 = 1, ST_U1 = 2, ST_U2 = 3, ST_H = 4, ST_BETA = 5, ST_EK = 6,
+  ST_C = 7, ST_NF = 8, ST_NSP = 9, ST_NU = 10, ST_T = 11, NST = 12
+};
+
+enum Scheme : int { SCH_CI = 0, SCH_CS1 = 1, SCH_CS2 = 2 };
+
+struct OpDev {
+  int mode;            // Scheme
+  double sp_scale;     // 0.5 symmetrized, 1.0 paper (implicit.py:385)
+  int chem;            // chemistry contributes to the diagonal
+  int dsp_per_species; // d_sp stored per species (chemistry) or once per cell
+  double* st;          // [NST][N]
+  double* Y;           // [ns][N] decoded mass fractions (CI sweeps: w, b species rows)
+  double* d;           // [N] d_flow (CS) or d_scal (CI)
+  double* dsp;         // [ns or 1][N] CS species diagonal
+  double* dinv_sp;     // [ns or 1][N] 1/d_sp
+  double* lam[3];      // face radii (CS flow / CI unified), face-shaped SoA
+  double* lamsp[3];    // CS species face radii
+  double* dom;         // [ns*ns][N] dOmega (full) or [ns][N] diagonal only (CS)
+  int dom_full;
+  double* lamS;        // [N] source spectral radius
+  double* dinv;        // [ns*ns][N] CI species block inverse
+  int neg_rhs;         // sweeps use rhs = -input (the residual R)
+};
+
+cudaError_t launch_residual(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
+                            const Mech& mech, const double* q, double* R, int first_order, bool k2d,
+                            unsigned long long* flags, cudaStream_t st);
+cudaError_t launch_padded(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
+                          const double* q, double* P, unsigned long long* flags, cudaStream_t st);
+
+cudaError_t launch_decode(const Model* mp, int ns, const GridDev& g, const double* q, double* out,
+                          unsigned long long* flags, cudaStream_t st);
+cudaError_t launch_source_jacobian(const Model* mp, int ns, const GridDev& g, const Mech& mech,
+                                   const double* q, double* dom, int dom_full, double* lamS,
+                                   const double* dom_in, unsigned long long* flags, cudaStream_t st);
+cudaError_t launch_production(const Model* mp, int ns, const GridDev& g, const Mech& mech,
+                              const double* q, double* om, unsigned long long* flags,
+                              cudaStream_t st);
+cudaError_t launch_time_step(const Model* mp, int ns, const GridDev& g, const double* q, double cfl,
+                             const double* lamS, double* dtau, double* lam_inv, double* lam_vis,
+                             unsigned long long* flags, cudaStream_t st);
+cudaError_t launch_assemble(const Model* mp, int ns, const GridDev& g, const double* q,
+                            const double* dtau, double theta, double dt, OpDev& op,
+                            unsigned long long* flags, cudaStream_t st);
+cudaError_t launch_assemble_cell(const Model* mp, int ns, const GridDev& g, const double* q,
+                                 const double* dtau, double theta, double dt, OpDev& op,
+                                 unsigned long long* flags, cudaStream_t st);
+cudaError_t launch_sweeps_generic(const Model* mdl, int ns, const GridDev& g, const OpDev& op,
+                                  const double* rhs, double* dq, double* dq_star, cudaStream_t st);
+cudaError_t launch_sweeps(const Model* mdl, int ns, const GridDev& g, const OpDev& op,
+                          const double* rhs, double* dq, double* dq_star, unsigned long long* flags,
+                          cudaStream_t st);
+cudaError_t launch_update(const Model* mp, int ns, const GridDev& g, int scheme, const double* q,
+                          const double* dq, double* qn, unsigned long long* flags, cudaStream_t st);
+cudaError_t launch_norms(int ns, long long N, const double* R, double* partial, double* out,
+                         cudaStream_t st);
+cudaError_t launch_correct(int mode, long long rows, int ns, const double* rs, const double* drs,
+                           const double* drho, double* out, unsigned long long* flags,
+                           cudaStream_t st);
+cudaError_t launch_transpose(long long N, int nv, const double* src, double* dst, int to_soa,
+                             cudaStream_t st);
+cudaError_t launch_export_op(const Model* mdl, int ns, const GridDev& g, const OpDev& op,
+                             const double* q, int what, double* dst, cudaStream_t st);
+cudaError_t launch_dtau_arrays(long long N, const double* li, const double* lv, const double* lS,
+                               double lS_scalar, double cfl, const double* J, double* dtau,
+                               unsigned long long* flags, cudaStream_t st);
+cudaError_t launch_check_2d(const GridDev& g, int* ok, cudaStream_t st);
+
+}  // namespace csb

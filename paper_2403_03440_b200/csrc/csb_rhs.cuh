@@ -1,0 +1,681 @@
+// csflow-b200: explicit residual R (V dQ/dt = -R), reference spatial.py:207-274.
+//
+// One CTA owns a TI x TJ x TK tile of cells.  It stages the decoded
+// primitives of the tile plus a 2-cell halo in shared memory (SoA, one
+// plane per component), evaluating boundary ghosts on the fly with the
+// reference's face-by-face fill order (boundary.py:53-114, see ghost_value),
+// then computes each face flux of the tile exactly once per direction
+// (MUSCL-minmod + Rusanov + central viscous, spatial.py:217-256) into a
+// shared flux buffer and differences it into R in direction order 0, 1, 2.
+//
+// K2D: nk == 1 with a k-boundary pair whose k-face fluxes and k tangential
+// differences cancel bit-exactly (outflow/outflow, periodic/periodic, or
+// symmetry/symmetry with w == 0).  The k layers are then neither
+// staged nor evaluated.  Any cell with w != 0 under symmetry raises
+// EB_KSKIP so the host can recompute with the general path.
+#pragma once
+#include "csb_common.cuh"
+#include "csb_kernels.cuh"
+
+namespace csb {
+
+// ----------------------------------------------------------------------------
+// ghost evaluation
+// ----------------------------------------------------------------------------
+
+// last fill op (index a*4 + side*2 + g-1, the reference's loop order) with
+// index < t that writes padded cell p; -1 if none.
+CSB_DEV int last_op(const int p[3], const int n[3], int t) {
+  int best = -1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    int side, g;
+    if (p[a] < NG) {
+      side = 0;
+      g = NG - p[a];
+    } else if (p[a] >= n[a] + NG) {
+      side = 1;
+      g = p[a] - (n[a] + NG) + 1;
+    } else {
+      continue;
+    }
+    const int o = a * 4 + side * 2 + (g - 1);
+    if (o < t && o > best) best = o;
+  }
+  return best;
+}
+
+// Value of padded cell (pi, pj, pk) after the full ghost fill, as the
+// composition of the per-face formulas applied to one interior source cell
+// (or the freestream, or NaN for a ghost the reference never fills).
+// out[0..nc) in padded layout [rho, u, v, w, p, Y.., T].
+template <int NSB>
+CSB_DEV void padded_value(const Model& m, const GridDev& g, const BCDev& bc,
+                          const double* __restrict__ q, int pi, int pj, int pk, double* out,
+                          unsigned long long* flags) {
+  const int ns = m.ns;
+  const int nc = 6 + ns;
+  int p[3] = {pi, pj, pk};
+  const int n[3] = {g.ni, g.nj, g.nk};
+  int op_list[12];
+  int op_pos[12][3];
+  int nops = 0;
+  int t = 12;
+  int base_kind = 0;  // 0 interior decode, 1 NaN, 2 farfield of face base_face
+  int base_face = 0;
+  while (true) {
+    const int o = last_op(p, n, t);
+    if (o < 0) break;
+    const int a = o >> 2, side = (o >> 1) & 1, gg = (o & 1) + 1;
+    const int face = a * 2 + side;
+    const int kind = bc.kind[face];
+    if (kind == BC_FARFIELD) {
+      base_kind = 2;
+      base_face = face;
+      break;
+    }
+    if (kind == BC_WALL || kind == BC_SYMMETRY) {
+      op_list[nops] = o;
+      op_pos[nops][0] = p[0];
+      op_pos[nops][1] = p[1];
+      op_pos[nops][2] = p[2];
+      ++nops;
+    }
+    int src;
+    if (kind == BC_OUTFLOW) src = side == 0 ? NG : n[a] + NG - 1;
+    else if (kind == BC_PERIODIC) src = side == 0 ? NG + n[a] - gg : NG + gg - 1;
+    else src = side == 0 ? NG + gg - 1 : NG + n[a] - gg;
+    p[a] = src;
+    t = o;
+  }
+  if (base_kind == 0) {
+    const bool interior = p[0] >= NG && p[0] < n[0] + NG && p[1] >= NG && p[1] < n[1] + NG &&
+                          p[2] >= NG && p[2] < n[2] + NG;
+    if (!interior) base_kind = 1;
+  }
+  if (base_kind == 1) {
+    for (int c = 0; c < nc; ++c) out[c] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  if (base_kind == 2) {
+    const double* fs = bc.fs + (long long)base_face * nc;
+    for (int c = 0; c < nc; ++c) out[c] = __ldg(fs + c);
+  } else {
+    const long long cell = cell_index(g, p[0] - NG, p[1] - NG, p[2] - NG);
+    Cell<NSB> cs;
+    if (!decode<NSB>(m, q + cell, g.N, cs)) raise_flag(flags, EB_DECODE, cell);
+    out[0] = cs.rho;
+    out[1] = cs.u[0];
+    out[2] = cs.u[1];
+    out[3] = cs.u[2];
+    out[4] = cs.p;
+#pragma unroll
+    for (int s = 0; s < NSB; ++s)
+      if (s < ns) out[5 + s] = cs.Y[s];
+    out[5 + ns] = cs.T;
+  }
+  // apply the recorded transforms innermost first
+  for (int r = nops - 1; r >= 0; --r) {
+    const int o = op_list[r];
+    const int a = o >> 2, side = (o >> 1) & 1;
+    const int face = a * 2 + side;
+    if (bc.kind[face] == BC_WALL) {
+      const double Tw = bc.Tw[face];
+      out[1] = -out[1];
+      out[2] = -out[2];
+      out[3] = -out[3];
+      const double Tg = npmax(2.0 * Tw - out[5 + ns], 0.1 * Tw);
+      double R = 0.0;
+      for (int s = 0; s < ns; ++s) R += out[5 + s] * m.Rs[s];
+      out[5 + ns] = Tg;
+      out[0] = out[4] / (R * Tg);
+    } else {  // symmetry
+      double nh[3];
+      if (bc.axis[face] >= 0) {
+        nh[0] = nh[1] = nh[2] = 0.0;
+        nh[bc.axis[face]] = 1.0;
+      } else {
+        int t3[3];
+        for (int x = 0; x < 3; ++x) {
+          int v = op_pos[r][x] - NG;
+          v = v < 0 ? 0 : (v > n[x] - 1 ? n[x] - 1 : v);
+          t3[x] = v;
+        }
+        t3[a] = side == 0 ? 0 : n[a];
+        double S[3];
+        load_S(g, a, face_index(g, a, t3[0], t3[1], t3[2]), S);
+        const double nrm = sqrt((S[0] * S[0] + S[1] * S[1]) + S[2] * S[2]);
+        nh[0] = S[0] / nrm;
+        nh[1] = S[1] / nrm;
+        nh[2] = S[2] / nrm;
+      }
+      const double un = (out[1] * nh[0] + out[2] * nh[1]) + out[3] * nh[2];
+      const double tu = 2.0 * un;
+      out[1] = out[1] - tu * nh[0];
+      out[2] = out[2] - tu * nh[1];
+      out[3] = out[3] - tu * nh[2];
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// face flux
+// ----------------------------------------------------------------------------
+
+struct FaceGeom {
+  double S[3];
+  double xn[3];      // S / Vf
+  double xt[2][3];   // face-averaged Sc_a * J for the two tangential axes (ascending)
+  int ta[2];         // tangential axis ids
+  int use_t[2];      // 0: skip (K2D k axis)
+};
+
+// Face state from W = [rho, u, p, Y] (spatial.py:42-66); returns false if
+// the face temperature is non-positive or non-finite.
+template <int NSB>
+CSB_DEV bool face_state(const Model& m, const double* W, double& T, double& c, double& et) {
+  double R = 0.0, cp = 0.0, yb = 0.0;
+#pragma unroll
+  for (int s = 0; s < NSB; ++s) {
+    if (s < m.ns) {
+      R += W[5 + s] * m.Rs[s];
+      cp += W[5 + s] * m.cp[s];
+      yb += W[5 + s] * m.bs[s];
+    }
+  }
+  T = W[4] / (W[0] * R);
+  const bool ok = (T > 0.0) && finite(T);
+  const double gamma = cp / (cp - R);
+  c = sqrt(gamma * R * T);
+  const double Ek = 0.5 * ((W[1] * W[1] + W[2] * W[2]) + W[3] * W[3]);
+  et = yb + (cp - R) * T + Ek;
+  return ok;
+}
+
+// Total flux through one face into F[c*ldF] (c < nv).  sP: staged padded
+// primitives, component plane stride ldP; cell offsets im/ip (the two
+// adjacent cells), imm/ipp (MUSCL outer cells), tangential strides st[2].
+template <int NSB>
+CSB_DEV bool face_flux(const Model& m, const double* sP, int ldP, int imm, int im, int ip, int ipp,
+                       const int st[2], const FaceGeom& fg, bool first_order, double* F, int ldF) {
+  const int ns = m.ns;
+  const int nv = 5 + ns;
+  bool ok = true;
+  // ---------------- convective part (Rusanov on MUSCL states)
+  {
+    double WL[5 + NSB], WR[5 + NSB];
+#pragma unroll
+    for (int c = 0; c < 5 + NSB; ++c) {
+      if (c < nv) {
+        const double vm = sP[c * ldP + im];
+        const double vp = sP[c * ldP + ip];
+        if (first_order) {
+          WL[c] = vm;
+          WR[c] = vp;
+        } else {
+          const double vmm = sP[c * ldP + imm];
+          const double vpp = sP[c * ldP + ipp];
+          const double dc = vp - vm;
+          WL[c] = vm + 0.5 * minmod(vm - vmm, dc);
+          WR[c] = vp - 0.5 * minmod(dc, vpp - vp);
+        }
+      }
+    }
+    double TL, cL, eL, TR, cR, eR;
+    ok &= face_state<NSB>(m, WL, TL, cL, eL);
+    ok &= face_state<NSB>(m, WR, TR, cR, eR);
+    const double* S = fg.S;
+    const double UL = WL[1] * S[0] + WL[2] * S[1] + WL[3] * S[2];
+    const double UR = WR[1] * S[0] + WR[2] * S[1] + WR[3] * S[2];
+    const double area = sqrt((S[0] * S[0] + S[1] * S[1]) + S[2] * S[2]);
+    const double lam = npmax(fabs(UL) + cL * area, fabs(UR) + cR * area);
+    const double hl = 0.5 * lam;
+    // c = 0
+    {
+      const double qL = WL[0], qR = WR[0];
+      F[0] = 0.5 * (UL * qL + UR * qR) - hl * (qR - qL);
+    }
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      const double qL = WL[0] * WL[1 + x], qR = WR[0] * WR[1 + x];
+      const double fl = UL * qL + WL[4] * S[x];
+      const double fr = UR * qR + WR[4] * S[x];
+      F[(1 + x) * ldF] = 0.5 * (fl + fr) - hl * (qR - qL);
+    }
+    {
+      const double qL = WL[0] * eL, qR = WR[0] * eR;
+      const double fl = UL * qL + WL[4] * UL;
+      const double fr = UR * qR + WR[4] * UR;
+      F[4 * ldF] = 0.5 * (fl + fr) - hl * (qR - qL);
+    }
+#pragma unroll
+    for (int s = 0; s < NSB; ++s) {
+      if (s < ns) {
+        const double qL = WL[0] * WL[5 + s], qR = WR[0] * WR[5 + s];
+        F[(5 + s) * ldF] = 0.5 * (UL * qL + UR * qR) - hl * (qR - qL);
+      }
+    }
+  }
+  // ---------------- viscous part (spatial.py:227-256, viscous_flux 143-168)
+  {
+    const int iT = 5 + ns;
+    double Wf[5 + NSB];
+#pragma unroll
+    for (int c = 0; c < 5 + NSB; ++c)
+      if (c < nv) Wf[c] = 0.5 * (sP[c * ldP + im] + sP[c * ldP + ip]);
+    double Tf, cf, ef;
+    ok &= face_state<NSB>(m, Wf, Tf, cf, ef);
+    const double rho = Wf[0];
+    double mu, kc, D;
+    transport<NSB>(m, Tf, Wf + 5, rho, mu, kc, D);
+    // gradient of component c, in the reference's summation order
+    // grad = grads[0] + grads[1] + grads[2] with grads[d] the normal part.
+    auto grad = [&](int c, double g[3]) {
+      const double dn = sP[c * ldP + ip] - sP[c * ldP + im];
+      double part[3][3];
+      int filled[3] = {0, 0, 0};
+      // normal direction: axis id is the one not in ta
+      int d = 3 - fg.ta[0] - fg.ta[1];
+#pragma unroll
+      for (int x = 0; x < 3; ++x) part[d][x] = dn * fg.xn[x];
+      filled[d] = 1;
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int a = fg.ta[t];
+        if (fg.use_t[t]) {
+          const int s = st[t];
+          const double cdm = 0.5 * (sP[c * ldP + im + s] - sP[c * ldP + im - s]);
+          const double cdp = 0.5 * (sP[c * ldP + ip + s] - sP[c * ldP + ip - s]);
+          const double dP = 0.5 * (cdm + cdp);
+#pragma unroll
+          for (int x = 0; x < 3; ++x) part[a][x] = dP * fg.xt[t][x];
+          filled[a] = 1;
+        }
+      }
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        double v = filled[0] ? part[0][x] : 0.0;
+        v = filled[1] ? (filled[0] ? v + part[1][x] : part[1][x]) : v;
+        v = filled[2] ? ((filled[0] || filled[1]) ? v + part[2][x] : part[2][x]) : v;
+        g[x] = v;
+      }
+    };
+    double gu[3][3], gT[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) grad(1 + i, gu[i]);
+    grad(iT, gT);
+    const double div = (gu[0][0] + gu[1][1]) + gu[2][2];
+    const double tdiv = 2.0 / 3.0 * mu * div;
+    double tS[3];
+    const double* S = fg.S;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        double tau = mu * (gu[i][x] + gu[x][i]);
+        if (x == i) tau -= tdiv;
+        acc = (x == 0) ? tau * S[0] : acc + tau * S[x];
+      }
+      tS[i] = acc;
+    }
+    // species diffusion with zero-sum correction
+    double js[NSB][3];
+    double jsum[3] = {0.0, 0.0, 0.0};
+    const double nrd = -(rho * D);
+#pragma unroll
+    for (int s = 0; s < NSB; ++s) {
+      if (s < ns) {
+        double gy[3];
+        grad(5 + s, gy);
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+          js[s][x] = nrd * gy[x];
+          jsum[x] += js[s][x];
+        }
+      }
+    }
+    double qv[3];
+    double hsj[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int s = 0; s < NSB; ++s) {
+      if (s < ns) {
+        const double hs = m.bs[s] + m.cp[s] * Tf;
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+          js[s][x] -= Wf[5 + s] * jsum[x];
+          hsj[x] += hs * js[s][x];
+        }
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < 3; ++x) qv[x] = -kc * gT[x] + hsj[x];
+    F[1 * ldF] += -tS[0];
+    F[2 * ldF] += -tS[1];
+    F[3 * ldF] += -tS[2];
+    const double utS = (Wf[1] * tS[0] + Wf[2] * tS[1]) + Wf[3] * tS[2];
+    const double qS = (qv[0] * S[0] + qv[1] * S[1]) + qv[2] * S[2];
+    F[4 * ldF] += -utS + qS;
+#pragma unroll
+    for (int s = 0; s < NSB; ++s)
+      if (s < ns) F[(5 + s) * ldF] += (js[s][0] * S[0] + js[s][1] * S[1]) + js[s][2] * S[2];
+  }
+  return ok;
+}
+
+// Net chemical production of one cell (chemistry.py:46-65).
+template <int NSB>
+CSB_DEV void omega_cell(const Model& m, const Mech& mech, double T, const double* rho_s,
+                        double* om) {
+  const int ns = m.ns;
+  double conc[NSB];
+#pragma unroll
+  for (int s = 0; s < NSB; ++s) {
+    om[s] = 0.0;
+    if (s < ns) conc[s] = rho_s[s] / m.M[s];
+  }
+  for (int r = 0; r < mech.nrx; ++r) {
+    const Reaction& rx = mech.rx[r];
+    double rate = rx.Af * pow(T, rx.bf) * exp(-rx.Eaf / (R_U * T));
+    for (int t = 0; t < rx.nr; ++t) {
+      const double c = conc[rx.rs[t]];
+      const double nu = rx.rn[t];
+      rate = rate * (nu == 1.0 ? c : (nu == 2.0 ? c * c : pow(c, nu)));
+    }
+    if (rx.has_back) {
+      double rb = rx.Ab * pow(T, rx.bb) * exp(-rx.Eab / (R_U * T));
+      for (int t = 0; t < rx.np; ++t) {
+        const double c = conc[rx.ps[t]];
+        const double nu = rx.pn[t];
+        rb = rb * (nu == 1.0 ? c : (nu == 2.0 ? c * c : pow(c, nu)));
+      }
+      rate = rate - rb;
+    }
+    if (!finite(rate)) {
+#pragma unroll
+      for (int s = 0; s < NSB; ++s)
+        if (s < ns) om[s] += 0.0 * rate;
+    }
+    for (int t = 0; t < rx.nd; ++t) om[rx.ds[t]] += rx.dn[t] * rate;
+  }
+#pragma unroll
+  for (int s = 0; s < NSB; ++s)
+    if (s < ns) om[s] = om[s] * m.M[s];
+}
+
+// ----------------------------------------------------------------------------
+// residual kernel
+// ----------------------------------------------------------------------------
+
+template <int NSB, bool K2D>
+__global__ void __launch_bounds__(256) k_residual(const Model* __restrict__ mp, GridDev g, BCDev bc,
+                                                  Mech mech, const double* __restrict__ q,
+                                                  double* __restrict__ R, int first_order, int TI,
+                                                  int TJ, int TK, unsigned long long* flags) {
+  extern __shared__ double smem[];
+  __shared__ Model sm;
+  {
+    const double* src = reinterpret_cast<const double*>(mp);
+    double* dst = reinterpret_cast<double*>(&sm);
+    for (int i = threadIdx.x; i < (int)(sizeof(Model) / sizeof(double)); i += blockDim.x)
+      dst[i] = src[i];
+  }
+  __syncthreads();
+  const Model& m = sm;
+  const int ns = m.ns;
+  const int nc = 6 + ns;
+  const int nv = 5 + ns;
+  const int BX = TI + 2 * NG, BY = TJ + 2 * NG, BZ = K2D ? 1 : TK + 2 * NG;
+  const int ldP = BX * BY * BZ;
+  const int nti = (g.ni + TI - 1) / TI, ntj = (g.nj + TJ - 1) / TJ;
+  int b = blockIdx.x;
+  const int ti = b % nti;
+  b /= nti;
+  const int tj = b % ntj;
+  const int tk = b / ntj;
+  const int i0 = ti * TI, j0 = tj * TJ, k0 = K2D ? 0 : tk * TK;
+  const int ci = min(TI, g.ni - i0), cj = min(TJ, g.nj - j0), ck = K2D ? 1 : min(TK, g.nk - k0);
+  double* sP = smem;
+  const int maxf = max(max((TI + 1) * TJ * TK, TI * (TJ + 1) * TK), TI * TJ * (K2D ? 1 : TK + 1));
+  double* sF = smem + (long long)nc * ldP;
+
+  // ---- stage decoded primitives + halo (padded coordinates = interior + NG)
+  for (int l = threadIdx.x; l < ldP; l += blockDim.x) {
+    const int lz = K2D ? 0 : l % BZ;
+    const int ly = K2D ? l % BY : (l / BZ) % BY;
+    const int lx = K2D ? l / BY : l / (BZ * BY);
+    const int pi = i0 + lx, pj = j0 + ly, pk = K2D ? NG : k0 + lz;
+    double v[6 + NSB];
+    const bool inside_pad = pi < g.ni + 2 * NG && pj < g.nj + 2 * NG && pk < g.nk + 2 * NG;
+    if (!inside_pad) {
+      for (int c = 0; c < nc; ++c) v[c] = 0.0;
+    } else {
+      const bool interior = pi >= NG && pi < g.ni + NG && pj >= NG && pj < g.nj + NG &&
+                            pk >= NG && pk < g.nk + NG;
+      if (interior) {
+        const long long cell = cell_index(g, pi - NG, pj - NG, pk - NG);
+        Cell<NSB> cs;
+        if (!decode<NSB>(m, q + cell, g.N, cs)) raise_flag(flags, EB_DECODE, cell);
+        if (K2D && bc.kind[4] == BC_SYMMETRY && q[cell + 3 * g.N] != 0.0)
+          raise_flag(flags, EB_KSKIP, cell);
+        v[0] = cs.rho;
+        v[1] = cs.u[0];
+        v[2] = cs.u[1];
+        v[3] = cs.u[2];
+        v[4] = cs.p;
+#pragma unroll
+        for (int s = 0; s < NSB; ++s)
+          if (s < ns) v[5 + s] = cs.Y[s];
+        v[5 + ns] = cs.T;
+      } else {
+        padded_value<NSB>(m, g, bc, q, pi, pj, pk, v, flags);
+      }
+    }
+    for (int c = 0; c < nc; ++c) sP[c * ldP + l] = v[c];
+  }
+  __syncthreads();
+
+  auto lidx = [&](int lx, int ly, int lz) { return K2D ? lx * BY + ly : (lx * BY + ly) * BZ + lz; };
+  const int strideX = K2D ? BY : BY * BZ, strideY = K2D ? 1 : BZ, strideZ = 1;
+  const int ndir = K2D ? 2 : 3;
+
+  for (int d = 0; d < ndir; ++d) {
+    // faces of direction d inside the tile: dims (ci+1, cj, ck) etc.
+    const int fx = ci + (d == 0), fy = cj + (d == 1), fz = ck + (d == 2);
+    const int nf = fx * fy * fz;
+    for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+      const int fk = f % fz;
+      const int fj = (f / fz) % fy;
+      const int fi = f / (fz * fy);
+      // local (staged) coordinates of the "p" cell (upper side of the face)
+      int lx = fi + NG, ly = fj + NG, lz = K2D ? 0 : fk + NG;
+      const int sd = d == 0 ? strideX : (d == 1 ? strideY : strideZ);
+      const int ip = lidx(lx, ly, lz);
+      const int im = ip - sd, imm = ip - 2 * sd, ipp = ip + sd;
+      // global face and the two adjacent cells
+      const int gi = i0 + fi, gj = j0 + fj, gk = k0 + fk;
+      FaceGeom fg;
+      const long long fidx = face_index(g, d, gi, gj, gk);
+      load_S(g, d, fidx, fg.S);
+      const int nd = d == 0 ? g.ni : (d == 1 ? g.nj : g.nk);
+      const int pos = d == 0 ? gi : (d == 1 ? gj : gk);
+      int cm[3] = {gi, gj, gk}, cp3[3] = {gi, gj, gk};
+      cm[d] -= 1;
+      const bool hasm = pos > 0, hasp = pos < nd;
+      const long long cellm = hasm ? cell_index(g, cm[0], cm[1], cm[2]) : -1;
+      const long long cellp = hasp ? cell_index(g, cp3[0], cp3[1], cp3[2]) : -1;
+      const double Vm = hasm ? __ldg(g.vol + cellm) : 0.0;
+      const double Vp = hasp ? __ldg(g.vol + cellp) : 0.0;
+      const double Vf = (hasm && hasp) ? 0.5 * (Vp + Vm) : (hasm ? Vm : Vp);
+#pragma unroll
+      for (int x = 0; x < 3; ++x) fg.xn[x] = fg.S[x] / Vf;
+      int st[2];
+      int t = 0;
+      for (int a = 0; a < 3; ++a) {
+        if (a == d) continue;
+        fg.ta[t] = a;
+        fg.use_t[t] = !(K2D && a == 2);
+        st[t] = a == 0 ? strideX : (a == 1 ? strideY : strideZ);
+        if (fg.use_t[t]) {
+          // Sc_a * J at the adjacent cells, face-averaged (spatial.py:241-248)
+          double xc[2][3];
+          for (int side = 0; side < 2; ++side) {
+            const bool has = side == 0 ? hasm : hasp;
+            if (!has) continue;
+            const int* cc = side == 0 ? cm : cp3;
+            double Slo[3], Shi[3];
+            int lo[3] = {cc[0], cc[1], cc[2]};
+            int hi[3] = {cc[0], cc[1], cc[2]};
+            hi[a] += 1;
+            load_S(g, a, face_index(g, a, lo[0], lo[1], lo[2]), Slo);
+            load_S(g, a, face_index(g, a, hi[0], hi[1], hi[2]), Shi);
+            const double J = 1.0 / (side == 0 ? Vm : Vp);
+            for (int x = 0; x < 3; ++x) xc[side][x] = (0.5 * (Slo[x] + Shi[x])) * J;
+          }
+          for (int x = 0; x < 3; ++x)
+            fg.xt[t][x] = (hasm && hasp) ? 0.5 * (xc[1][x] + xc[0][x]) : (hasm ? xc[0][x] : xc[1][x]);
+        }
+        ++t;
+      }
+      if (!face_flux<NSB>(m, sP, ldP, imm, im, ip, ipp, st, fg, first_order != 0, sF + f, maxf))
+        raise_flag(flags, EB_FACE_T, hasp ? cellp : cellm);
+    }
+    __syncthreads();
+    // difference into R (R = 0 + dR_0 + dR_1 + dR_2, spatial.py:258-259)
+    const int ncell = ci * cj * ck;
+    for (int l = threadIdx.x; l < ncell; l += blockDim.x) {
+      const int kk = l % ck, jj = (l / ck) % cj, ii = l / (ck * cj);
+      const long long cell = cell_index(g, i0 + ii, j0 + jj, k0 + kk);
+      int flo, fhi;
+      if (d == 0) {
+        flo = (ii * fy + jj) * fz + kk;
+        fhi = ((ii + 1) * fy + jj) * fz + kk;
+      } else if (d == 1) {
+        flo = (ii * fy + jj) * fz + kk;
+        fhi = (ii * fy + jj + 1) * fz + kk;
+      } else {
+        flo = (ii * fy + jj) * fz + kk;
+        fhi = flo + 1;
+      }
+      for (int c = 0; c < nv; ++c) {
+        const double dR = sF[c * maxf + fhi] - sF[c * maxf + flo];
+        double* r = R + (long long)c * g.N + cell;
+        if (d == 0) *r = dR;
+        else *r = *r + dR;
+      }
+    }
+    __syncthreads();
+  }
+
+  // chemistry source (spatial.py:261-267) and the finite check (269-271)
+  const int ncell = ci * cj * ck;
+  for (int l = threadIdx.x; l < ncell; l += blockDim.x) {
+    const int kk = l % ck, jj = (l / ck) % cj, ii = l / (ck * cj);
+    const long long cell = cell_index(g, i0 + ii, j0 + jj, k0 + kk);
+    if (mech.nrx > 0) {
+      const int ls = lidx(ii + NG, jj + NG, K2D ? 0 : kk + NG);
+      double rs[NSB], om[NSB];
+      const double rho = sP[ls];
+#pragma unroll
+      for (int s = 0; s < NSB; ++s)
+        if (s < ns) rs[s] = rho * sP[(5 + s) * ldP + ls];
+      omega_cell<NSB>(m, mech, sP[(5 + ns) * ldP + ls], rs, om);
+      const double V = __ldg(g.vol + cell);
+#pragma unroll
+      for (int s = 0; s < NSB; ++s)
+        if (s < ns) {
+          double* r = R + (long long)(5 + s) * g.N + cell;
+          *r = *r - om[s] * V;
+        }
+    }
+    bool fin = true;
+    for (int c = 0; c < nv; ++c) fin &= finite(R[(long long)c * g.N + cell]);
+    if (!fin) raise_flag(flags, EB_RES_NONFINITE, cell);
+  }
+}
+
+// Full padded primitive array (API: assemble_residual(return_padded=True)),
+// SoA [nc][(ni+4)(nj+4)(nk+4)].
+template <int NSB>
+__global__ void k_padded(const Model* __restrict__ mp, GridDev g, BCDev bc,
+                         const double* __restrict__ q, double* __restrict__ P,
+                         unsigned long long* flags) {
+  const Model& m = *mp;
+  const int nc = 6 + m.ns;
+  const int PX = g.ni + 2 * NG, PY = g.nj + 2 * NG, PZ = g.nk + 2 * NG;
+  const long long NP = (long long)PX * PY * PZ;
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < NP;
+       l += (long long)gridDim.x * blockDim.x) {
+    const int pk = l % PZ, pj = (l / PZ) % PY, pi = l / ((long long)PZ * PY);
+    double v[6 + NSB];
+    padded_value<NSB>(m, g, bc, q, pi, pj, pk, v, flags);
+    for (int c = 0; c < nc; ++c) P[c * NP + l] = v[c];
+  }
+}
+
+// ----------------------------------------------------------------------------
+// host launchers
+// ----------------------------------------------------------------------------
+
+static inline void pick_tile(int ns, bool k2d, int nk, int& TI, int& TJ, int& TK, size_t& smem) {
+  const int nc = 6 + ns, nv = 5 + ns;
+  const size_t budget = 200 * 1024;
+  if (k2d) {
+    const int cand[][2] = {{15, 16}, {7, 16}, {7, 8}, {3, 8}, {3, 4}, {1, 4}};
+    for (auto& c : cand) {
+      TI = c[0];
+      TJ = c[1];
+      TK = 1;
+      const size_t ldP = (size_t)(TI + 4) * (TJ + 4);
+      const size_t maxf = std::max((size_t)(TI + 1) * TJ, (size_t)TI * (TJ + 1));
+      smem = (ldP * nc + maxf * nv) * sizeof(double);
+      if (smem <= budget) return;
+    }
+  } else {
+    const int cand[][3] = {{6, 8, 4}, {4, 4, 4}, {4, 4, 2}, {2, 4, 2}, {2, 2, 2}, {1, 2, 1}};
+    for (auto& c : cand) {
+      TI = c[0];
+      TJ = c[1];
+      TK = std::min(c[2], nk);
+      const size_t ldP = (size_t)(TI + 4) * (TJ + 4) * (TK + 4);
+      const size_t maxf = std::max(std::max((size_t)(TI + 1) * TJ * TK, (size_t)TI * (TJ + 1) * TK),
+                                   (size_t)TI * TJ * (TK + 1));
+      smem = (ldP * nc + maxf * nv) * sizeof(double);
+      if (smem <= budget) return;
+    }
+  }
+}
+
+cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
+                            const Mech& mech, const double* q, double* R, int first_order, bool k2d,
+                            unsigned long long* flags, cudaStream_t st) {
+  int TI, TJ, TK;
+  size_t smem;
+  pick_tile(ns, k2d, g.nk, TI, TJ, TK, smem);
+  const long long ntiles = (long long)((g.ni + TI - 1) / TI) * ((g.nj + TJ - 1) / TJ) *
+                           (k2d ? 1 : (g.nk + TK - 1) / TK);
+  cudaError_t err = cudaSuccess;
+  CSB_NS_DISPATCH(ns, {
+    if (k2d) {
+      auto kfn = k_residual<NSB, true>;
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kfn<<<(unsigned)ntiles, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags);
+    } else {
+      auto kfn = k_residual<NSB, false>;
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kfn<<<(unsigned)ntiles, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags);
+    }
+    err = cudaGetLastError();
+  });
+  return err;
+}
+
+cudaError_t CSB_BK(launch_padded)(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
+                          const double* q, double* P, unsigned long long* flags, cudaStream_t st) {
+  const long long NP = (long long)(g.ni + 4) * (g.nj + 4) * (g.nk + 4);
+  const int blocks = (int)std::min<long long>((NP + 127) / 128, 148 * 16);
+  CSB_NS_DISPATCH(ns, { k_padded<NSB><<<blocks, 128, 0, st>>>(mp, g, bc, q, P, flags); });
+  return cudaGetLastError();
+}
+
+}  // namespace csb

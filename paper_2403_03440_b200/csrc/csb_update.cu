@@ -1,0 +1,123 @@
+// csflow-b200: norms, standalone corrections, layout transpose
+// (reference driver.py:85-90, implicit.py:113-135).
+#include "csb_common.cuh"
+#include "csb_kernels.cuh"
+
+namespace csb {
+
+// correct_increment_cs1 / correct_normalize_cs2 on plain (rows, ns) arrays
+// (implicit.py:113-135); mode 1 = CS1, 2 = CS2.  Row-major AoS like the
+// reference's (..., ns) arrays; drho has one value per row.
+__global__ void k_correct(int mode, long long rows, int ns, const double* rs, const double* drs,
+                          const double* drho, double* out, unsigned long long* flags) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < rows;
+       r += (long long)gridDim.x * blockDim.x) {
+    const double* a = rs + r * ns;
+    const double* b = drs + r * ns;
+    double* o = out + r * ns;
+    double tot = 0.0, ds = 0.0;
+    for (int s = 0; s < ns; ++s) {
+      tot += a[s];
+      ds += b[s];
+    }
+    if (mode == 1) {
+      const double defect = drho[r] - ds;
+      for (int s = 0; s < ns; ++s) o[s] = a[s] + b[s] + (a[s] / tot) * defect;
+    } else {
+      const double rnew = tot + drho[r];
+      double rawsum = 0.0;
+      for (int s = 0; s < ns; ++s) rawsum += a[s] + b[s];
+      for (int s = 0; s < ns; ++s) o[s] = rnew * (a[s] + b[s]) / rawsum;
+    }
+    double osum = 0.0;
+    for (int s = 0; s < ns; ++s) osum += o[s];
+    bool ok = !(osum <= 0.0);
+    for (int s = 0; s < ns; ++s)
+      if (o[s] < -EPS_NEG * osum) ok = false;
+    if (!ok) raise_flag(flags, EB_GATE, r);
+  }
+}
+
+// residual_norms partial sums: flow = sum R[0..4]^2, species = sum (sum_s R_s)^2,
+// density = sum R0^2.  Deterministic two-pass reduction.
+constexpr int NORM_BS = 256;
+__global__ void k_norms_partial(int ns, long long N, const double* __restrict__ R, double* partial) {
+  __shared__ double sh[3][NORM_BS / 32];
+  double a = 0.0, b = 0.0, d = 0.0;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < N;
+       c += (long long)gridDim.x * blockDim.x) {
+    const double r0 = R[c];
+    double f = r0 * r0;
+#pragma unroll
+    for (int m = 1; m < 5; ++m) {
+      const double v = R[m * N + c];
+      f += v * v;
+    }
+    double s = 0.0;
+    for (int k = 0; k < ns; ++k) s += R[(5 + k) * N + c];
+    a += f;
+    b += s * s;
+    d += r0 * r0;
+  }
+  double v3[3] = {a, b, d};
+  for (int k = 0; k < 3; ++k) {
+    double v = v3[k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sh[k][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0.0;
+    for (int w = 0; w < NORM_BS / 32; ++w) v += sh[threadIdx.x][w];
+    partial[threadIdx.x * gridDim.x + blockIdx.x] = v;
+  }
+}
+
+__global__ void k_norms_final(int nblocks, const double* partial, double* out) {
+  const int k = threadIdx.x;
+  if (k < 3) {
+    double v = 0.0;
+    for (int i = 0; i < nblocks; ++i) v += partial[k * nblocks + i];
+    out[k] = sqrt(v);
+  }
+}
+
+// AoS (N, nv) <-> SoA (nv, N)
+__global__ void k_transpose(long long N, int nv, const double* __restrict__ src,
+                            double* __restrict__ dst, int to_soa) {
+  const long long total = N * nv;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (to_soa) {
+      const long long c = e % N, m = e / N;  // write-coalesced
+      dst[e] = src[c * nv + m];
+    } else {
+      const long long m = e % nv, c = e / nv;
+      dst[e] = src[m * N + c];
+    }
+  }
+}
+
+
+cudaError_t launch_correct(int mode, long long rows, int ns, const double* rs, const double* drs,
+                           const double* drho, double* out, unsigned long long* flags,
+                           cudaStream_t st) {
+  k_correct<<<grid_for(rows, 128), 128, 0, st>>>(mode, rows, ns, rs, drs, drho, out, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_norms(int ns, long long N, const double* R, double* partial, double* out,
+                         cudaStream_t st) {
+  const int nb = 296;
+  k_norms_partial<<<nb, NORM_BS, 0, st>>>(ns, N, R, partial);
+  k_norms_final<<<1, 32, 0, st>>>(nb, partial, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(long long N, int nv, const double* src, double* dst, int to_soa,
+                             cudaStream_t st) {
+  k_transpose<<<grid_for(N * nv, 256), 256, 0, st>>>(N, nv, src, dst, to_soa);
+  return cudaGetLastError();
+}
+
+}  // namespace csb

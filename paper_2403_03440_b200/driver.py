@@ -1,0 +1,440 @@
+"""Steady pseudo-time driver on the GPU (drop-in for reference driver.py).
+
+``Case``, ``GroupedResidual``, ``ConvergenceHistory``, ``residual_norms``,
+``_apply_update``, ``_implicit_step``, ``_step_with_retries`` and
+``steady_solve`` keep the reference's names, fields and semantics
+(driver.py:38-317).  The field stays on the device for the whole march; each
+iteration is one residual launch, one norms reduction and one fused implicit
+step (csb_implicit_step), with one host sync to read the norms and the device
+flag word that drives the CFL-halving retries.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from .boundary import FACE_NAMES
+from .device import (F_DECODE, F_FACE_T, F_GATE, F_GATE_DECODE, F_KSKIP, F_RES_NONFINITE,
+                     SCHEMES, SoA, get_engine, is_torch)
+from .errors import Diverged, NonPhysicalState, NoWallBoundary
+from .mixture import CellPrimitive, MixtureModel, cloned_mixture, prim_to_cons, transport
+from .spatial import residual_device
+
+MAX_STEP_RETRIES = 5  # driver.py:35
+
+
+@dataclass
+class Case:
+    """Everything one solver run needs (driver.py:38-75)."""
+
+    grid: object
+    model: MixtureModel
+    bcs: dict
+    freestream: CellPrimitive
+    mech: object = None
+    scheme: str = "CI"
+    cfl: float = 5.0
+    cfl_ramp: Optional[tuple] = None
+    species_offdiag: str = "symmetrized"
+    first_order: bool = False
+    max_iters: int = 2000
+    residual_drop_orders: float = 6.0
+    monitor_every: int = 10
+    monitor_window: int = 20
+    monitor_rel_change: Optional[float] = None
+    dt: Optional[float] = None
+    theta: float = 2.0
+    n_steps: int = 0
+    inner_orders: float = 4.0
+    inner_max: int = 60
+    stop_on_absolute_floor: bool = True
+
+    def initial_field(self):
+        q0 = prim_to_cons(self.freestream, self.model)
+        return np.broadcast_to(q0, self.grid.dims + (self.model.nvar,)).copy()
+
+    def cfl_at(self, it: int) -> float:
+        if self.cfl_ramp is None:
+            return self.cfl
+        start, factor, every = self.cfl_ramp
+        return min(self.cfl, start * factor ** (it // max(int(every), 1)))
+
+
+@dataclass
+class GroupedResidual:
+    flow: float
+    species: float
+    density: float
+
+
+@dataclass
+class ConvergenceHistory:
+    """driver.py:93-125, plus per-iteration retry counts."""
+
+    iters: list = field(default_factory=list)
+    res_flow: list = field(default_factory=list)
+    res_species: list = field(default_factory=list)
+    res_density: list = field(default_factory=list)
+    q_stag: list = field(default_factory=list)
+    wall_seconds: list = field(default_factory=list)
+    implicit_seconds: list = field(default_factory=list)
+    cfl: list = field(default_factory=list)
+    retries: list = field(default_factory=list)
+    metadata: dict = field(default_factory=dict)
+    reason: str = ""
+
+    def record(self, it, norms, q_stag, wall_s, imp_s, cfl, retries=0):
+        self.iters.append(it)
+        self.res_flow.append(norms.flow)
+        self.res_species.append(norms.species)
+        self.res_density.append(norms.density)
+        self.q_stag.append(q_stag)
+        self.wall_seconds.append(wall_s)
+        self.implicit_seconds.append(imp_s)
+        self.cfl.append(cfl)
+        self.retries.append(retries)
+
+    def iterations_to_drop(self, orders: float) -> Optional[int]:
+        if not self.res_density:
+            return None
+        target = self.res_density[0] * 10.0 ** (-orders)
+        for it, r in zip(self.iters, self.res_density):
+            if r <= target:
+                return it
+        return None
+
+
+_NORM_MODELS = {}
+
+
+def _norm_engine(ns):
+    m = _NORM_MODELS.get(ns)
+    if m is None:
+        m = _NORM_MODELS[ns] = cloned_mixture(ns)
+    return get_engine(None, m)
+
+
+def _norms_device(eng, R_t, out=None):
+    out = eng.empty(4) if out is None else out
+    eng._chk(eng.lib.csb_residual_norms(eng.ctx, R_t.shape[1], R_t.data_ptr(), out.data_ptr(),
+                                        ctypes.c_void_p(eng.stream)), "residual_norms")
+    return out
+
+
+def residual_norms(R) -> GroupedResidual:
+    """Grouped L2 norms (driver.py:85-90) as one device reduction."""
+    if isinstance(R, SoA):
+        t = R.t
+        eng = _norm_engine(t.shape[0] - 5)
+    else:
+        nv = int(np.shape(R)[-1])
+        eng = _norm_engine(nv - 5)
+        t = eng.to_soa(R, nv)
+    v = _norms_device(eng, t).cpu().numpy()
+    return GroupedResidual(flow=float(v[0]), species=float(v[1]), density=float(v[2]))
+
+
+def _apply_update(q, dq, scheme, model):
+    """Species closure (driver.py:216-229) on the device; raises like the
+    reference when the correction / last-species reconstruction goes negative."""
+    eng = get_engine(None, model)
+    qa = q if (is_torch(q) or isinstance(q, SoA)) else np.asarray(q, dtype=float)
+    shape = tuple(qa.shape if not isinstance(qa, SoA) else qa.dims + (model.nvar,))
+    n = int(np.prod(shape[:-1]))
+    qs = eng.to_soa(qa.reshape(n, model.nvar) if not isinstance(qa, SoA) else qa, model.nvar)
+    dqa = dq if (is_torch(dq) or isinstance(dq, SoA)) else np.asarray(dq, dtype=float)
+    ds = eng.to_soa(dqa.reshape(n, model.nvar) if not isinstance(dqa, SoA) else dqa, model.nvar)
+    qn = eng.empty(model.nvar, n)
+    eng._chk(eng.lib.csb_apply_update(eng.ctx, n, qs.data_ptr(), ds.data_ptr(), SCHEMES[scheme],
+                                      qn.data_ptr(), ctypes.c_void_p(eng.stream)), "_apply_update")
+    flags, cell, _ = eng.status()
+    if flags & F_GATE:
+        raise NonPhysicalState("consistency correction produced negative species density"
+                               if scheme != "CI" else "reconstructed last species went negative")
+    if isinstance(q, SoA):
+        return SoA(qn, q.dims)
+    return eng.from_soa(qn, q, shape)
+
+
+# --------------------------------------------------------------------------
+# wall heat flux monitor (driver.py:132-205)
+# --------------------------------------------------------------------------
+
+def _wall_faces(bcs):
+    return [name for name in FACE_NAMES if bcs[name].kind == "noslip_isothermal"]
+
+
+class _WallGeom:
+    """Wall-distance factors per wall face (setup: node geometry only)."""
+
+    def __init__(self, grid, bcs):
+        nodes = grid.nodes
+        cc = 0.125 * (nodes[:-1, :-1, :-1] + nodes[1:, :-1, :-1] + nodes[:-1, 1:, :-1]
+                      + nodes[:-1, :-1, 1:] + nodes[1:, 1:, :-1] + nodes[1:, :-1, 1:]
+                      + nodes[:-1, 1:, 1:] + nodes[1:, 1:, 1:])
+        self.faces = {}
+        for name in _wall_faces(bcs):
+            fid = FACE_NAMES.index(name)
+            axis, side = divmod(fid, 2)
+            S = np.moveaxis(grid.face_areas(axis), axis, 0)[-1 if side else 0]
+            nhat = S / np.linalg.norm(S, axis=-1, keepdims=True)
+            nhat = nhat.copy() if side == 0 else -nhat
+            nm = np.moveaxis(nodes, axis, 0)[-1 if side else 0]
+            fc = 0.25 * (nm[:-1, :-1] + nm[1:, :-1] + nm[:-1, 1:] + nm[1:, 1:])
+            ccm = np.moveaxis(cc, axis, 0)
+            c1 = ccm[-1 if side else 0]
+            c2 = ccm[-2 if side else 1]
+            d1 = np.abs(np.einsum("...c,...c->...", c1 - fc, nhat))
+            d2 = np.abs(np.einsum("...c,...c->...", c2 - fc, nhat))
+            self.faces[name] = (axis, side, d1, d2)
+
+
+def _wall_rows(eng, q_soa, axis, side):
+    """Decoded primitives of the first two cell layers next to a wall face."""
+    from .mixture import _prim_from_raw
+    ni, nj, nk = eng.dims
+    n = eng.dims[axis]
+    idx = np.arange(eng.N).reshape(eng.dims)
+    take = lambda layer: np.take(idx, layer, axis=axis)
+    l1 = take(n - 1 if side else 0)
+    l2 = take(n - 2 if side else 1)
+    sel = eng.torch.as_tensor(np.concatenate([l1.ravel(), l2.ravel()]), device=eng.device)
+    sub = q_soa[:, sel].contiguous()
+    m = sub.shape[1]
+    out = eng.empty(12 + eng.ns, m)
+    eng._chk(eng.lib.csb_cons_to_prim(eng.ctx, m, sub.data_ptr(), out.data_ptr(),
+                                      ctypes.c_void_p(eng.stream)), "wall rows")
+    prim = _prim_from_raw(out, (m,), eng.ns, None)
+    h = m // 2
+    shp = l1.shape
+    cut = lambda a, k: np.asarray(a)[k * h:(k + 1) * h].reshape(shp + np.asarray(a).shape[1:])
+    return ({"T": cut(prim.T, 0), "p": cut(prim.p, 0), "Y": cut(prim.Y, 0)},
+            {"T": cut(prim.T, 1), "p": cut(prim.p, 1)})
+
+
+def _wall_heat_flux_device(eng, q_soa, geom, bcs, model):
+    out = {}
+    for name, (axis, side, d1, d2) in geom.faces.items():
+        P1, P2 = _wall_rows(eng, q_soa, axis, side)
+        Tw = bcs[name].T_wall
+        dTdn = (((P1["T"] - Tw) * d2 ** 2 - (P2["T"] - Tw) * d1 ** 2) / (d1 * d2 * (d2 - d1)))
+        Y = P1["Y"]
+        rho_w = P1["p"] / ((Y @ model.R_s) * Tw)
+        ws = CellPrimitive(rho=rho_w, u=np.zeros(rho_w.shape + (3,)), p=P1["p"],
+                           T=np.full_like(rho_w, Tw), Y=Y, c=None, gamma=None, h=None, Ek=None)
+        _, k_w, _ = transport(ws, model)
+        out[name] = (k_w * dTdn, P1["p"])
+    return out
+
+
+def wall_heat_flux(P_or_q, grid, bcs, model):
+    """Wall-normal heat flux per wall face (driver.py:132-184).  Accepts the
+    conservative field (any flavour) or a padded primitive array."""
+    if not _wall_faces(bcs):
+        raise NoWallBoundary("no noslip_isothermal boundary in this case")
+    eng = get_engine(grid, model)
+    arr = P_or_q
+    if not isinstance(arr, SoA) and np.shape(arr)[:3] == tuple(n + 4 for n in grid.dims):
+        a = np.asarray(arr)[2:-2, 2:-2, 2:-2]
+        ns = model.ns
+        Y = a[..., 5:5 + ns]
+        from .mixture import make_primitive
+        prim = make_primitive(model, rho=a[..., 0], u=a[..., 1:4], T=a[..., 5 + ns], Y=Y)
+        arr = prim_to_cons(prim, model)
+    qs = eng.to_soa(arr, eng.nv)
+    res = _wall_heat_flux_device(eng, qs, _WallGeom(grid, bcs), bcs, model)
+    return {k: v[0] for k, v in res.items()}
+
+
+def _stagnation_monitor_device(eng, q_soa, geom, bcs, model):
+    """driver.py:187-205: heat flux at the wall cell with the peak pressure."""
+    if not geom.faces:
+        return float("nan")
+    best, best_p = float("nan"), -np.inf
+    for name, (qw, p1) in _wall_heat_flux_device(eng, q_soa, geom, bcs, model).items():
+        idx = np.unravel_index(int(np.argmax(p1)), p1.shape)
+        if p1[idx] > best_p:
+            best_p = float(p1[idx])
+            best = float(qw[idx])
+    return best
+
+
+# --------------------------------------------------------------------------
+# implicit step and the steady march
+# --------------------------------------------------------------------------
+
+class _Stepper:
+    """Device buffers of one march."""
+
+    def __init__(self, case):
+        self.case = case
+        self.eng = eng = get_engine(case.grid, case.model)
+        eng.set_bcs(case.bcs)
+        eng.set_mechanism(case.mech)
+        if case.scheme == "CI" and eng.chem_on():
+            eng.ensure_workspace(True)
+        self.scheme = SCHEMES[case.scheme]
+        self.paper = int(case.species_offdiag == "paper")
+        self.R = eng.empty(eng.nv, eng.N)
+        self.norms = eng.empty(4)
+        torch = eng.torch
+        self.ev0 = torch.cuda.Event(enable_timing=True)
+        self.ev1 = torch.cuda.Event(enable_timing=True)
+
+    def implicit(self, q_t, R_t, cfl, out_t):
+        """One fused implicit step; returns (ok, flags, seconds)."""
+        eng = self.eng
+        self.ev0.record()
+        eng._chk(eng.lib.csb_implicit_step(eng.ctx, q_t.data_ptr(), R_t.data_ptr(), float(cfl),
+                                           self.scheme, self.paper, None, out_t.data_ptr(),
+                                           ctypes.c_void_p(eng.stream)), "_implicit_step")
+        self.ev1.record()
+        flags, cell, cnt = eng.status()
+        secs = self.ev0.elapsed_time(self.ev1) * 1e-3
+        return flags, cell, secs
+
+
+def _implicit_step(case, q, R, cfl, theta=0.0, dt=None, q_n=None, q_nm1=None):
+    """One LU-SGS update at fixed CFL; returns (q_new, implicit_seconds)
+    (driver.py:232-251).  Steady mode only (dual time is out of scope)."""
+    if dt is not None:
+        raise NotImplementedError("dual-time stepping (unsteady_solve) is out of scope")
+    st = _Stepper(case)
+    eng = st.eng
+    qs = eng.to_soa(q, eng.nv)
+    Rs = eng.to_soa(R, eng.nv)
+    out = eng.empty(eng.nv, eng.N)
+    flags, cell, secs = st.implicit(qs, Rs, cfl, out)
+    flags &= ~F_KSKIP
+    if flags:
+        eng.raise_for(flags, cell, "_implicit_step")
+    if isinstance(q, SoA):
+        return SoA(out, eng.dims), secs
+    return eng.from_soa(out, q, tuple(eng.dims) + (eng.nv,)), secs
+
+
+def implicit_step_raw(case, q, R, cfl, dom_override=None):
+    """Fused implicit step that reports instead of raising:
+    returns (q_new, flags, gate_count, first_bad_cell).  ``dom_override``
+    injects dOmega (..., ns, ns)."""
+    st = _Stepper(case)
+    eng = st.eng
+    qs = eng.to_soa(q, eng.nv)
+    Rs = eng.to_soa(R, eng.nv)
+    dom = None
+    if dom_override is not None:
+        dom = eng.to_soa(np.asarray(dom_override, float).reshape(tuple(eng.dims) + (eng.ns ** 2,)),
+                         eng.ns ** 2)
+    out = eng.empty(eng.nv, eng.N)
+    eng._chk(eng.lib.csb_implicit_step(eng.ctx, qs.data_ptr(), Rs.data_ptr(), float(cfl),
+                                       st.scheme, st.paper,
+                                       dom.data_ptr() if dom is not None else None,
+                                       out.data_ptr(), ctypes.c_void_p(eng.stream)),
+             "_implicit_step")
+    flags, cell, cnt = eng.status()
+    like = q if is_torch(q) else np.empty(0)
+    return eng.from_soa(out, like, tuple(eng.dims) + (eng.nv,)), flags & ~F_KSKIP, cnt, cell
+
+
+def _step_device(st, q_t, R_t, cfl, out_t):
+    """_step_with_retries (driver.py:254-263) on device buffers.
+    Returns (cfl_used, implicit_seconds, retries)."""
+    eng = st.eng
+    total = 0.0
+    for attempt in range(MAX_STEP_RETRIES + 1):
+        flags, cell, secs = st.implicit(q_t, R_t, cfl, out_t)
+        total += secs
+        flags &= ~F_KSKIP
+        # first failure in the reference's stage order (driver.py:235-250):
+        # decode (NonPhysicalState, retried) -> dtau (ZeroWavespeed) ->
+        # assembly/sweeps (SingularDiagonal) -> closure + gate (retried)
+        if flags & F_DECODE:
+            nonphys = True
+        else:
+            eng.raise_for(flags, cell, "_implicit_step", order=("zero", "singular"))
+            nonphys = bool(flags & (F_GATE | F_GATE_DECODE))
+        if not nonphys:
+            return cfl, total, attempt
+        if attempt == MAX_STEP_RETRIES:
+            raise Diverged(f"step failed after {MAX_STEP_RETRIES} CFL halvings (CFL={cfl:g})")
+        cfl *= 0.5
+    raise AssertionError("unreachable")
+
+
+def _reference_density_residual(case) -> float:
+    """driver.py:208-213."""
+    inf = case.freestream
+    speed = float(np.linalg.norm(inf.u) + inf.c)
+    areas = [np.linalg.norm(case.grid.face_areas(d), axis=-1).mean() for d in range(3)]
+    return float(inf.rho) * speed * max(areas) * np.sqrt(case.grid.ncells)
+
+
+def steady_solve(case, q0=None, *, return_device=False):
+    """March to steady state; returns (q, ConvergenceHistory) (driver.py:266-317)."""
+    st = _Stepper(case)
+    eng = st.eng
+    q_init = case.initial_field() if q0 is None else q0
+    q = eng.to_soa(q_init, eng.nv).clone()
+    q_next = eng.empty(eng.nv, eng.N)
+    hist = ConvergenceHistory(metadata={
+        "scheme": case.scheme, "cfl": case.cfl, "cfl_ramp": case.cfl_ramp,
+        "monitor_every": case.monitor_every, "monitor_window": case.monitor_window,
+    })
+    ref_floor = 1e-12 * _reference_density_residual(case)
+    cfl_scale = 1.0
+    samples = []
+    walls = bool(_wall_faces(case.bcs))
+    geom = _WallGeom(case.grid, case.bcs) if walls else None
+    for it in range(1, case.max_iters + 1):
+        t0 = time.perf_counter()
+        residual_device(eng, q, case.first_order, R=st.R)
+        v = _norms_device(eng, st.R, st.norms).cpu().numpy()
+        norms = GroupedResidual(float(v[0]), float(v[1]), float(v[2]))
+        if not np.isfinite(norms.flow) or not np.isfinite(norms.species):
+            raise Diverged(f"non-finite residual norm at iteration {it}")
+        sample = float("nan")
+        if case.monitor_rel_change is not None or walls:
+            if it % case.monitor_every == 0 or it == 1:
+                sample = _stagnation_monitor_device(eng, q, geom, case.bcs, case.model) \
+                    if walls else float("nan")
+                samples.append(sample)
+        cfl_now = case.cfl_at(it - 1) * cfl_scale
+        if case.stop_on_absolute_floor and norms.density <= ref_floor:
+            hist.record(it, norms, sample, time.perf_counter() - t0, 0.0, cfl_now)
+            hist.reason = "converged_absolute"
+            break
+        drop = (hist.res_density[0] * 10.0 ** (-case.residual_drop_orders)
+                if hist.res_density and np.isfinite(case.residual_drop_orders) else None)
+        if drop is not None and norms.density <= drop:
+            hist.record(it, norms, sample, time.perf_counter() - t0, 0.0, cfl_now)
+            hist.reason = "converged_residual_drop"
+            break
+        if case.monitor_rel_change is not None and len(samples) >= case.monitor_window:
+            w = np.array(samples[-case.monitor_window:])
+            if np.all(np.isfinite(w)) and np.max(np.abs(w - w[-1])) \
+                    <= case.monitor_rel_change * max(abs(w[-1]), 1e-300):
+                hist.record(it, norms, sample, time.perf_counter() - t0, 0.0, cfl_now)
+                hist.reason = "converged_monitor_plateau"
+                break
+        cfl_used, t_imp, retries = _step_device(st, q, st.R, cfl_now, q_next)
+        q, q_next = q_next, q
+        if cfl_used < cfl_now:
+            cfl_scale *= cfl_used / cfl_now
+        else:
+            cfl_scale = min(1.0, cfl_scale * 1.2)
+        hist.record(it, norms, sample, time.perf_counter() - t0, t_imp, cfl_used, retries)
+    else:
+        hist.reason = "max_iters"
+    if return_device:
+        return SoA(q, eng.dims), hist
+    like = q0 if (q0 is not None and is_torch(q0)) else np.empty(0)
+    return eng.from_soa(q, like, tuple(eng.dims) + (eng.nv,)), hist
+
+
+__all__ = ["Case", "ConvergenceHistory", "GroupedResidual", "MAX_STEP_RETRIES", "residual_norms",
+           "steady_solve", "wall_heat_flux", "_apply_update", "_implicit_step"]

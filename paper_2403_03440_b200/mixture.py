@@ -174,3 +174,77 @@ def cloned_mixture(ns: int, Pr: float = 0.72, Sc: float = 0.7) -> MixtureModel:
     """mixture.py:422-425 (the paper's species-scaling benchmark mixture)."""
     return MixtureModel(species=tuple(nitrogen_like(f"N2_{i:04d}") for i in range(ns)),
                         Pr=Pr, Sc=Sc)
+
+
+# ----------------------------------------------------------------------------
+# device decode (cons_to_prim on the GPU)
+# ----------------------------------------------------------------------------
+
+class DevicePrimitive(CellPrimitive):
+    """CellPrimitive produced on the device; keeps the conservative field so
+    downstream device calls (cell_spectral_radii, ...) need not re-encode."""
+
+
+def _decode_soa(eng, qs, like, n=None):
+    """Device decode of SoA q (nv, N) -> CellPrimitive shaped like the grid
+    (numpy unless `like` is a torch tensor)."""
+    import ctypes
+    n = eng.N if n is None else n
+    out = eng.empty(12 + eng.ns, n)
+    eng._chk(eng.lib.csb_cons_to_prim(eng.ctx, n, qs.data_ptr(), out.data_ptr(),
+                                      ctypes.c_void_p(eng.stream)), "cons_to_prim")
+    eng.check("cons_to_prim", order=("decode",))
+    shape = tuple(eng.dims) if n == eng.N else (n,)
+    return _prim_from_raw(out, shape, eng.ns, like)
+
+
+def _prim_from_raw(out, shape, ns, like):
+    from .device import is_torch
+    if is_torch(like):
+        o = out.to(like.device)
+        f = lambda k: o[k].reshape(shape)
+        Y = o[12:].T.reshape(shape + (ns,))
+        u = o[1:4].T.reshape(shape + (3,))
+    else:
+        o = out.cpu().numpy()
+        f = lambda k: o[k].reshape(shape)
+        Y = np.ascontiguousarray(o[12:].T.reshape(shape + (ns,)))
+        u = np.ascontiguousarray(o[1:4].T.reshape(shape + (3,)))
+    return DevicePrimitive(rho=f(0), u=u, p=f(4), T=f(5), Y=Y, c=f(6), gamma=f(7), h=f(8),
+                           Ek=f(9))
+
+
+def cons_to_prim(q, model: MixtureModel, eps_neg: float = EPS_NEG) -> CellPrimitive:
+    """Decode conservatives on the GPU (mixture.py:287-307)."""
+    from .device import get_engine, is_torch
+    if eps_neg != EPS_NEG:
+        raise ValueError("the device decode uses the reference's eps_neg = 1e-10")
+    eng = get_engine(None, model)
+    qa = q if is_torch(q) else np.asarray(q, dtype=float)
+    shape = tuple(qa.shape[:-1])
+    n = int(np.prod(shape)) if shape else 1
+    qs = eng.to_soa(qa.reshape(n, model.nvar), model.nvar)
+    import ctypes
+    out = eng.empty(12 + eng.ns, n)
+    eng._chk(eng.lib.csb_cons_to_prim(eng.ctx, n, qs.data_ptr(), out.data_ptr(),
+                                      ctypes.c_void_p(eng.stream)), "cons_to_prim")
+    eng.check("cons_to_prim", order=("decode",))
+    prim = _prim_from_raw(out, shape, model.ns, q)
+    object.__setattr__(prim, "_q", q)
+    return prim
+
+
+def transport(prim: CellPrimitive, model: MixtureModel):
+    """Mixture (mu, k, D) (mixture.py:354-372), evaluated on the host.
+
+    Setup/diagnostic helper only (wall heat flux, tests); the kernels carry
+    their own device copy of this closure."""
+    T = np.asarray(prim.T, dtype=float)[..., np.newaxis]
+    mu_ref = np.array([s.mu_ref for s in model.species])
+    T_mu = np.array([s.T_mu for s in model.species])
+    S_mu = np.array([s.S_mu for s in model.species])
+    mu_s = mu_ref * (T / T_mu) ** 1.5 * (T_mu + S_mu) / (T + S_mu)
+    mu = np.sum(np.asarray(prim.Y) * mu_s, axis=-1)
+    k = mu * (np.asarray(prim.Y) @ model.cp_s) / model.Pr
+    D = (mu / (np.asarray(prim.rho) * model.Sc))[..., np.newaxis] * np.ones(model.ns)
+    return mu, k, D

@@ -1,0 +1,165 @@
+"""GPU parity: the CUDA path (through the drop-in API and the C ABI) against
+the reference's golden fixtures and the pinned CPU oracle.
+
+Tolerance (north_star / SURVEY §8(d)): per component,
+max_cells |X_gpu - X_ref| / max_cells |X_ref| <= 1e-10 for R, dtau, d,
+lambda_face, dq*, dq and Q^{m+1} with frozen chemistry; with chemistry the
+finite-difference dOmega is injected and dOmega itself is
+checked against an FD-noise bound.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from golden_cases import comp_relerr, get, has, load, relerr
+from product_cases import golden_product, spec_oracle, spec_product
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+CASES = ["box_air5", "ogrid_air11", "chem3d", "thin", "warped"]
+
+
+def _keys(case):
+    return sorted({k.split("/")[1] for k in load() if k.startswith(case + "/") and k.endswith("/dq")})
+
+
+CASE_KEYS = [(c, k) for c in CASES for k in _keys(c)]
+
+
+def _api():
+    from paper_2403_03440_b200 import driver, implicit, lusgs, spatial
+    return spatial, implicit, lusgs, driver
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_residual_matches_reference(case):
+    spatial, *_ = _api()
+    grid, model, bcs, mech, q, _ = golden_product(case)
+    fo = bool(get(case, "first_order"))
+    R, P = spatial.assemble_residual(q, grid, bcs, mech, model, first_order=fo, return_padded=True)
+    assert comp_relerr(R, get(case, "R")) <= TOL
+    Pref = get(case, "P")
+    np.testing.assert_array_equal(np.isnan(P), np.isnan(Pref))
+    assert relerr(np.nan_to_num(P), np.nan_to_num(Pref)) <= 1e-13
+    R1 = spatial.assemble_residual(q, grid, bcs, mech, model, first_order=True)
+    assert comp_relerr(R1, get(case, "R_first_order")) <= TOL
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_radii_and_dtau_match_reference(case):
+    _, implicit, _, _ = _api()
+    from paper_2403_03440_b200.mixture import cons_to_prim
+    grid, model, bcs, mech, q, cfl = golden_product(case)
+    prim = cons_to_prim(q, model)
+    li, lv = implicit.cell_spectral_radii(prim, grid, model)
+    assert relerr(li, get(case, "lam_inv")) <= TOL
+    assert relerr(lv, get(case, "lam_vis")) <= TOL
+    dom = get(case, "dOm") if has(case, "dOm") else None
+    dtau = implicit.pseudo_time_step(q, grid, mech, model, cfl, dom_override=dom)
+    assert relerr(dtau, get(case, "dtau")) <= TOL
+
+
+@pytest.mark.parametrize("case,key", CASE_KEYS)
+def test_operator_sweeps_update_match_reference(case, key):
+    _, implicit, lusgs, driver = _api()
+    grid, model, bcs, mech, q, cfl = golden_product(case)
+    scheme = key.split("_")[0]
+    offd = "paper" if key.endswith("_paper") else "symmetrized"
+    dom = get(case, "dOm") if has(case, "dOm") else None
+    op = implicit.assemble_lhs(q, grid, scheme, get(case, "dtau"), mech, model,
+                               species_offdiag=offd, dom_override=dom)
+    pre = key + "/"
+    assert relerr(op.w, get(case, pre + "w")) <= TOL
+    assert relerr(op.b, get(case, pre + "b")) <= TOL
+    assert relerr(op.d_scal, get(case, pre + "d_scal")) <= TOL
+    for d in range(3):
+        assert relerr(op.lam_face[d], get(case, pre + f"lam_face{d}")) <= TOL
+    if scheme != "CI":
+        assert relerr(op.d_species, get(case, pre + "d_species")) <= TOL
+        assert relerr(op.sp_lower, get(case, pre + "sp_lower")) <= TOL
+        assert relerr(op.sp_upper, get(case, pre + "sp_upper")) <= TOL
+        for d in range(3):
+            assert relerr(op.lam_face_sp[d], get(case, pre + f"lam_face_sp{d}")) <= TOL
+    if has(case, pre + "dinv"):
+        assert relerr(op.dinv_species_block, get(case, pre + "dinv")) <= 1e-9
+    rhs = -get(case, "R")
+    dq, star = lusgs.lusgs_solve(op, rhs, return_forward=True)
+    assert comp_relerr(star, get(case, pre + "dq_star")) <= TOL
+    assert comp_relerr(dq, get(case, pre + "dq")) <= TOL
+    if offd == "symmetrized":
+        from paper_2403_03440_b200.driver import Case
+        case_obj = Case(grid=grid, model=model, bcs=bcs, freestream=None, mech=mech, scheme=scheme,
+                        cfl=cfl)
+        qn, flags, cnt, cell = driver.implicit_step_raw(case_obj, q, get(case, "R"), cfl,
+                                                        dom_override=dom)
+        assert comp_relerr(qn, get(case, pre + "q_new")) <= TOL
+        bad = get(case, pre + "gate_bad")
+        assert cnt == int(bad.sum())
+        if cnt:
+            assert cell == int(np.flatnonzero(bad.ravel())[0])
+
+
+def test_chemistry_against_reference():
+    from paper_2403_03440_b200.chemistry import production_rates, source_jacobian
+    from paper_2403_03440_b200.mixture import cons_to_prim
+    from product_cases import model_from_table
+    from golden_cases import mech as omech
+    import product_cases as pc
+    model = model_from_table(get("rates", "species"), get("rates", "PrSc"))
+    _, _, _, mech, q, _ = golden_product("rates")
+    prim = cons_to_prim(q, model)
+    om = production_rates(prim, mech, model)
+    ref = get("rates", "omega")
+    assert relerr(om, ref) <= 1e-12
+    dOm = source_jacobian(prim, mech, model)
+    dref = get("rates", "dOm")
+    # FD noise bound: ulp noise in omega / h
+    rho = np.asarray(prim.rho)
+    h = 1e-8 * np.abs(np.asarray(prim.Y) * rho[..., None])
+    h = np.maximum(h, 1e-12 * rho[..., None])
+    bound = 64 * np.finfo(float).eps * np.max(np.abs(ref), axis=-1)[..., None, None] / h[..., None, :]
+    assert np.all(np.abs(dOm - dref) <= bound + 1e-9 * np.abs(dref))
+
+
+# ---------------------------------------------------------------- configs vs oracle
+
+def _full_iteration_vs_oracle(spec, schemes, tol=TOL):
+    from paper_2403_03440_b200 import driver, implicit, spatial
+    grid, model, bcs, mech = spec_product(spec)
+    th, og, obcs, omech = spec_oracle(spec)
+    q = spec.q
+    R = spatial.assemble_residual(q, grid, bcs, mech, model)
+    Ro = O.residual(q, og, obcs, omech, th)
+    assert comp_relerr(R, Ro) <= tol
+    dtau = implicit.pseudo_time_step(q, grid, mech, model, spec.cfl)
+    for sch in schemes:
+        res = O.implicit_step(q, Ro, og, omech, th, sch, spec.cfl, want_star=False)
+        assert relerr(dtau, res.dtau) <= tol
+        case = driver.Case(grid=grid, model=model, bcs=bcs, freestream=None, mech=mech, scheme=sch,
+                           cfl=spec.cfl)
+        qn, flags, cnt, cell = driver.implicit_step_raw(case, q, Ro, spec.cfl)
+        assert comp_relerr(qn - q, res.q_new - q) <= tol
+        assert cnt == int(res.bad.sum())
+
+
+def test_config0_one_iteration_vs_oracle():
+    from paper_2403_03440_b200 import configs as C
+    _full_iteration_vs_oracle(C.config0(seed=0), ("CS1", "CS2", "CI"))
+
+
+def test_config1_shape_vs_oracle():
+    from paper_2403_03440_b200 import configs as C
+    _full_iteration_vs_oracle(C.config1(seed=1, dims=(160, 128, 1)), ("CS1", "CI"))
+
+
+def test_config2_shape_vs_oracle():
+    from paper_2403_03440_b200 import configs as C
+    _full_iteration_vs_oracle(C.config2(seed=2, dims=(96, 64, 1)), ("CS1",))
+
+
+def test_config3_species_vs_oracle():
+    from paper_2403_03440_b200 import configs as C
+    for ns in (11, 20):
+        _full_iteration_vs_oracle(C.config3(ns, dims=(40, 32, 1)), ("CS1", "CI"))
