@@ -71,6 +71,8 @@ int csb_create(csb_ctx** out);
 void csb_destroy(csb_ctx* ctx);
 const char* csb_last_error(const csb_ctx* ctx);
 int csb_version(void);
+/* Kernel launches issued by this library so far (all contexts). */
+unsigned long long csb_launch_count(void);
 
 /* Species table, host arrays of length ns (MixtureModel, mixture.py:58-104). */
 int csb_set_model(csb_ctx* ctx, int ns, const double* M, const double* cp, const double* hf,
@@ -102,7 +104,7 @@ size_t csb_workspace_bytes(const csb_ctx* ctx, int with_block);
 int csb_set_workspace(csb_ctx* ctx, void* dev, size_t bytes);
 
 /* Read and clear the device flag word (synchronises `stream`).  flags: bit
- * set; first_cell: first offending cell of the lowest set bit; gate_count:
+ * set; first_cell: smallest offending cell index over all set bits; gate_count:
  * number of cells that failed the post-update gate. */
 int csb_status(csb_ctx* ctx, unsigned long long* flags, long long* first_cell,
                long long* gate_count, void* stream);

@@ -24,6 +24,7 @@ _hp = ctypes.POINTER(ctypes.c_double)
 # name -> (restype, argtypes); the ABI test checks every header symbol is here
 SIGNATURES = {
     "csb_version": (_i, []),
+    "csb_launch_count": (ctypes.c_ulonglong, []),
     "csb_create": (_i, [ctypes.POINTER(_p)]),
     "csb_destroy": (None, [_p]),
     "csb_last_error": (ctypes.c_char_p, [_p]),

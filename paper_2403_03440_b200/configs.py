@@ -301,3 +301,30 @@ def config4(seed=4, dims=(4096, 2048, 1)):
     q = np.broadcast_to(q0, tuple(dims) + (16,)).copy()  # Case.initial_field (driver.py:67-69)
     return CaseSpec("config4", ogrid_nodes(dims), sp, cylinder_bcs(fs), q, 1000.0,
                     extra={"iterations": 500, "cfl_ramp": (1.0, 2.0, 45)})
+
+
+# ------------------------------------------------------------ product objects
+
+def build_case(spec):
+    """(grid, model, bcs, mech) drop-in objects for a CaseSpec."""
+    from .boundary import BoundaryCondition
+    from .chemistry import Mechanism, Reaction
+    from .grid import compute_metrics
+    from .mixture import MixtureModel, SpeciesData, make_primitive
+    model = MixtureModel(species=tuple(SpeciesData(s.name, s.M, s.cp, s.hf, s.Tref, s.mu_ref,
+                                                   s.T_mu, s.S_mu) for s in spec.species),
+                         Pr=spec.Pr, Sc=spec.Sc)
+    grid = compute_metrics(spec.nodes)
+    bcs = {}
+    for name in FACES:
+        b = spec.bcs[name]
+        fr = None
+        if b.fs is not None:
+            rho, u, T, Y = b.fs
+            fr = make_primitive(model, rho=rho, u=u, T=T, Y=Y)
+        bcs[name] = BoundaryCondition(b.kind, freestream=fr, T_wall=b.T_wall, axis=b.axis)
+    mech = None
+    if spec.reactions:
+        mech = Mechanism(tuple(Reaction(np.asarray(r.nu_r, float), np.asarray(r.nu_p, float), r.Af,
+                                        r.bf, r.Eaf, backward=r.back) for r in spec.reactions))
+    return grid, model, bcs, mech

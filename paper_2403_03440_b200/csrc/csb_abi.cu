@@ -181,6 +181,8 @@ extern "C" {
 
 int csb_version(void) { return 1; }
 
+unsigned long long csb_launch_count(void) { return launch_count(); }
+
 int csb_create(csb_ctx** out) {
   if (!out) return CSB_E_BADARG;
   *out = new csb_ctx();
@@ -368,11 +370,11 @@ int csb_status(csb_ctx* c, unsigned long long* flags, long long* first_cell, lon
   if (e != cudaSuccess) return cuda_check(c, e, "read status");
   if (flags) *flags = h[0];
   if (first_cell) {
-    *first_cell = -1;
+    *first_cell = -1;  // smallest offending cell over all raised bits
     for (int b = 0; b < EB_COUNT; ++b)
-      if (h[0] & (1ull << b)) {
-        *first_cell = (long long)h[1 + b];
-        break;
+      if ((h[0] & (1ull << b)) && b != EB_KSKIP) {
+        const long long cb = (long long)h[1 + b];
+        if (*first_cell < 0 || cb < *first_cell) *first_cell = cb;
       }
   }
   if (gate_count) *gate_count = (long long)h[FLAG_GATE_COUNT];
@@ -527,7 +529,7 @@ int csb_operator_field(csb_ctx* c, const double* q, int which, double* dst, void
     e = cp(c->op.dinv, (size_t)ns * ns * N);
   } else if (which == 13) {
     if (!c->op.dom_full) return fail(c, CSB_E_STATE, "full dOmega not stored");
-    e = cp(c->op.dom, (size_t)ns * ns * N);
+    e = launch_export_op(c->d_model, ns, c->g, c->op, q, 4, dst, st);
   } else {
     return fail(c, CSB_E_BADARG, "unknown operator field");
   }

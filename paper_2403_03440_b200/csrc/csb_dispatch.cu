@@ -1,8 +1,14 @@
 // csflow-b200: route ns to the per-bucket launchers (csb_bucket.cu).
+#include <atomic>
+
 #include "csb_common.cuh"
 #include "csb_kernels.cuh"
 
 namespace csb {
+
+static std::atomic<unsigned long long> g_launches{0};
+void note_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 #define CSB_DECL(b)                                                                               \
   cudaError_t launch_residual_b##b(const Model*, int, const GridDev&, const BCDev&, const Mech&,   \
@@ -49,48 +55,58 @@ CSB_BUCKET_LIST(CSB_DECL)
 cudaError_t launch_residual(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                             const Mech& mech, const double* q, double* R, int first_order, bool k2d,
                             unsigned long long* flags, cudaStream_t st) {
+  note_launches(1);
   CSB_ROUTE(launch_residual, mp, ns, g, bc, mech, q, R, first_order, k2d, flags, st)
 }
 cudaError_t launch_padded(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                           const double* q, double* P, unsigned long long* flags, cudaStream_t st) {
+  note_launches(1);
   CSB_ROUTE(launch_padded, mp, ns, g, bc, q, P, flags, st)
 }
 cudaError_t launch_decode(const Model* mp, int ns, const GridDev& g, const double* q, double* out,
                           unsigned long long* flags, cudaStream_t st) {
+  note_launches(1);
   CSB_ROUTE(launch_decode, mp, ns, g, q, out, flags, st)
 }
 cudaError_t launch_source_jacobian(const Model* mp, int ns, const GridDev& g, const Mech& mech,
                                    const double* q, double* dom, int dom_full, double* lamS,
                                    const double* dom_in, unsigned long long* flags,
                                    cudaStream_t st) {
+  note_launches(1);
   CSB_ROUTE(launch_source_jacobian, mp, ns, g, mech, q, dom, dom_full, lamS, dom_in, flags, st)
 }
 cudaError_t launch_production(const Model* mp, int ns, const GridDev& g, const Mech& mech,
                               const double* q, double* om, unsigned long long* flags,
                               cudaStream_t st) {
+  note_launches(1);
   CSB_ROUTE(launch_production, mp, ns, g, mech, q, om, flags, st)
 }
 cudaError_t launch_time_step(const Model* mp, int ns, const GridDev& g, const double* q, double cfl,
                              const double* lamS, double* dtau, double* lam_inv, double* lam_vis,
                              unsigned long long* flags, cudaStream_t st) {
+  note_launches(1);
   CSB_ROUTE(launch_time_step, mp, ns, g, q, cfl, lamS, dtau, lam_inv, lam_vis, flags, st)
 }
 cudaError_t launch_assemble_cell(const Model* mp, int ns, const GridDev& g, const double* q,
                                  const double* dtau, double theta, double dt, OpDev& op,
                                  unsigned long long* flags, cudaStream_t st) {
+  note_launches(1);
   CSB_ROUTE(launch_assemble_cell, mp, ns, g, q, dtau, theta, dt, op, flags, st)
 }
 cudaError_t launch_sweeps_generic(const Model* mdl, int ns, const GridDev& g, const OpDev& op,
                                   const double* rhs, double* dq, double* dq_star, cudaStream_t st) {
+  note_launches(2ull * ((g.ni - 1) + (g.nj - 1) + (g.nk - 1) + 1));
   CSB_ROUTE(launch_sweeps_generic, mdl, ns, g, op, rhs, dq, dq_star, st)
 }
 cudaError_t launch_update(const Model* mp, int ns, const GridDev& g, int scheme, const double* q,
                           const double* dq, double* qn, unsigned long long* flags,
                           cudaStream_t st) {
+  note_launches(1);
   CSB_ROUTE(launch_update, mp, ns, g, scheme, q, dq, qn, flags, st)
 }
 cudaError_t launch_export_op(const Model* mdl, int ns, const GridDev& g, const OpDev& op,
                              const double* q, int what, double* dst, cudaStream_t st) {
+  note_launches(1);
   CSB_ROUTE(launch_export_op, mdl, ns, g, op, q, what, dst, st)
 }
 

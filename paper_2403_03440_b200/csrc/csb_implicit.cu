@@ -155,6 +155,7 @@ __global__ void k_check_2d(GridDev g, int* ok) {
 cudaError_t launch_dtau_arrays(long long N, const double* li, const double* lv, const double* lS,
                                double lS_scalar, double cfl, const double* J, double* dtau,
                                unsigned long long* flags, cudaStream_t st) {
+  note_launches(1);
   k_dtau_arrays<<<grid_for(N, 256), 256, 0, st>>>(N, li, lv, lS, lS_scalar, cfl, J, dtau, flags);
   return cudaGetLastError();
 }
@@ -164,6 +165,7 @@ cudaError_t launch_assemble(const Model* mp, int ns, const GridDev& g, const dou
                             unsigned long long* flags, cudaStream_t st) {
   cudaError_t e = launch_assemble_cell(mp, ns, g, q, dtau, theta, dt, op, flags, st);
   if (e != cudaSuccess) return e;
+  note_launches(3);
   for (int d = 0; d < 3; ++d) k_assemble_face<<<grid_for(g.NF[d], 256), 256, 0, st>>>(g, op, d);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -172,6 +174,7 @@ cudaError_t launch_assemble(const Model* mp, int ns, const GridDev& g, const dou
     const size_t smem = (size_t)wpb * ns * (2 * ns + 1) * sizeof(double);
     cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int blocks = (int)std::min<long long>((g.N + wpb - 1) / wpb, 148LL * 64);
+    note_launches(1);
     k_block_inverse<<<blocks, 32 * wpb, smem, st>>>(ns, g, op, flags);
     e = cudaGetLastError();
   }

@@ -102,6 +102,7 @@ __global__ void k_transpose(long long N, int nv, const double* __restrict__ src,
 cudaError_t launch_correct(int mode, long long rows, int ns, const double* rs, const double* drs,
                            const double* drho, double* out, unsigned long long* flags,
                            cudaStream_t st) {
+  note_launches(1);
   k_correct<<<grid_for(rows, 128), 128, 0, st>>>(mode, rows, ns, rs, drs, drho, out, flags);
   return cudaGetLastError();
 }
@@ -109,6 +110,7 @@ cudaError_t launch_correct(int mode, long long rows, int ns, const double* rs, c
 cudaError_t launch_norms(int ns, long long N, const double* R, double* partial, double* out,
                          cudaStream_t st) {
   const int nb = 296;
+  note_launches(2);
   k_norms_partial<<<nb, NORM_BS, 0, st>>>(ns, N, R, partial);
   k_norms_final<<<1, 32, 0, st>>>(nb, partial, out);
   return cudaGetLastError();
@@ -116,6 +118,7 @@ cudaError_t launch_norms(int ns, long long N, const double* R, double* partial, 
 
 cudaError_t launch_transpose(long long N, int nv, const double* src, double* dst, int to_soa,
                              cudaStream_t st) {
+  note_launches(1);
   k_transpose<<<grid_for(N * nv, 256), 256, 0, st>>>(N, nv, src, dst, to_soa);
   return cudaGetLastError();
 }

@@ -104,7 +104,10 @@ __global__ void k_export(const Model* __restrict__ mp, GridDev g, OpDev op,
   const long long N = g.N;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < N;
        c += (long long)gridDim.x * blockDim.x) {
-    if (what <= 1) {
+    if (what == 4) {  // vdom = dOmega * V (implicit.py:356)
+      const double V = __ldg(g.vol + c);
+      for (int e = 0; e < ns * ns; ++e) dst[(long long)e * N + c] = op.dom[(long long)e * N + c] * V;
+    } else if (what <= 1) {
       Cell<NSB> cs;
       decode<NSB>(m, q + c, N, cs);
       if (what == 0) {

@@ -178,6 +178,8 @@ class Engine:
     def cell_ijk(self, cell):
         if cell < 0:
             return None
+        if cell >= self.N:  # grid-free call with an explicit cell count
+            return int(cell)
         return tuple(int(x) for x in np.unravel_index(cell, self.dims))
 
     def raise_for(self, flags, cell, stage="", order=("decode", "zero", "singular", "gate", "gate_decode")):

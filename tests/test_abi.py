@@ -16,7 +16,7 @@ def header_symbols():
     for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
         txt = open(h).read()
         txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-        for m in re.finditer(r"^\s*(?:const\s+)?[a-z_]+\s*\**\s*(csb_[a-z0-9_]+)\s*\(", txt, flags=re.M):
+        for m in re.finditer(r"^\s*(?:[a-z_]+\s*\**\s+)+(csb_[a-z0-9_]+)\s*\(", txt, flags=re.M):
             syms.add(m.group(1))
     return syms
 
