@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Benchmark: implicit cell-iterations/s of the component-split (CS1) implicit
+pseudo-time iteration on one B200 (BASELINE.json metric), config 1.
+
+One step = one full implicit iteration over the 512 x 512 config-1 field
+(5-species air, CFL 50): residual R, grouped norms, local time step, CS
+operator assembly, forward + backward LU-SGS sweeps, CS1 closure + gate.
+Inputs are resident in HBM; L2 is flushed (512 MiB write) before every timed
+step.  Prints ONE JSON line (rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 (torchrun): independent replicas, one per GPU (the LU-SGS sweep has a
+serial dependency chain; the path does not shard).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "implicit cell-iterations/s (split vs coupled) at 1 B200; % HBM roofline"
+UNIT = "cell-iterations/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=1)
+    p.add_argument("--scheme", default="CS1", choices=["CS1", "CS2", "CI"])
+    p.add_argument("--no-extras", action="store_true", help="skip coupled/e2e/cpu legs")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload_spec(cfgnum):
+    from paper_2403_03440_b200 import configs as C
+    if cfgnum == 0:
+        return C.config0(seed=0), "config0: 64x64 box, air5 thermo, frozen chemistry, CFL 10"
+    if cfgnum == 1:
+        return C.config1(seed=1), "config1: 512x512 box (dx=dy=1e-3 m), air5 thermo, frozen chemistry, CFL 50"
+    if cfgnum == 3:
+        return C.config3(11, seed=3), "config3 ns=11: 1024x1024 box, 11-species, frozen, CFL 10"
+    raise SystemExit(f"config {cfgnum} not benchmarked")
+
+
+def algorithmic_bytes(nv):
+    """Canonical accounting: doubles per cell per kernel pass."""
+    return {"rhs": 2 * nv + 7, "assemble": nv + 16, "sweeps": 2 * (3 * nv + 12),
+            "total": 9 * nv + 47}
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- our arm
+class Runner:
+    def __init__(self, spec, scheme):
+        import torch
+        from paper_2403_03440_b200 import configs as C
+        from paper_2403_03440_b200.device import SCHEMES, get_engine
+        self.torch = torch
+        grid, model, bcs, mech = C.build_case(spec)
+        self.eng = eng = get_engine(grid, model)
+        eng.set_bcs(bcs)
+        eng.set_mechanism(mech)
+        self.spec = spec
+        self.scheme = SCHEMES[scheme]
+        self.q = eng.to_soa(spec.q, eng.nv).clone()
+        self.qn = eng.empty(eng.nv, eng.N)
+        self.R = eng.empty(eng.nv, eng.N)
+        self.norms = eng.empty(4)
+        self.lib = eng.lib
+        self.stream = ctypes.c_void_p(eng.stream)
+        torch.cuda.synchronize()
+
+    def step(self, q=None, qn=None, scheme=None):
+        e = self.eng
+        rc = self.lib.csb_iteration(e.ctx, (q if q is not None else self.q).data_ptr(),
+                                    float(self.spec.cfl),
+                                    self.scheme if scheme is None else scheme, 0, 0,
+                                    (qn if qn is not None else self.qn).data_ptr(),
+                                    self.R.data_ptr(), self.norms.data_ptr(), self.stream)
+        if rc:
+            raise RuntimeError(self.lib.csb_last_error(e.ctx))
+
+    def stages(self, reps=3):
+        """Per-stage device time (ms), instrumented pass outside the timed region."""
+        torch, e, lib, st = self.torch, self.eng, self.lib, self.stream
+        names = ["rhs", "norms", "dtau", "assemble", "sweeps", "update"]
+        acc = {n: 0.0 for n in names}
+        dq = e.empty(e.nv, e.N)
+        dtau = e.empty(e.N)
+        for _ in range(reps):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+            ev[0].record()
+            lib.csb_residual(e.ctx, self.q.data_ptr(), self.R.data_ptr(), None, 0, st)
+            ev[1].record()
+            lib.csb_residual_norms(e.ctx, e.N, self.R.data_ptr(), self.norms.data_ptr(), st)
+            ev[2].record()
+            lib.csb_time_step(e.ctx, self.q.data_ptr(), float(self.spec.cfl), None, dtau.data_ptr(), st)
+            ev[3].record()
+            lib.csb_assemble(e.ctx, self.q.data_ptr(), dtau.data_ptr(), self.scheme, 0, 0.0, -1.0,
+                             None, st)
+            ev[4].record()
+            lib.csb_lusgs(e.ctx, self.R.data_ptr(), dq.data_ptr(), None, st)
+            ev[5].record()
+            lib.csb_apply_update(e.ctx, e.N, self.q.data_ptr(), dq.data_ptr(), self.scheme,
+                                 self.qn.data_ptr(), st)
+            ev[6].record()
+            torch.cuda.synchronize()
+            for i, n in enumerate(names):
+                acc[n] += ev[i].elapsed_time(ev[i + 1])
+        e.status()
+        return {n: acc[n] / reps for n in names}
+
+
+def flush_buffer(torch):
+    return torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+
+def timed_steps(run, K, W, flush, sampler=None, scheme=None):
+    torch = run.torch
+    for _ in range(W):
+        flush.zero_()
+        run.step(scheme=scheme)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(K)]
+    l0 = run.lib.csb_launch_count()
+    for a, b in evs:
+        flush.zero_()
+        a.record()
+        run.step(scheme=scheme)
+        b.record()
+    torch.cuda.synchronize()
+    launches = run.lib.csb_launch_count() - l0
+    ms = [a.elapsed_time(b) for a, b in evs]
+    return float(sum(ms)), launches
+
+
+def e2e_steps(run, K, W):
+    """Same iteration through the C ABI with HOST (pinned) buffers in the
+    reference layout (ni, nj, nk, nv): H2D copy, AoS->SoA, iteration,
+    SoA->AoS, D2H of Q^{m+1} and the norms, all inside the timed region."""
+    torch, e, lib = run.torch, run.eng, run.lib
+    nv, N = e.nv, e.N
+    host_q = torch.from_numpy(np.ascontiguousarray(run.spec.q.reshape(N, nv))).pin_memory()
+    host_out = torch.empty((N, nv), dtype=torch.float64).pin_memory()
+    host_norms = torch.empty(4, dtype=torch.float64).pin_memory()
+    dev_aos = e.empty(N, nv)
+    q_soa = e.empty(nv, N)
+    out_aos = e.empty(N, nv)
+    st = run.stream
+
+    def one():
+        dev_aos.copy_(host_q, non_blocking=True)
+        lib.csb_transpose(N, nv, dev_aos.data_ptr(), q_soa.data_ptr(), 1, st)
+        run.step(q=q_soa)
+        lib.csb_transpose(N, nv, run.qn.data_ptr(), out_aos.data_ptr(), 0, st)
+        host_out.copy_(out_aos, non_blocking=True)
+        host_norms.copy_(run.norms, non_blocking=True)
+
+    for _ in range(W):
+        one()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(K):
+        one()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b), N * nv * 8, N * nv * 8 + 3 * 8
+
+
+def ncu_traffic(path=os.path.join(ROOT, "profiles", "ncu_traffic.json")):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- CPU legs
+def oracle_sample(cfgnum, scheme, dims=(128, 128, 1)):
+    """The CPU oracle (the reference algorithm restated in numpy/numba) on a
+    bounded sample of the workload: same config distribution, `dims` cells."""
+    import oracle as O
+    from paper_2403_03440_b200 import configs as C
+    if cfgnum == 0:
+        spec = C.config0(seed=0, dims=dims)
+    elif cfgnum == 3:
+        spec = C.config3(11, seed=3, dims=dims)
+    else:
+        spec = C.config1(seed=1, dims=dims)
+    th = O.Thermo([s.M for s in spec.species], [s.cp for s in spec.species],
+                  [s.hf for s in spec.species], [s.Tref for s in spec.species],
+                  [s.mu_ref for s in spec.species], [s.T_mu for s in spec.species],
+                  [s.S_mu for s in spec.species], spec.Pr, spec.Sc)
+    grid = O.Grid(spec.nodes)
+    bcs = {n: O.BC(b.kind, Tw=b.T_wall, axis=b.axis) for n, b in spec.bcs.items()}
+
+    def one():
+        R = O.residual(spec.q, grid, bcs, None, th)
+        O.norms(R)
+        O.implicit_step(spec.q, R, grid, None, th, scheme, spec.cfl, want_star=False)
+
+    return spec, one
+
+
+def cpu_baseline(cfgnum, scheme, reps=2):
+    spec, one = oracle_sample(cfgnum, scheme)
+    _, warm = oracle_sample(cfgnum, scheme, dims=(8, 8, 1))
+    warm()  # numba JIT
+    one()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        one()
+    dt = (time.perf_counter() - t0) / reps
+    n = spec.ncells
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle (numpy + numba sweeps, the reference algorithm restated) full "
+                      f"{scheme} iteration on a {spec.dims[0]}x{spec.dims[1]} sample of the same "
+                      f"config distribution, mean of {reps} after warm-up; single-threaded like "
+                      f"the reference (host cpu_count={os.cpu_count()})"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    spec_full, desc = workload_spec(args.config)
+    spec, one = oracle_sample(args.config, args.scheme)
+    _, warm = oracle_sample(args.config, args.scheme, dims=(8, 8, 1))
+    warm()
+    for _ in range(max(args.warmup, 1)):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    dt = time.perf_counter() - t0
+    n = spec.ncells
+    value = n * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": desc + f", {args.scheme} full implicit iteration", "scheme": args.scheme,
+                   "sample_cells": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"each step = one full {args.scheme} iteration of the CPU oracle "
+                                   f"on a {spec.dims[0]}x{spec.dims[1]} sample of the workload "
+                                   f"(bounded; the reference path is serial)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- main
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    spec, desc = workload_spec(args.config)
+    run = Runner(spec, args.scheme)
+    flush = flush_buffer(torch)
+    # settle clocks (untimed), then sample clocks across warm-up + timed region
+    t_end = time.perf_counter() + 0.5
+    while time.perf_counter() < t_end:
+        run.step()
+        torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms, launches = timed_steps(run, args.steps, args.warmup, flush)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    fl, cell, gate = run.eng.status()
+    N = run.eng.N
+    nv = run.eng.nv
+    value = world * N * args.steps / (total_ms * 1e-3)
+
+    extras = {}
+    if not args.no_extras:
+        # split vs coupled at equal care: the CI operator on the same workload
+        ci_ms, _ = timed_steps(run, max(3, args.steps // 2), 2, flush, scheme=0)
+        extras["coupled_CI"] = {"value": N * max(3, args.steps // 2) / (ci_ms * 1e-3), "unit": UNIT}
+        run.eng.status()
+        e2e_ms, h2d, d2h = e2e_steps(run, args.steps, max(1, args.warmup // 2))
+        e2e = {"value": world * N * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+        run.eng.status()
+    else:
+        e2e = None
+    stages = run.stages()
+    ab = algorithmic_bytes(nv)
+    peak, peak_src = peaks()
+    dom = max(("rhs", "sweeps", "assemble"), key=lambda k: stages[k] if k != "assemble"
+              else stages["assemble"] + stages["dtau"])
+    dom_ms = stages[dom] if dom != "assemble" else stages["assemble"] + stages["dtau"]
+    bytes_dom = N * ab[dom] * 8
+    achieved = bytes_dom / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tr = ncu_traffic()
+    if tr and dom in tr.get("per_launch_bytes", {}):
+        traffic = tr["per_launch_bytes"][dom]
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "kernel": dom,
+                "algorithmic_bytes_per_cell": ab[dom] * 8, "peak_source": peak_src,
+                "note": "achieved = SURVEY §8(d) algorithmic bytes of the stage / its CUDA-event time"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": desc + f", {args.scheme} full implicit iteration per step",
+                   "grid": "x".join(map(str, spec.dims)), "ns": spec.ns, "scheme": args.scheme,
+                   "cfl": spec.cfl, "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "flushed (512 MiB device write) before every timed step",
+                   "inputs": "resident in HBM (value); host pinned buffers (e2e)"},
+        "roofline": roofline,
+        "stages_ms": stages,
+        "iteration_roofline_frac": (N * ab["total"] * 8 / (total_ms / args.steps * 1e-3) / 1e9) / peak,
+        "gate_failures": gate,
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / args.steps,
+        "clocks": clk,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    line.update(extras)
+    if rank == 0 and not args.no_extras:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args.config, args.scheme)
+        except Exception as exc:  # the CPU leg must not kill the GPU line
+            line["cpu_baseline"] = {"value": None, "error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
