@@ -81,17 +81,28 @@ __global__ void k_update(const Model* __restrict__ mp, long long N, int scheme,
                          const double* __restrict__ q, const double* __restrict__ dq,
                          double* __restrict__ qn, unsigned long long* flags) {
   const Model& m = *mp;
-  unsigned bad_count = 0;
+  // per-thread tallies, reduced per warp at the end (random states fail the
+  // gate in most cells: one atomic per warp, not per cell)
+  unsigned long long bad_count = 0, first1 = ~0ull, first2 = ~0ull;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < N;
        c += (long long)gridDim.x * blockDim.x) {
     const bool ok1 = closure<NSB>(scheme, m.ns, q + c, dq + c, qn + c, N);
     Cell<NSB> cs;
     const bool ok2 = decode<NSB>(m, qn + c, N, cs);  // admissibility gate (driver.py:250)
-    if (!ok1) raise_flag(flags, EB_GATE, c);
-    if (!ok2) raise_flag(flags, EB_GATE_DECODE, c);
+    if (!ok1 && first1 == ~0ull) first1 = (unsigned long long)c;
+    if (!ok2 && first2 == ~0ull) first2 = (unsigned long long)c;
     if (!(ok1 && ok2)) ++bad_count;
   }
-  if (bad_count) atomicAdd(flags + FLAG_GATE_COUNT, (unsigned long long)bad_count);
+  for (int o = 16; o > 0; o >>= 1) {
+    bad_count += __shfl_xor_sync(0xffffffffu, bad_count, o);
+    first1 = min(first1, __shfl_xor_sync(0xffffffffu, first1, o));
+    first2 = min(first2, __shfl_xor_sync(0xffffffffu, first2, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (bad_count) atomicAdd(flags + FLAG_GATE_COUNT, bad_count);
+    if (first1 != ~0ull) raise_flag(flags, EB_GATE, (long long)first1);
+    if (first2 != ~0ull) raise_flag(flags, EB_GATE_DECODE, (long long)first2);
+  }
 }
 
 // Operator export (reference ImplicitOperator fields, implicit.py:59-81, 385-395)
