@@ -181,6 +181,12 @@ int csb_residual_norms(csb_ctx* ctx, long long N, const double* R, double* out3,
 int csb_implicit_step(csb_ctx* ctx, const double* q, const double* R, double cfl, int scheme,
                       int offdiag_paper, const double* dOm_in, double* q_new, void* stream);
 
+/* As csb_implicit_step with a path choice (0 auto, 1 generic hyperplane
+ * sweeps, 2 the 2-D wavefront path) and an optional dq output [nv][N]. */
+int csb_implicit_step_ex(csb_ctx* ctx, const double* q, const double* R, double cfl, int scheme,
+                         int offdiag_paper, const double* dOm_in, double* q_new, double* dq_out,
+                         int path, void* stream);
+
 /* One steady iteration (driver.py:279-308 without the retry/stop logic):
  * R = residual(q) (R_out nullable: internal), norms -> norms3 (device,
  * nullable), q_new = implicit step. */

@@ -36,6 +36,9 @@ struct csb_ctx {
   double *dtau = nullptr, *R = nullptr, *dq = nullptr, *partial = nullptr, *norms = nullptr;
   double* dom_scratch = nullptr;
   int assembled_scheme = -1;
+  WaveBufs wb{};
+  bool wave_ok = false;
+  int wave_disabled = 0;
   std::string err;
 };
 
@@ -164,6 +167,24 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
   c->dq = k.take<double>((size_t)nv * N);
   c->partial = k.take<double>(3 * 512);
   c->norms = k.take<double>(4);
+  // 2-D wavefront path buffers (csb_wave.cuh): strip-skewed planes
+  c->wave_ok = false;
+  if (c->g.nk == 1) {
+    Skew sk;
+    sk.ni = c->g.ni;
+    sk.nj = c->g.nj;
+    sk.nstrip = (c->g.nj + 31) / 32;
+    sk.T = ((c->g.ni + 31 + 3) / 4) * 4;
+    sk.Np = (long long)sk.nstrip * sk.T * 32 + 4 * 32 * 2;
+    const int nrec = nv + 1 + ns + 29;
+    c->wb.sk = sk;
+    c->wb.rec = k.take<double>((size_t)nrec * sk.Np);
+    c->wb.dqs = k.take<double>((size_t)nv * sk.Np);
+    c->wb.dqw = k.take<double>((size_t)nv * sk.Np);
+    c->wb.hand = k.take<double>((size_t)sk.nstrip * sk.ni * nv);
+    c->wb.prog = k.take<int>((size_t)sk.nstrip + 1);
+    c->wave_ok = true;
+  }
   return k.off;
 }
 
@@ -572,11 +593,41 @@ int csb_residual_norms(csb_ctx* c, long long N, const double* R, double* out3, v
                     "norms");
 }
 
+// path: 0 auto, 1 generic (hyperplane sweeps), 2 2-D wavefront
 static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cfl, int scheme,
-                         int offdiag_paper, const double* dOm_in, double* q_new, cudaStream_t st) {
+                         int offdiag_paper, const double* dOm_in, double* q_new, cudaStream_t st,
+                         int path = 0, double* dq_out = nullptr) {
   const bool chem = mech_of(c).nrx > 0;
   const bool full = chem && scheme == SCH_CI;
   if (full && !c->ws_block) return fail(c, CSB_E_STATE, "CI with chemistry needs block workspace");
+  const bool wave = path != 1 && c->wave_ok && !c->wave_disabled && scheme != SCH_CI &&
+                    c->geom2d_ok;
+  if (path == 2 && !wave) return fail(c, CSB_E_STATE, "2-D wavefront path not applicable");
+  if (wave) {
+    cudaError_t e = cudaSuccess;
+    const double* lamS = nullptr;
+    const double* domd = nullptr;
+    int dstride = 1;
+    if (chem) {
+      OpDev& op = c->op;
+      op.dom_full = c->ws_block ? 1 : 0;
+      e = launch_source_jacobian(c->d_model, c->ns, c->g, mech_of(c), q, op.dom, op.dom_full,
+                                 op.lamS, dOm_in, c->flags, st);
+      lamS = op.lamS;
+      domd = op.dom;
+      dstride = op.dom_full ? c->ns + 1 : 1;
+    }
+    if (e == cudaSuccess)
+      e = launch_wave_step(c->d_model, c->ns, c->g, c->wb, q, R, cfl, lamS, domd, dstride,
+                           chem ? 1 : 0, scheme, offdiag_paper ? 1.0 : 0.5, q_new, dq_out, c->flags,
+                           st);
+    if (e == cudaErrorInvalidConfiguration && path == 0) {
+      c->wave_disabled = 1;  // ring does not fit shared memory: generic path
+      cudaGetLastError();
+    } else {
+      return cuda_check(c, e, "implicit step (wavefront)");
+    }
+  }
   int r = time_step_impl(c, q, cfl, dOm_in, c->dtau, full, st);
   if (r) return r;
   OpDev& op = c->op;
@@ -584,12 +635,21 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
   r = assemble_impl(c, q, c->dtau, scheme, offdiag_paper, 0.0, 0.0, dOm_in, true, st);
   if (r) return r;
   // rhs = -R: the sweeps negate on load (exact)
-  cudaError_t e = cudaMemsetAsync(c->dq, 0, sizeof(double) * (5 + c->ns) * c->g.N, st);
+  double* dq = dq_out ? dq_out : c->dq;
+  cudaError_t e = cudaMemsetAsync(dq, 0, sizeof(double) * (5 + c->ns) * c->g.N, st);
   op.neg_rhs = 1;
-  if (e == cudaSuccess) e = launch_sweeps(c->d_model, c->ns, c->g, op, R, c->dq, nullptr, c->flags, st);
+  if (e == cudaSuccess) e = launch_sweeps(c->d_model, c->ns, c->g, op, R, dq, nullptr, c->flags, st);
   op.neg_rhs = 0;
-  if (e == cudaSuccess) e = launch_update(c->d_model, c->ns, c->g, scheme, q, c->dq, q_new, c->flags, st);
+  if (e == cudaSuccess) e = launch_update(c->d_model, c->ns, c->g, scheme, q, dq, q_new, c->flags, st);
   return cuda_check(c, e, "implicit step");
+}
+
+int csb_implicit_step_ex(csb_ctx* c, const double* q, const double* R, double cfl, int scheme,
+                         int offdiag_paper, const double* dOm_in, double* q_new, double* dq_out,
+                         int path, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  return implicit_impl(c, q, R, cfl, scheme, offdiag_paper, dOm_in, q_new, S(stream), path, dq_out);
 }
 
 int csb_implicit_step(csb_ctx* c, const double* q, const double* R, double cfl, int scheme,

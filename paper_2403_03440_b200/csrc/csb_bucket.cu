@@ -7,3 +7,4 @@
 #include "csb_implicit.cuh"
 #include "csb_sweep.cuh"
 #include "csb_update.cuh"
+#include "csb_wave.cuh"

@@ -34,7 +34,11 @@ unsigned long long launch_count() { return g_launches.load(std::memory_order_rel
   cudaError_t launch_update_b##b(const Model*, int, const GridDev&, int, const double*,            \
                                  const double*, double*, unsigned long long*, cudaStream_t);       \
   cudaError_t launch_export_op_b##b(const Model*, int, const GridDev&, const OpDev&,               \
-                                    const double*, int, double*, cudaStream_t);
+                                    const double*, int, double*, cudaStream_t);                    \
+  cudaError_t launch_wave_step_b##b(const Model*, int, const GridDev&, const WaveBufs&,            \
+                                    const double*, const double*, double, const double*,           \
+                                    const double*, int, int, int, double, double*, double*,        \
+                                    unsigned long long*, cudaStream_t);
 CSB_BUCKET_LIST(CSB_DECL)
 #undef CSB_DECL
 
@@ -108,6 +112,16 @@ cudaError_t launch_export_op(const Model* mdl, int ns, const GridDev& g, const O
                              const double* q, int what, double* dst, cudaStream_t st) {
   note_launches(1);
   CSB_ROUTE(launch_export_op, mdl, ns, g, op, q, what, dst, st)
+}
+
+cudaError_t launch_wave_step(const Model* mp, int ns, const GridDev& g, const WaveBufs& wb,
+                             const double* q, const double* R, double cfl, const double* lamS,
+                             const double* domd, int dom_stride, int per_species, int scheme,
+                             double sp_scale, double* qn, double* dq_std,
+                             unsigned long long* flags, cudaStream_t st) {
+  note_launches(4);
+  CSB_ROUTE(launch_wave_step, mp, ns, g, wb, q, R, cfl, lamS, domd, dom_stride, per_species, scheme,
+            sp_scale, qn, dq_std, flags, st)
 }
 
 }  // namespace csb

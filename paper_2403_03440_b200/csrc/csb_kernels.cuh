@@ -34,6 +34,28 @@ struct OpDev {
   int neg_rhs;         // sweeps use rhs = -input (the residual R)
 };
 
+// Strip-skewed 2-D layout of the wavefront path (csb_wave.cuh): cell (i, j)
+// at ((j>>5)*T + i + (j&31))*32 + (j&31).
+struct Skew {
+  int ni, nj, nstrip, T;
+  long long Np;  // plane stride (padded)
+};
+
+struct WaveBufs {
+  Skew sk;
+  double* rec;   // sweep records [nrec][Np]
+  double* dqs;   // forward output dq* [nv][Np]
+  double* dqw;   // backward output dq [nv][Np]
+  double* hand;  // strip hand-off [nstrip][ni][nv]
+  int* prog;     // [nstrip + 1] progress flags + ticket
+};
+
+cudaError_t launch_wave_step(const Model* mp, int ns, const GridDev& g, const WaveBufs& wb,
+                             const double* q, const double* R, double cfl, const double* lamS,
+                             const double* domd, int dom_stride, int per_species, int scheme,
+                             double sp_scale, double* qn, double* dq_std,
+                             unsigned long long* flags, cudaStream_t st);
+
 cudaError_t launch_residual(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                             const Mech& mech, const double* q, double* R, int first_order, bool k2d,
                             unsigned long long* flags, cudaStream_t st);

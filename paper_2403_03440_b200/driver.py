@@ -318,10 +318,11 @@ def _implicit_step(case, q, R, cfl, theta=0.0, dt=None, q_n=None, q_nm1=None):
     return eng.from_soa(out, q, tuple(eng.dims) + (eng.nv,)), secs
 
 
-def implicit_step_raw(case, q, R, cfl, dom_override=None):
+def implicit_step_raw(case, q, R, cfl, dom_override=None, path=0, want_dq=False):
     """Fused implicit step that reports instead of raising:
-    returns (q_new, flags, gate_count, first_bad_cell).  ``dom_override``
-    injects dOmega (..., ns, ns)."""
+    returns (q_new, flags, gate_count, first_bad_cell) [+ dq].
+    ``dom_override`` injects dOmega (..., ns, ns); ``path``: 0
+    auto, 1 generic hyperplane sweeps, 2 the 2-D wavefront path."""
     st = _Stepper(case)
     eng = st.eng
     qs = eng.to_soa(q, eng.nv)
@@ -331,14 +332,20 @@ def implicit_step_raw(case, q, R, cfl, dom_override=None):
         dom = eng.to_soa(np.asarray(dom_override, float).reshape(tuple(eng.dims) + (eng.ns ** 2,)),
                          eng.ns ** 2)
     out = eng.empty(eng.nv, eng.N)
-    eng._chk(eng.lib.csb_implicit_step(eng.ctx, qs.data_ptr(), Rs.data_ptr(), float(cfl),
-                                       st.scheme, st.paper,
-                                       dom.data_ptr() if dom is not None else None,
-                                       out.data_ptr(), ctypes.c_void_p(eng.stream)),
+    dqo = eng.empty(eng.nv, eng.N) if want_dq else None
+    eng._chk(eng.lib.csb_implicit_step_ex(eng.ctx, qs.data_ptr(), Rs.data_ptr(), float(cfl),
+                                          st.scheme, st.paper,
+                                          dom.data_ptr() if dom is not None else None,
+                                          out.data_ptr(), dqo.data_ptr() if dqo is not None else None,
+                                          int(path), ctypes.c_void_p(eng.stream)),
              "_implicit_step")
     flags, cell, cnt = eng.status()
     like = q if is_torch(q) else np.empty(0)
-    return eng.from_soa(out, like, tuple(eng.dims) + (eng.nv,)), flags & ~F_KSKIP, cnt, cell
+    shape = tuple(eng.dims) + (eng.nv,)
+    res = (eng.from_soa(out, like, shape), flags & ~F_KSKIP, cnt, cell)
+    if want_dq:
+        res = res + (eng.from_soa(dqo, like, shape),)
+    return res
 
 
 def _step_device(st, q_t, R_t, cfl, out_t):

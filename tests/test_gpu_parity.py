@@ -163,3 +163,33 @@ def test_config3_species_vs_oracle():
     from paper_2403_03440_b200 import configs as C
     for ns in (11, 20):
         _full_iteration_vs_oracle(C.config3(ns, dims=(40, 32, 1)), ("CS1", "CI"))
+
+
+# ---------------------------------------------------------------- 2-D wavefront path
+
+def _wave_vs_generic(spec, scheme, tol=1e-12):
+    from paper_2403_03440_b200 import driver, spatial
+    from paper_2403_03440_b200.configs import build_case
+    grid, model, bcs, mech = build_case(spec)
+    R = spatial.assemble_residual(spec.q, grid, bcs, mech, model)
+    case = driver.Case(grid=grid, model=model, bcs=bcs, freestream=None, mech=mech, scheme=scheme,
+                       cfl=spec.cfl)
+    qg, fg, cg, _, dg = driver.implicit_step_raw(case, spec.q, R, spec.cfl, path=1, want_dq=True)
+    qw, fw, cw, _, dw = driver.implicit_step_raw(case, spec.q, R, spec.cfl, path=2, want_dq=True)
+    assert comp_relerr(dw, dg) <= tol
+    assert comp_relerr(qw - spec.q, qg - spec.q) <= tol
+    assert (fw, cw) == (fg, cg)
+
+
+@pytest.mark.parametrize("dims", [(64, 64, 1), (40, 45, 1), (3, 70, 1), (50, 7, 1), (33, 96, 1)])
+@pytest.mark.parametrize("scheme", ["CS1", "CS2"])
+def test_wavefront_matches_generic_box(dims, scheme):
+    from paper_2403_03440_b200 import configs as C
+    _wave_vs_generic(C.config0(seed=7, dims=dims), scheme)
+
+
+def test_wavefront_matches_generic_ogrid_and_chemistry():
+    from paper_2403_03440_b200 import configs as C
+    _wave_vs_generic(C.config2(seed=2, dims=(48, 40, 1)), "CS1")
+    _wave_vs_generic(C.config3(20, dims=(24, 40, 1), chemistry=True), "CS1")
+    _wave_vs_generic(C.config3(40, dims=(24, 36, 1)), "CS2")
