@@ -156,34 +156,33 @@ class Runner:
             raise RuntimeError(self.lib.csb_last_error(e.ctx))
 
     def stages(self, reps=3):
-        """Per-stage device time (ms), instrumented pass outside the timed region."""
+        """Per-stage device time (ms) of the production path (2-D wavefront),
+        instrumented pass outside the timed region."""
         torch, e, lib, st = self.torch, self.eng, self.lib, self.stream
-        names = ["rhs", "norms", "dtau", "assemble", "sweeps", "update"]
+        names = ["rhs", "norms", "srcjac", "records", "sweep_fwd", "sweep_bwd", "epilogue"]
         acc = {n: 0.0 for n in names}
-        dq = e.empty(e.nv, e.N)
-        dtau = e.empty(e.N)
+        ms5 = (ctypes.c_float * 5)()
         for _ in range(reps):
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             ev[0].record()
             lib.csb_residual(e.ctx, self.q.data_ptr(), self.R.data_ptr(), None, 0, st)
             ev[1].record()
             lib.csb_residual_norms(e.ctx, e.N, self.R.data_ptr(), self.norms.data_ptr(), st)
             ev[2].record()
-            lib.csb_time_step(e.ctx, self.q.data_ptr(), float(self.spec.cfl), None, dtau.data_ptr(), st)
-            ev[3].record()
-            lib.csb_assemble(e.ctx, self.q.data_ptr(), dtau.data_ptr(), self.scheme, 0, 0.0, -1.0,
-                             None, st)
-            ev[4].record()
-            lib.csb_lusgs(e.ctx, self.R.data_ptr(), dq.data_ptr(), None, st)
-            ev[5].record()
-            lib.csb_apply_update(e.ctx, e.N, self.q.data_ptr(), dq.data_ptr(), self.scheme,
-                                 self.qn.data_ptr(), st)
-            ev[6].record()
             torch.cuda.synchronize()
-            for i, n in enumerate(names):
-                acc[n] += ev[i].elapsed_time(ev[i + 1])
+            acc["rhs"] += ev[0].elapsed_time(ev[1])
+            acc["norms"] += ev[1].elapsed_time(ev[2])
+            rc = lib.csb_profile_step(e.ctx, self.q.data_ptr(), self.R.data_ptr(),
+                                      float(self.spec.cfl), self.scheme, self.qn.data_ptr(), ms5, st)
+            if rc:
+                raise RuntimeError(lib.csb_last_error(e.ctx))
+            for k, n in enumerate(names[2:]):
+                acc[n] += ms5[k]
         e.status()
-        return {n: acc[n] / reps for n in names}
+        out = {n: acc[n] / reps for n in names}
+        out["sweeps"] = out["sweep_fwd"] + out["sweep_bwd"]
+        out["assemble"] = out["srcjac"] + out["records"]
+        return out
 
 
 def flush_buffer(torch):
@@ -387,9 +386,8 @@ def main():
     stages = run.stages()
     ab = algorithmic_bytes(nv)
     peak, peak_src = peaks()
-    dom = max(("rhs", "sweeps", "assemble"), key=lambda k: stages[k] if k != "assemble"
-              else stages["assemble"] + stages["dtau"])
-    dom_ms = stages[dom] if dom != "assemble" else stages["assemble"] + stages["dtau"]
+    dom = max(("rhs", "sweeps", "assemble"), key=lambda k: stages[k])
+    dom_ms = stages[dom]
     bytes_dom = N * ab[dom] * 8
     achieved = bytes_dom / (dom_ms * 1e-3) / 1e9
     traffic = None

@@ -187,6 +187,11 @@ int csb_implicit_step_ex(csb_ctx* ctx, const double* q, const double* R, double 
                          int offdiag_paper, const double* dOm_in, double* q_new, double* dq_out,
                          int path, void* stream);
 
+/* Instrumented 2-D wavefront implicit step: ms5 = {source Jacobian, records,
+ * forward sweep, backward sweep, epilogue} device milliseconds (synchronises). */
+int csb_profile_step(csb_ctx* ctx, const double* q, const double* R, double cfl, int scheme,
+                     double* q_new, float* ms5, void* stream);
+
 /* One steady iteration (driver.py:279-308 without the retry/stop logic):
  * R = residual(q) (R_out nullable: internal), norms -> norms3 (device,
  * nullable), q_new = implicit step. */

@@ -50,6 +50,7 @@ SIGNATURES = {
     "csb_correct": (_i, [_p, _i, _ll, _i, _dp, _dp, _dp, _dp, _p]),
     "csb_residual_norms": (_i, [_p, _ll, _dp, _dp, _p]),
     "csb_implicit_step": (_i, [_p, _dp, _dp, _d, _i, _i, _dp, _dp, _p]),
+    "csb_profile_step": (_i, [_p, _dp, _dp, _d, _i, _dp, ctypes.POINTER(ctypes.c_float), _p]),
     "csb_implicit_step_ex": (_i, [_p, _dp, _dp, _d, _i, _i, _dp, _dp, _dp, _i, _p]),
     "csb_iteration": (_i, [_p, _dp, _d, _i, _i, _i, _dp, _dp, _dp, _p]),
     "csb_transpose": (_i, [_ll, _i, _dp, _dp, _i, _p]),

@@ -175,10 +175,11 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
     sk.nj = c->g.nj;
     sk.nstrip = (c->g.nj + 31) / 32;
     sk.T = ((c->g.ni + 31 + 3) / 4) * 4;
-    sk.Np = (long long)sk.nstrip * sk.T * 32 + 4 * 32 * 2;
-    const int nrec = nv + 1 + ns + 29;
+    sk.Np = (long long)sk.nstrip * sk.T * 32;  // cells per plane (step-major groups)
     c->wb.sk = sk;
-    c->wb.rec = k.take<double>((size_t)nrec * sk.Np);
+    c->wb.recC = k.take<double>((size_t)(14 + ns) * sk.Np);
+    c->wb.recF = k.take<double>((size_t)(nv + 8) * sk.Np);
+    c->wb.recB = k.take<double>((size_t)8 * sk.Np);
     c->wb.dqs = k.take<double>((size_t)nv * sk.Np);
     c->wb.dqw = k.take<double>((size_t)nv * sk.Np);
     c->wb.hand = k.take<double>((size_t)sk.nstrip * sk.ni * nv);
@@ -377,6 +378,15 @@ int csb_set_workspace(csb_ctx* c, void* dev, size_t bytes) {
   c->ws_bytes = bytes;
   c->has_ws = true;
   c->assembled_scheme = -1;
+  if (c->wave_ok) {
+    // wavefront padding slots (t - r outside [0, ni), rows beyond nj) are never
+    // written by the records kernel: they must hold zeros so that padding
+    // cells contribute exactly nothing to the sweep (csb_wave.cuh)
+    const int nv = 5 + c->ns;
+    const size_t planes = (size_t)(14 + c->ns) + (nv + 8) + 8 + 2 * (size_t)nv;
+    if (cudaMemset(c->wb.recC, 0, planes * c->wb.sk.Np * sizeof(double)) != cudaSuccess)
+      return fail(c, CSB_E_CUDA, "zero wavefront records");
+  }
   return reset_flags(c, 0) ? CSB_E_CUDA : (cudaDeviceSynchronize() == cudaSuccess ? CSB_OK : CSB_E_CUDA);
 }
 
@@ -596,7 +606,7 @@ int csb_residual_norms(csb_ctx* c, long long N, const double* R, double* out3, v
 // path: 0 auto, 1 generic (hyperplane sweeps), 2 2-D wavefront
 static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cfl, int scheme,
                          int offdiag_paper, const double* dOm_in, double* q_new, cudaStream_t st,
-                         int path = 0, double* dq_out = nullptr) {
+                         int path = 0, double* dq_out = nullptr, cudaEvent_t* ev = nullptr) {
   const bool chem = mech_of(c).nrx > 0;
   const bool full = chem && scheme == SCH_CI;
   if (full && !c->ws_block) return fail(c, CSB_E_STATE, "CI with chemistry needs block workspace");
@@ -620,7 +630,7 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
     if (e == cudaSuccess)
       e = launch_wave_step(c->d_model, c->ns, c->g, c->wb, q, R, cfl, lamS, domd, dstride,
                            chem ? 1 : 0, scheme, offdiag_paper ? 1.0 : 0.5, q_new, dq_out, c->flags,
-                           st);
+                           st, ev);
     if (e == cudaErrorInvalidConfiguration && path == 0) {
       c->wave_disabled = 1;  // ring does not fit shared memory: generic path
       cudaGetLastError();
@@ -642,6 +652,24 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
   op.neg_rhs = 0;
   if (e == cudaSuccess) e = launch_update(c->d_model, c->ns, c->g, scheme, q, dq, q_new, c->flags, st);
   return cuda_check(c, e, "implicit step");
+}
+
+int csb_profile_step(csb_ctx* c, const double* q, const double* R, double cfl, int scheme,
+                     double* q_new, float* ms5, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  cudaStream_t st = S(stream);
+  cudaEvent_t ev[6];
+  for (int k = 0; k < 6; ++k) cudaEventCreate(&ev[k]);
+  cudaEventRecord(ev[5], st);
+  r = implicit_impl(c, q, R, cfl, scheme, 0, nullptr, q_new, st, 2, nullptr, ev);
+  if (r == CSB_OK) {
+    cudaStreamSynchronize(st);
+    cudaEventElapsedTime(&ms5[0], ev[5], ev[0]);  // source Jacobian (chemistry) / launch gap
+    for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&ms5[1 + k], ev[k], ev[k + 1]);
+  }
+  for (int k = 0; k < 6; ++k) cudaEventDestroy(ev[k]);
+  return r;
 }
 
 int csb_implicit_step_ex(csb_ctx* c, const double* q, const double* R, double cfl, int scheme,

@@ -38,7 +38,7 @@ unsigned long long launch_count() { return g_launches.load(std::memory_order_rel
   cudaError_t launch_wave_step_b##b(const Model*, int, const GridDev&, const WaveBufs&,            \
                                     const double*, const double*, double, const double*,           \
                                     const double*, int, int, int, double, double*, double*,        \
-                                    unsigned long long*, cudaStream_t);
+                                    unsigned long long*, cudaStream_t, cudaEvent_t*);
 CSB_BUCKET_LIST(CSB_DECL)
 #undef CSB_DECL
 
@@ -118,10 +118,10 @@ cudaError_t launch_wave_step(const Model* mp, int ns, const GridDev& g, const Wa
                              const double* q, const double* R, double cfl, const double* lamS,
                              const double* domd, int dom_stride, int per_species, int scheme,
                              double sp_scale, double* qn, double* dq_std,
-                             unsigned long long* flags, cudaStream_t st) {
+                             unsigned long long* flags, cudaStream_t st, cudaEvent_t* ev) {
   note_launches(4);
   CSB_ROUTE(launch_wave_step, mp, ns, g, wb, q, R, cfl, lamS, domd, dom_stride, per_species, scheme,
-            sp_scale, qn, dq_std, flags, st)
+            sp_scale, qn, dq_std, flags, st, ev)
 }
 
 }  // namespace csb

@@ -43,9 +43,11 @@ struct Skew {
 
 struct WaveBufs {
   Skew sk;
-  double* rec;   // sweep records [nrec][Np]
-  double* dqs;   // forward output dq* [nv][Np]
-  double* dqw;   // backward output dq [nv][Np]
+  double* recC;  // sweep records, group C (both sweeps), step-major
+  double* recF;  // group F (forward: rhs + upper faces)
+  double* recB;  // group B (backward: lower faces)
+  double* dqs;   // forward output dq* [step-major, nv planes]
+  double* dqw;   // backward output dq
   double* hand;  // strip hand-off [nstrip][ni][nv]
   int* prog;     // [nstrip + 1] progress flags + ticket
 };
@@ -54,7 +56,8 @@ cudaError_t launch_wave_step(const Model* mp, int ns, const GridDev& g, const Wa
                              const double* q, const double* R, double cfl, const double* lamS,
                              const double* domd, int dom_stride, int per_species, int scheme,
                              double sp_scale, double* qn, double* dq_std,
-                             unsigned long long* flags, cudaStream_t st);
+                             unsigned long long* flags, cudaStream_t st,
+                             cudaEvent_t* ev = nullptr);
 
 cudaError_t launch_residual(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                             const Mech& mech, const double* q, double* R, int first_order, bool k2d,

@@ -2,31 +2,35 @@
 //
 //   k_records2d  : fused local time step + CS operator assembly (reference
 //                  implicit.py:33-44, 144-197, 329-403), written as "sweep
-//                  records" in the strip-skewed layout below;
+//                  records" in the strip-skewed, step-major layout below;
 //   k_wave2d<F/B>: the LU-SGS forward / backward sweep (lusgs.py:150-247) as
 //                  a pipelined wavefront over 32-row strips;
 //   k_epilogue2d : species closure CS1/CS2 + admissibility gate
 //                  (driver.py:216-229, 250; implicit.py:113-141).
 //
-// Strip-skewed layout.  Rows j are grouped in strips of 32 (s = j >> 5,
-// r = j & 31).  Cell (i, j) lives at physical index ((s*T + t)*32 + r) with
-// t = i + r, T = ni + 31 rounded up to a multiple of WK.  At wavefront step t
-// of strip s, row r processes column i = t - r, so the 32 cells of one step
-// are 32 consecutive doubles in every record plane: the sweep streams its
-// inputs with 1 KiB TMA bulk copies (4 steps per copy) and writes its output
-// coalesced.  The backward sweep visits the same physical steps in reverse
-// (cell (i, j) of the backward step for slot t is the same cell), so it
-// reads dq* and the records with the same contiguous copies.
+// Strip-skewed, step-major layout.  Rows j are grouped in strips of 32
+// (s = j >> 5, r = j & 31).  At wavefront step t of strip s, row r processes
+// column i = t - r.  A record group with NG planes stores plane p of cell
+// (i, j) at ((s*T + t)*NG + p)*32 + r with t = i + r (T = ni + 31 rounded up
+// to a multiple of WK).  WK consecutive steps of one strip are therefore one
+// contiguous block of WK*NG*32 doubles: the sweep streams each group with a
+// single TMA bulk copy per WK steps into an mbarrier ring.  The backward sweep
+// visits the same physical steps in reverse (backward slot t holds the same
+// cells), so it streams the same blocks in reverse order.
+//
+// Record groups: C (both sweeps) = invd, invs[nsI], w[5], b[5], u, v, hr;
+// F (forward) = rhs[nv], upper-i face (Sx, Sy, lam, lamsp), upper-j face;
+// B (backward) = lower-i face, lower-j face; Q = dq* (forward output,
+// backward input); W = dq (backward output).
 //
 // One CTA per strip (dynamic ticket => deadlock-free ordering):
 //   warp 0: flow chain (5 components, rank-2 half-block products),
 //   warp 1: species chain (ns scalar chains),
-//   warp 2: producer (TMA bulk copies into an mbarrier ring + the upstream
-//           strip's hand-off values, polled from L2),
+//   warp 2: producer (TMA bulk copies + the upstream strip's hand-off values,
+//           polled from L2),
 //   warp 3: publisher (this strip's hand-off row to L2 + progress flag).
 // Row r hands its j-direction contribution to row r+1 (r-1 backward) with a
-// warp shuffle; strip boundaries go through L2.  The chains never touch
-// global memory except coalesced output stores.
+// warp shuffle; strip boundaries go through L2.
 #pragma once
 
 #include "csb_common.cuh"
@@ -37,29 +41,22 @@ namespace csb {
 constexpr int WK = 4;          // wavefront steps per ring slot
 constexpr int HRING = 64;      // hand-off ring (columns)
 
-// record planes (plane stride Np): rhs[nv], invd, invs[nsI], w[5], b[5],
-// uv[2], hr, fiu[4], fju[4], fil[4], fjl[4]  (face data: Sx, Sy, lam, lamsp)
 struct RecMap {
   int nv, nsI;
-  CSB_DEV int invd() const { return nv; }
-  CSB_DEV int invs() const { return nv + 1; }
-  CSB_DEV int w() const { return nv + 1 + nsI; }
+  // group C
+  CSB_DEV int invd() const { return 0; }
+  CSB_DEV int invs() const { return 1; }
+  CSB_DEV int w() const { return 1 + nsI; }
   CSB_DEV int b() const { return w() + 5; }
   CSB_DEV int uv() const { return w() + 10; }
   CSB_DEV int hr() const { return w() + 12; }
-  CSB_DEV int fiu() const { return w() + 13; }
-  CSB_DEV int fju() const { return w() + 17; }
-  CSB_DEV int fil() const { return w() + 21; }
-  CSB_DEV int fjl() const { return w() + 25; }
-  CSB_DEV int nrec() const { return w() + 29; }
-  CSB_DEV int nring() const { return w() + 21; }  // planes streamed per sweep
+  CSB_DEV int nc() const { return w() + 13; }
+  // group F: rhs[nv], fi[4], fj[4]; group B: fi[4], fj[4]
+  CSB_DEV int nf() const { return nv + 8; }
 };
 
-
 // ---------------------------------------------------------------- PTX helpers
-CSB_DEV unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
+CSB_DEV unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 CSB_DEV void mbar_init(unsigned long long* b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
 }
@@ -68,6 +65,11 @@ CSB_DEV void mbar_arrive(unsigned long long* b) {
 }
 CSB_DEV void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+CSB_DEV void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)),
                "r"(bytes)
                : "memory");
 }
@@ -86,6 +88,11 @@ CSB_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long 
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+CSB_DEV int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 CSB_DEV int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -95,6 +102,11 @@ CSB_DEV void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 CSB_DEV int ld_volatile_s(const int* p) { return *(volatile const int*)p; }
+
+// step-major group address of (strip s, step t, plane p, row r)
+CSB_DEV long long gaddr(const Skew& k, int NG, int s, int t, int p, int r) {
+  return (((long long)s * k.T + t) * NG + p) * 32 + r;
+}
 
 // ============================================================== records
 // Tile = one strip (32 rows) x C columns.  Phase A: per cell (tile + 1-cell
@@ -107,19 +119,24 @@ __global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp,
                                                    const double* __restrict__ R, double cfl,
                                                    const double* __restrict__ lamS,
                                                    const double* __restrict__ domd, int dom_stride,
-                                                   int per_species, double* __restrict__ rec, int C,
+                                                   int per_species, double* __restrict__ recC,
+                                                   double* __restrict__ recF,
+                                                   double* __restrict__ recB, int C,
                                                    unsigned long long* flags) {
   extern __shared__ double sm[];
   const Model& m = *mp;
   const int ns = m.ns, nv = 5 + ns, nsI = per_species ? ns : 1;
   RecMap rm{nv, nsI};
-  const int nrec = rm.nrec();
+  const int NC = rm.nc(), NF = rm.nf();
   const int ncb = (g.ni + C - 1) / C;
   const int s = blockIdx.x / ncb, ib = blockIdx.x % ncb;
   const int i0 = ib * C, j0 = s * 32;
   const int HX = C + 2, HY = 34, NH = HX * HY;
-  double* A = sm;                   // [6][NH]: u, v, w, c, nf, nsp   (+ V in [6])
-  double* Bv = sm + 7 * NH;         // [nrec][C*32]
+  const int CT = C * 32;
+  double* A = sm;            // [7][NH]: u, v, w, c, nf, nsp, V
+  double* BC = sm + 7 * NH;  // [NC][CT] | [NF][CT] | [8][CT]
+  double* BF = BC + (long long)NC * CT;
+  double* BB = BF + (long long)NF * CT;
   const long long N = g.N;
   // ---------------- phase A: halo-extended per-cell quantities
   for (int l = threadIdx.x; l < NH; l += blockDim.x) {
@@ -144,7 +161,6 @@ __global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp,
     if (!inner) continue;
     if (!ok) raise_flag(flags, EB_DECODE, c);
     const int e = (hx - 1) * 32 + (hy - 1);  // tile-local cell (column-major by i)
-    const int CT = C * 32;
     // cell radii at the cell-averaged metric, dtau (implicit.py:152-163, 33-44)
     double li[3], lv[3], rf = 0.0, rsp = 0.0;
 #pragma unroll
@@ -175,46 +191,44 @@ __global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp,
     const double base = V / dtau;
     const double dflow = base + rf;
     bool bad = !(fabs(dflow) >= 1e-300) || !isfinite(dflow);
-    Bv[rm.invd() * CT + e] = 1.0 / dflow;
+    BC[rm.invd() * CT + e] = 1.0 / dflow;
     const double dsp0 = base + rsp;
     if (per_species) {
       for (int sp = 0; sp < ns; ++sp) {
         const double v = dsp0 - domd[(long long)sp * dom_stride * N + c] * V;
         bad |= !(fabs(v) >= 1e-300) || !isfinite(v);
-        Bv[(rm.invs() + sp) * CT + e] = 1.0 / v;
+        BC[(rm.invs() + sp) * CT + e] = 1.0 / v;
       }
     } else {
       bad |= !(fabs(dsp0) >= 1e-300) || !isfinite(dsp0);
-      Bv[rm.invs() * CT + e] = 1.0 / dsp0;
+      BC[rm.invs() * CT + e] = 1.0 / dsp0;
     }
     if (bad) raise_flag(flags, EB_SINGULAR, c);
-    for (int k = 0; k < nv; ++k) Bv[k * CT + e] = -R[(long long)k * N + c];
+    for (int k = 0; k < nv; ++k) BF[k * CT + e] = -R[(long long)k * N + c];
     const double beta = cs.gamma - 1.0;
     const int pw = rm.w(), pb = rm.b();
-    Bv[(pw + 0) * CT + e] = cs.rho;
-    Bv[(pw + 1) * CT + e] = cs.rho * cs.u[0];
-    Bv[(pw + 2) * CT + e] = cs.rho * cs.u[1];
-    Bv[(pw + 3) * CT + e] = cs.rho * cs.u[2];
-    Bv[(pw + 4) * CT + e] = cs.rho * cs.h;
-    Bv[(pb + 0) * CT + e] = beta * cs.Ek;
-    Bv[(pb + 1) * CT + e] = -beta * cs.u[0];
-    Bv[(pb + 2) * CT + e] = -beta * cs.u[1];
-    Bv[(pb + 3) * CT + e] = -beta * cs.u[2];
-    Bv[(pb + 4) * CT + e] = beta;
-    Bv[(rm.uv() + 0) * CT + e] = cs.u[0];
-    Bv[(rm.uv() + 1) * CT + e] = cs.u[1];
-    Bv[rm.hr() * CT + e] = 0.5 / cs.rho;
+    BC[(pw + 0) * CT + e] = cs.rho;
+    BC[(pw + 1) * CT + e] = cs.rho * cs.u[0];
+    BC[(pw + 2) * CT + e] = cs.rho * cs.u[1];
+    BC[(pw + 3) * CT + e] = cs.rho * cs.u[2];
+    BC[(pw + 4) * CT + e] = cs.rho * cs.h;
+    BC[(pb + 0) * CT + e] = beta * cs.Ek;
+    BC[(pb + 1) * CT + e] = -beta * cs.u[0];
+    BC[(pb + 2) * CT + e] = -beta * cs.u[1];
+    BC[(pb + 3) * CT + e] = -beta * cs.u[2];
+    BC[(pb + 4) * CT + e] = beta;
+    BC[(rm.uv() + 0) * CT + e] = cs.u[0];
+    BC[(rm.uv() + 1) * CT + e] = cs.u[1];
+    BC[rm.hr() * CT + e] = 0.5 / cs.rho;
   }
   __syncthreads();
   // ---------------- phase B: face radii of the 4 faces of every tile cell
-  const int CT = C * 32;
   for (int e = threadIdx.x; e < CT; e += blockDim.x) {
     const int ii = e / 32, jj = e % 32;
     const int i = i0 + ii, j = j0 + jj;
     if (i >= g.ni || j >= g.nj) continue;
     const int hc = (ii + 1) * HY + (jj + 1);
     // faces: 0 upper-i (i+1), 1 upper-j (j+1), 2 lower-i (i), 3 lower-j (j)
-    const int planes[4] = {rm.fiu(), rm.fju(), rm.fil(), rm.fjl()};
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
       const int d = f & 1;
@@ -228,7 +242,6 @@ __global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp,
       load_S(g, d, face_index(g, d, fi, fj, 0), S);
       const double a2 = (S[0] * S[0] + S[1] * S[1]) + S[2] * S[2];
       const double ar = sqrt(a2);
-      // the two adjacent cells: (fi-1, fj) / (fi, fj) for d=0, etc.
       const int nb = upper ? (d == 0 ? hc + HY : hc + 1) : (d == 0 ? hc - HY : hc - 1);
       const bool nb_in = upper ? (d == 0 ? i + 1 < g.ni : j + 1 < g.nj) : (d == 0 ? i > 0 : j > 0);
       const int lo = upper ? hc : nb, hi = upper ? nb : hc;  // lower/upper cell of the face
@@ -245,28 +258,30 @@ __global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp,
         lf = lam(hc, false);
         ls = lam(hc, true);
       }
-      Bv[(planes[f] + 0) * CT + e] = S[0];
-      Bv[(planes[f] + 1) * CT + e] = S[1];
-      Bv[(planes[f] + 2) * CT + e] = lf;
-      Bv[(planes[f] + 3) * CT + e] = ls;
+      double* dst = upper ? BF + (long long)(nv + 4 * d) * CT : BB + (long long)(4 * d) * CT;
+      dst[0 * CT + e] = S[0];
+      dst[1 * CT + e] = S[1];
+      dst[2 * CT + e] = lf;
+      dst[3 * CT + e] = ls;
     }
   }
   __syncthreads();
-  // ---------------- phase C: skewed stores, one diagonal segment at a time
-  // the tile covers steps t in [i0, i0 + C + 31); element (t, r) <-> cell (t - r, r)
+  // ---------------- phase C: skewed step-major stores
+  // tile steps tt in [0, C + 31): element (tt, r) <-> cell (i0 + tt - r, j0 + r)
   const int nt = C + 31;
   for (int e = threadIdx.x; e < nt * 32; e += blockDim.x) {
     const int tt = e / 32, r = e % 32;
-    const int ii = tt - r;  // tile-local column
+    const int ii = tt - r;
     if (ii < 0 || ii >= C) continue;
     const int i = i0 + ii, j = j0 + r;
-    const long long dst = ((long long)s * sk.T + i + r) * 32 + r;
+    // cells outside the grid are padding slots: zeroed once at workspace
+    // setup and never written (i >= ni would also step past the strip)
+    if (i >= g.ni || j >= g.nj) continue;
+    const int t = i + r;
     const int el = ii * 32 + r;
-    if (i >= g.ni || j >= g.nj) {
-      for (int p = 0; p < nrec; ++p) rec[(long long)p * sk.Np + dst] = 0.0;
-    } else {
-      for (int p = 0; p < nrec; ++p) rec[(long long)p * sk.Np + dst] = Bv[p * CT + el];
-    }
+    for (int p = 0; p < NC; ++p) recC[gaddr(sk, NC, s, t, p, r)] = BC[p * CT + el];
+    for (int p = 0; p < NF; ++p) recF[gaddr(sk, NF, s, t, p, r)] = BF[p * CT + el];
+    for (int p = 0; p < 8; ++p) recB[gaddr(sk, 8, s, t, p, r)] = BB[p * CT + el];
   }
 }
 
@@ -274,9 +289,10 @@ __global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp,
 struct WaveArgs {
   Skew sk;
   int ni, nj, ns, nv, nsI, nslots, D;
-  const double* rec;
-  const double* dqs;   // backward: forward output (dq*)
-  double* out;         // forward: dq*; backward: dq
+  const double* recC;
+  const double* recX;  // forward: F group; backward: Q (dq*)
+  const double* recB;  // backward faces
+  double* out;         // forward: dq* (Q); backward: dq (W), step-major [nv]
   double* hand;        // [nstrip][ni][nv]
   int* prog;           // [nstrip]
   int* ticket;
@@ -291,12 +307,16 @@ __global__ void __launch_bounds__(128, 1) k_wave2d(WaveArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nv = a.nv, ns = a.ns, D = a.D;
   RecMap rm{nv, a.nsI};
-  const int NP = rm.nring();
-  const long long Np = a.sk.Np;
-  const int slot_dbl = NP * WK * 32;
-  double* ring = wsm;                                   // [D][NP][WK][32]
-  double* hin = ring + (long long)D * slot_dbl;         // [D][WK][nv]
-  double* hout = hin + D * WK * nv;                     // [HRING][nv]
+  const int NC = rm.nc();
+  const int NX = BWD ? nv : rm.nf();  // planes of the X group (rhs+faces | dq*)
+  const int NB = BWD ? 8 : 0;
+  const long long slotC = (long long)WK * NC * 32, slotX = (long long)WK * NX * 32,
+                  slotB = (long long)WK * NB * 32;
+  double* ringC = wsm;                // [D][WK][NC][32]
+  double* ringX = ringC + D * slotC;  // [D][WK][NX][32]
+  double* ringB = ringX + D * slotX;  // [D][WK][8][32] (backward)
+  double* hin = ringB + D * slotB;    // [D][WK][nv]
+  double* hout = hin + D * WK * nv;   // [HRING][nv]
   if (threadIdx.x == 0) {
     const int tk = atomicAdd(a.ticket, 1);
     s_strip = BWD ? a.sk.nstrip - 1 - tk : tk;
@@ -323,19 +343,25 @@ __global__ void __launch_bounds__(128, 1) k_wave2d(WaveArgs a) {
       const int k = BWD ? nslots - 1 - ks : ks;
       const int buf = ks % D;
       if (ks >= D) mbar_wait(&empty_bar[buf], ((ks / D) - 1) & 1);
+      if (lane == 0) {
+        // bulk copies first: they do not depend on the upstream strip
+        const unsigned bC = (unsigned)(slotC * 8), bX = (unsigned)(slotX * 8),
+                       bB = (unsigned)(slotB * 8);
+        mbar_expect_tx(&full_bar[buf], bC + bX + bB);
+        const long long st = (long long)s * T + (long long)k * WK;
+        bulk_g2s(ringC + buf * slotC, a.recC + st * NC * 32, bC, &full_bar[buf]);
+        bulk_g2s(ringX + buf * slotX, a.recX + st * NX * 32, bX, &full_bar[buf]);
+        if (BWD) bulk_g2s(ringB + buf * slotB, a.recB + st * 8 * 32, bB, &full_bar[buf]);
+      }
       // upstream hand-off for this slot's WK steps (first row's columns)
       double* hb = hin + buf * WK * nv;
       if (has_up) {
         int need;
-        if (!BWD) {
-          const int cmax = min(k * WK + WK - 1, a.ni - 1);  // first row = 0: col = t
-          need = cmax + 1;
-        } else {
-          const int cmin = max(k * WK - rt, 0);  // first row = rt: col = t - rt
-          need = a.ni - cmin;
-        }
+        if (!BWD) need = min(k * WK + WK - 1, a.ni - 1) + 1;  // first row 0: col = t
+        else need = a.ni - max(k * WK - rt, 0);               // first row rt: col = t - rt
         need = max(0, min(need, a.ni));
-        while (ld_acquire(a.prog + up) < need) __nanosleep(64);
+        while (ld_relaxed(a.prog + up) < need) __nanosleep(20);
+        (void)ld_acquire(a.prog + up);
         for (int e = lane; e < WK * nv; e += 32) {
           const int kk = e / nv, c = e % nv;
           const int t = k * WK + kk;
@@ -348,21 +374,7 @@ __global__ void __launch_bounds__(128, 1) k_wave2d(WaveArgs a) {
         for (int e = lane; e < WK * nv; e += 32) hb[e] = 0.0;
       }
       __syncwarp();
-      double* dst = ring + (long long)buf * slot_dbl;
-      const unsigned bytes = WK * 32 * sizeof(double);
-      if (lane == 0) {
-        mbar_arrive_tx(&full_bar[buf], bytes * NP);
-        const long long off = ((long long)s * T + (long long)k * WK) * 32;
-        for (int p = 0; p < NP; ++p) {
-          const double* src;
-          if (p < nv) src = (BWD ? a.dqs : a.rec) + (long long)p * Np;
-          else if (p < rm.fiu()) src = a.rec + (long long)p * Np;
-          else src = a.rec + (long long)(p + (BWD ? 8 : 0)) * Np;
-          bulk_g2s(dst + (long long)p * WK * 32, src + off, bytes, &full_bar[buf]);
-        }
-      } else {
-        mbar_arrive(&full_bar[buf]);
-      }
+      mbar_arrive(&full_bar[buf]);  // all 32 lanes, after their hand-off writes
     }
     return;
   }
@@ -376,8 +388,8 @@ __global__ void __launch_bounds__(128, 1) k_wave2d(WaveArgs a) {
       __threadfence_block();
       const int dn = min(d0, d1);
       int cnt;
-      if (!BWD) cnt = dn * WK - rt;                  // bottom..: cols < cnt done (top row rt)
-      else cnt = a.ni - (nslots - dn) * WK;          // bottom row 0: cols >= (nslots-dn)*WK done
+      if (!BWD) cnt = dn * WK - rt;          // cols < cnt done (top row rt: t = col + rt)
+      else cnt = a.ni - (nslots - dn) * WK;  // bottom row 0: cols >= (nslots-dn)*WK done
       cnt = max(0, min(cnt, a.ni));
       if (cnt > next) {
         for (int e = lane; e < (cnt - next) * nv; e += 32) {
@@ -390,7 +402,7 @@ __global__ void __launch_bounds__(128, 1) k_wave2d(WaveArgs a) {
         if (lane == 0) st_release(a.prog + s, cnt);
         next = cnt;
       } else {
-        __nanosleep(32);
+        __nanosleep(20);
       }
     }
     return;
@@ -399,9 +411,16 @@ __global__ void __launch_bounds__(128, 1) k_wave2d(WaveArgs a) {
   // -------------------------------------------------------- chains
   const unsigned FULL = 0xffffffffu;
   const double sgn = BWD ? -1.0 : 1.0;
-  const bool first = BWD ? (lane == rt) : (lane == 0);   // receives the upstream hand-off
-  const bool last = BWD ? (lane == 0) : (lane == rt);    // sends the downstream hand-off
-  const int pF1 = rm.fiu(), pF2 = rm.fju();               // ring positions of the two faces
+  const bool first = BWD ? (lane == rt) : (lane == 0);  // receives the upstream hand-off
+  const bool last = BWD ? (lane == 0) : (lane == rt);   // sends the downstream hand-off
+  const bool row_ok = j0 + lane < a.nj;
+  auto real = [&](int t) { return row_ok && t - lane >= 0 && t - lane < a.ni; };
+  // plane pointers inside a slot: C group, X group (rhs|dq*), faces (F tail | B)
+  auto slot_ptrs = [&](int buf, int kk, const double*& pc, const double*& px, const double*& pfc) {
+    pc = ringC + buf * slotC + (long long)kk * NC * 32 + lane;
+    px = ringX + buf * slotX + (long long)kk * NX * 32 + lane;
+    pfc = BWD ? ringB + buf * slotB + (long long)kk * 8 * 32 + lane : px + (long long)nv * 32;
+  };
   if (warp == 0) {
     // ------------------------------ flow chain: 5 components per row
     double oi[5] = {0, 0, 0, 0, 0}, oj[5] = {0, 0, 0, 0, 0};
@@ -409,13 +428,13 @@ __global__ void __launch_bounds__(128, 1) k_wave2d(WaveArgs a) {
       const int k = BWD ? nslots - 1 - ks : ks;
       const int buf = ks % D;
       mbar_wait(&full_bar[buf], (ks / D) & 1);
-      const double* sl = ring + (long long)buf * slot_dbl + lane;
       const double* hb = hin + buf * WK * nv;
 #pragma unroll
       for (int mstep = 0; mstep < WK; ++mstep) {
         const int kk = BWD ? WK - 1 - mstep : mstep;
         const int t = k * WK + kk;
-        auto P = [&](int p) { return sl[(p * WK + kk) * 32]; };
+        const double *pc, *px, *pf;
+        slot_ptrs(buf, kk, pc, px, pf);
         double ij[5];
 #pragma unroll
         for (int c = 0; c < 5; ++c)
@@ -424,28 +443,29 @@ __global__ void __launch_bounds__(128, 1) k_wave2d(WaveArgs a) {
 #pragma unroll
           for (int c = 0; c < 5; ++c) ij[c] = hb[kk * nv + c];
         }
-        const double invd = P(rm.invd());
+        const double invd = pc[rm.invd() * 32];
         double dq[5];
 #pragma unroll
         for (int c = 0; c < 5; ++c) {
-          if (BWD) dq[c] = P(c) - (oi[c] + ij[c]) * invd;
-          else dq[c] = ((P(c) + oi[c]) + ij[c]) * invd;
+          if (BWD) dq[c] = px[c * 32] - (oi[c] + ij[c]) * invd;
+          else dq[c] = ((px[c * 32] + oi[c]) + ij[c]) * invd;
+          if (!real(t)) dq[c] = 0.0;  // padding cells carry exactly nothing
         }
         if (t < T) {
-          const long long o = ((long long)s * T + t) * 32 + lane;
 #pragma unroll
-          for (int c = 0; c < 5; ++c) a.out[(long long)c * Np + o] = dq[c];
+          for (int c = 0; c < 5; ++c) a.out[gaddr(a.sk, nv, s, t, c, lane)] = dq[c];
         }
         // outgoing half-block products through the two faces (rank-2 form)
-        const double w0 = P(rm.w()), w1 = P(rm.w() + 1), w2 = P(rm.w() + 2), w3 = P(rm.w() + 3),
-                     w4 = P(rm.w() + 4);
-        const double sb = P(rm.b()) * dq[0] + P(rm.b() + 1) * dq[1] + P(rm.b() + 2) * dq[2] +
-                          P(rm.b() + 3) * dq[3] + P(rm.b() + 4) * dq[4];
-        const double u = P(rm.uv()), v = P(rm.uv() + 1), hr = P(rm.hr());
+        const int pw = rm.w(), pb = rm.b();
+        const double w0 = pc[pw * 32], w1 = pc[(pw + 1) * 32], w2 = pc[(pw + 2) * 32],
+                     w3 = pc[(pw + 3) * 32], w4 = pc[(pw + 4) * 32];
+        const double sb = pc[pb * 32] * dq[0] + pc[(pb + 1) * 32] * dq[1] +
+                          pc[(pb + 2) * 32] * dq[2] + pc[(pb + 3) * 32] * dq[3] +
+                          pc[(pb + 4) * 32] * dq[4];
+        const double u = pc[rm.uv() * 32], v = pc[(rm.uv() + 1) * 32], hr = pc[rm.hr() * 32];
 #pragma unroll
         for (int f = 0; f < 2; ++f) {
-          const int pf = f == 0 ? pF1 : pF2;
-          const double Sx = P(pf), Sy = P(pf + 1), lam = P(pf + 2);
+          const double Sx = pf[(4 * f) * 32], Sy = pf[(4 * f + 1) * 32], lam = pf[(4 * f + 2) * 32];
           const double U = u * Sx + v * Sy;
           const double sa = (-U * hr) * dq[0] + (Sx * hr) * dq[1] + (Sy * hr) * dq[2];
           const double sig = 0.5 * (U + sgn * lam);
@@ -479,31 +499,32 @@ __global__ void __launch_bounds__(128, 1) k_wave2d(WaveArgs a) {
       const int k = BWD ? nslots - 1 - ks : ks;
       const int buf = ks % D;
       mbar_wait(&full_bar[buf], (ks / D) & 1);
-      const double* sl = ring + (long long)buf * slot_dbl + lane;
       const double* hb = hin + buf * WK * nv;
 #pragma unroll
       for (int mstep = 0; mstep < WK; ++mstep) {
         const int kk = BWD ? WK - 1 - mstep : mstep;
         const int t = k * WK + kk;
-        auto P = [&](int p) { return sl[(p * WK + kk) * 32]; };
-        const double u = P(rm.uv()), v = P(rm.uv() + 1);
-        const double U1 = u * P(pF1) + v * P(pF1 + 1);
-        const double U2 = u * P(pF2) + v * P(pF2 + 1);
-        const double c1 = a.sp_scale * (U1 + sgn * P(pF1 + 3));
-        const double c2 = a.sp_scale * (U2 + sgn * P(pF2 + 3));
-        const long long o = ((long long)s * T + t) * 32 + lane;
+        const double *pc, *px, *pf;
+        slot_ptrs(buf, kk, pc, px, pf);
+        const double u = pc[rm.uv() * 32], v = pc[(rm.uv() + 1) * 32];
+        const double U1 = u * pf[0] + v * pf[32];
+        const double U2 = u * pf[4 * 32] + v * pf[5 * 32];
+        const double c1 = a.sp_scale * (U1 + sgn * pf[3 * 32]);
+        const double c2 = a.sp_scale * (U2 + sgn * pf[7 * 32]);
         const int col = t - lane;
-        const double inv0 = P(rm.invs());
+        const bool rl = real(t);
+        const double inv0 = pc[rm.invs() * 32];
 #pragma unroll
         for (int c = 0; c < NSB; ++c) {
           if (c < ns) {
             double ijc = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
             if (first) ijc = hb[kk * nv + 5 + c];
-            const double inv = per ? P(rm.invs() + c) : inv0;
+            const double inv = per ? pc[(rm.invs() + c) * 32] : inv0;
             double dq;
-            if (BWD) dq = P(5 + c) - (oi[c] + ijc) * inv;
-            else dq = ((P(5 + c) + oi[c]) + ijc) * inv;
-            if (t < T) a.out[(long long)(5 + c) * Np + o] = dq;
+            if (BWD) dq = px[(5 + c) * 32] - (oi[c] + ijc) * inv;
+            else dq = ((px[(5 + c) * 32] + oi[c]) + ijc) * inv;
+            if (!rl) dq = 0.0;
+            if (t < T) a.out[gaddr(a.sk, nv, s, t, 5 + c, lane)] = dq;
             oi[c] = c1 * dq;
             oj[c] = c2 * dq;
             if (last && col >= 0 && col < a.ni) hout[(col % HRING) * nv + 5 + c] = oj[c];
@@ -541,9 +562,9 @@ __global__ void __launch_bounds__(256) k_epilogue2d(const Model* __restrict__ mp
   for (int e = threadIdx.x; e < nt * 32; e += blockDim.x) {
     const int tt = e / 32, r = e % 32;
     const int ii = tt - r;
-    if (ii < 0 || ii >= C) continue;
-    const long long src = ((long long)s * sk.T + i0 + ii + r) * 32 + r;
-    for (int c = 0; c < nv; ++c) es[c * CT + ii * 32 + r] = dqw[(long long)c * sk.Np + src];
+    if (ii < 0 || ii >= C || i0 + ii >= g.ni || j0 + r >= g.nj) continue;
+    const int t = i0 + ii + r;
+    for (int c = 0; c < nv; ++c) es[c * CT + ii * 32 + r] = dqw[gaddr(sk, nv, s, t, c, r)];
   }
   __syncthreads();
   // phase B: closure + gate in standard order (coalesced over j)
@@ -559,7 +580,6 @@ __global__ void __launch_bounds__(256) k_epilogue2d(const Model* __restrict__ mp
       if (k < nv) d[k] = es[k * CT + e];
     if (dq_std)
       for (int k = 0; k < nv; ++k) dq_std[(long long)k * N + c] = d[k];
-    // closure (driver.py:216-229) with dq from registers
     const double* qc = q + c;
     double* qo = qn + c;
 #pragma unroll
@@ -630,38 +650,46 @@ __global__ void __launch_bounds__(256) k_epilogue2d(const Model* __restrict__ mp
 }
 
 // ============================================================== launcher
-inline int wave_ring_depth(int NP, int nv) {
-  const size_t slot = (size_t)NP * WK * 32 * sizeof(double);
-  const size_t fixed = (size_t)HRING * nv * sizeof(double);
-  for (int D = 4; D >= 2; --D)
-    if (slot * D + (size_t)D * WK * nv * 8 + fixed <= 215 * 1024) return D;
+inline size_t wave_smem(int D, int NC, int NX, int NB, int nv) {
+  return ((size_t)D * WK * 32 * (NC + NX + NB) + (size_t)D * WK * nv + (size_t)HRING * nv) *
+         sizeof(double);
+}
+
+inline int wave_ring_depth(int NC, int nv) {
+  const int NX = nv + 8;  // forward is the larger of the two layouts
+  for (int D = 6; D >= 2; --D)
+    if (wave_smem(D, NC, NX, 0, nv) <= 215 * 1024 && wave_smem(D, NC, nv, 8, nv) <= 215 * 1024)
+      return D;
   return 0;
 }
 
 cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, const WaveBufs& wb,
                                      const double* q, const double* R, double cfl,
                                      const double* lamS, const double* domd, int dom_stride,
-                                     int per_species,
-                                     int scheme, double sp_scale, double* qn, double* dq_std,
-                                     unsigned long long* flags, cudaStream_t st) {
+                                     int per_species, int scheme, double sp_scale, double* qn,
+                                     double* dq_std, unsigned long long* flags, cudaStream_t st,
+                                     cudaEvent_t* ev) {
   CSB_NS_DISPATCH(ns, {
     const int nv = 5 + ns, nsI = per_species ? ns : 1;
     const Skew& sk = wb.sk;
-    const int nrec = nv + 1 + nsI + 29;
+    const int NC = 14 + nsI, NF = nv + 8;
+    const int D = wave_ring_depth(NC, nv);
+    if (D == 0) return cudaErrorInvalidConfiguration;
     // records
     int C = 8;
-    while (C > 1 && ((size_t)nrec * C * 32 + 7 * (C + 2) * 34) * sizeof(double) > 200 * 1024) C /= 2;
-    const size_t rsm = ((size_t)nrec * C * 32 + 7 * (size_t)(C + 2) * 34) * sizeof(double);
+    auto rsm_of = [&](int c) {
+      return ((size_t)(NC + NF + 8) * c * 32 + 7 * (size_t)(c + 2) * 34) * sizeof(double);
+    };
+    while (C > 1 && rsm_of(C) > 200 * 1024) C /= 2;
+    const size_t rsm = rsm_of(C);
     cudaFuncSetAttribute(k_records2d<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
     const int ncb = (g.ni + C - 1) / C;
+    if (ev) cudaEventRecord(ev[0], st);
     k_records2d<NSB><<<sk.nstrip * ncb, 256, rsm, st>>>(mp, g, sk, q, R, cfl, lamS, domd,
-                                                        dom_stride, per_species, wb.rec, C, flags);
+                                                        dom_stride, per_species, wb.recC, wb.recF,
+                                                        wb.recB, C, flags);
+    if (ev) cudaEventRecord(ev[1], st);
     // sweeps
-    const int NP = nv + nsI + 22;
-    const int D = wave_ring_depth(NP, nv);
-    if (D == 0) return cudaErrorInvalidConfiguration;
-    const size_t wsm = ((size_t)D * NP * WK * 32 + (size_t)D * WK * nv + (size_t)HRING * nv) *
-                       sizeof(double);
     WaveArgs wa;
     wa.sk = sk;
     wa.ni = g.ni;
@@ -671,27 +699,33 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     wa.nsI = nsI;
     wa.nslots = sk.T / WK;
     wa.D = D;
-    wa.rec = wb.rec;
+    wa.recC = wb.recC;
     wa.hand = wb.hand;
     wa.prog = wb.prog;
     wa.ticket = wb.prog + sk.nstrip;
     wa.sp_scale = sp_scale;
-    cudaFuncSetAttribute(k_wave2d<NSB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
-    cudaFuncSetAttribute(k_wave2d<NSB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+    const size_t fsm = wave_smem(D, NC, NF, 0, nv), bsm = wave_smem(D, NC, nv, 8, nv);
+    cudaFuncSetAttribute(k_wave2d<NSB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+    cudaFuncSetAttribute(k_wave2d<NSB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
     cudaMemsetAsync(wb.prog, 0, sizeof(int) * (sk.nstrip + 1), st);
-    wa.dqs = nullptr;
+    wa.recX = wb.recF;
+    wa.recB = nullptr;
     wa.out = wb.dqs;
-    k_wave2d<NSB, false><<<sk.nstrip, 128, wsm, st>>>(wa);
+    k_wave2d<NSB, false><<<sk.nstrip, 128, fsm, st>>>(wa);
+    if (ev) cudaEventRecord(ev[2], st);
     cudaMemsetAsync(wb.prog, 0, sizeof(int) * (sk.nstrip + 1), st);
-    wa.dqs = wb.dqs;
+    wa.recX = wb.dqs;
+    wa.recB = wb.recB;
     wa.out = wb.dqw;
-    k_wave2d<NSB, true><<<sk.nstrip, 128, wsm, st>>>(wa);
+    k_wave2d<NSB, true><<<sk.nstrip, 128, bsm, st>>>(wa);
+    if (ev) cudaEventRecord(ev[3], st);
     // epilogue
-    int CE = 8;
+    const int CE = 8;
     const size_t esm = (size_t)nv * CE * 32 * sizeof(double);
     cudaFuncSetAttribute(k_epilogue2d<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
     k_epilogue2d<NSB><<<sk.nstrip * ((g.ni + CE - 1) / CE), 256, esm, st>>>(
         mp, g, sk, scheme, q, wb.dqw, qn, dq_std, CE, flags);
+    if (ev) cudaEventRecord(ev[4], st);
   });
   return cudaGetLastError();
 }
