@@ -174,19 +174,38 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
     sk.ni = c->g.ni;
     sk.nj = c->g.nj;
     sk.nstrip = (c->g.nj + 31) / 32;
-    sk.T = ((c->g.ni + 31 + 3) / 4) * 4;
+    sk.T = ((c->g.ni + 31 + TQ - 1) / TQ) * TQ;
     sk.Np = (long long)sk.nstrip * sk.T * 32;  // cells per plane (step-major groups)
     c->wb.sk = sk;
-    c->wb.recC = k.take<double>((size_t)(14 + ns) * sk.Np);
-    c->wb.recF = k.take<double>((size_t)(nv + 8) * sk.Np);
-    c->wb.recB = k.take<double>((size_t)8 * sk.Np);
-    c->wb.dqs = k.take<double>((size_t)nv * sk.Np);
-    c->wb.dqw = k.take<double>((size_t)nv * sk.Np);
-    c->wb.hand = k.take<double>((size_t)sk.nstrip * sk.ni * nv);
-    c->wb.prog = k.take<int>((size_t)sk.nstrip + 1);
+    const int nsb = bucket_of(ns);
+    c->wb.ff = k.take<double>((size_t)30 * sk.Np);
+    c->wb.fb = k.take<double>((size_t)30 * sk.Np);
+    c->wb.fw = k.take<double>((size_t)5 * sk.Np);
+    c->wb.sf = k.take<double>((size_t)(2 * nsb + 2) * sk.Np);
+    c->wb.sb = k.take<double>((size_t)(2 * nsb + 2) * sk.Np);
+    c->wb.sw = k.take<double>((size_t)nsb * sk.Np);
+    c->wb.hand = k.take<double>((size_t)2 * sk.nstrip * sk.ni * (5 + nsb));
+    c->wb.prog = k.take<int>(2);
+    c->wb.nsI = 0;
     c->wave_ok = true;
   }
   return k.off;
+}
+
+// Wavefront padding slots (t - r outside [0, ni), rows beyond nj, padding
+// species) are never written by the records kernel: they must hold zeros so
+// that padding cells contribute exactly nothing to the sweeps (csb_wave.cuh).
+int zero_wave_records(csb_ctx* c, cudaStream_t st) {
+  const int nsb = bucket_of(c->ns);
+  const WaveBufs& w = c->wb;
+  const std::pair<double*, int> groups[] = {{w.ff, 30},          {w.fb, 30},
+                                            {w.fw, 5},           {w.sf, 2 * nsb + 2},
+                                            {w.sb, 2 * nsb + 2}, {w.sw, nsb}};
+  for (const auto& gp : groups)
+    if (cudaMemsetAsync(gp.first, 0, (size_t)gp.second * w.sk.Np * sizeof(double), st) !=
+        cudaSuccess)
+      return 1;
+  return 0;
 }
 
 int reset_flags(csb_ctx* c, cudaStream_t st) {
@@ -382,10 +401,7 @@ int csb_set_workspace(csb_ctx* c, void* dev, size_t bytes) {
     // wavefront padding slots (t - r outside [0, ni), rows beyond nj) are never
     // written by the records kernel: they must hold zeros so that padding
     // cells contribute exactly nothing to the sweep (csb_wave.cuh)
-    const int nv = 5 + c->ns;
-    const size_t planes = (size_t)(14 + c->ns) + (nv + 8) + 8 + 2 * (size_t)nv;
-    if (cudaMemset(c->wb.recC, 0, planes * c->wb.sk.Np * sizeof(double)) != cudaSuccess)
-      return fail(c, CSB_E_CUDA, "zero wavefront records");
+    if (zero_wave_records(c, 0)) return fail(c, CSB_E_CUDA, "zero wavefront records");
   }
   return reset_flags(c, 0) ? CSB_E_CUDA : (cudaDeviceSynchronize() == cudaSuccess ? CSB_OK : CSB_E_CUDA);
 }
@@ -626,6 +642,12 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
       lamS = op.lamS;
       domd = op.dom;
       dstride = op.dom_full ? c->ns + 1 : 1;
+    }
+    const int nsI = chem ? c->ns : 1;
+    if (e == cudaSuccess && c->wb.nsI != nsI) {
+      // species record layout changes with nsI: re-zero the padding slots
+      e = zero_wave_records(c, st) ? cudaErrorUnknown : cudaSuccess;
+      c->wb.nsI = nsI;
     }
     if (e == cudaSuccess)
       e = launch_wave_step(c->d_model, c->ns, c->g, c->wb, q, R, cfl, lamS, domd, dstride,

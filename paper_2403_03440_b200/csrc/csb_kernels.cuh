@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <utility>
 
 #include "csb_common.cuh"
 
@@ -36,20 +37,26 @@ struct OpDev {
 
 // Strip-skewed 2-D layout of the wavefront path (csb_wave.cuh): cell (i, j)
 // at ((j>>5)*T + i + (j&31))*32 + (j&31).
+constexpr int TQ = 16;  // T is a multiple of TQ; wavefront slot lengths divide TQ
+
 struct Skew {
   int ni, nj, nstrip, T;
   long long Np;  // plane stride (padded)
 };
 
+// Sweep records of the wavefront path, one set per subsystem, all step-major
+// (plane layouts in csb_wave.cuh).  NSB = species bucket of the model.
 struct WaveBufs {
   Skew sk;
-  double* recC;  // sweep records, group C (both sweeps), step-major
-  double* recF;  // group F (forward: rhs + upper faces)
-  double* recB;  // group B (backward: lower faces)
-  double* dqs;   // forward output dq* [step-major, nv planes]
-  double* dqw;   // backward output dq
-  double* hand;  // strip hand-off [nstrip][ni][nv]
-  int* prog;     // [nstrip + 1] progress flags + ticket
+  double* ff;     // flow forward group (30 planes)
+  double* fb;     // flow backward group (30 planes, incl. dq*)
+  double* fw;     // flow dq (5 planes)
+  double* sf;     // species forward group (nsI + NSB + 2 planes)
+  double* sb;     // species backward group (nsI + 2 + NSB planes, incl. dq*)
+  double* sw;     // species dq (NSB planes)
+  double* hand;   // strip hand-off rows [2 sweeps][flow nstrip*ni*5 | species nstrip*ni*NSB]
+  int* prog;      // [2]: flow and species CTA tickets
+  int nsI;        // species-diagonal planes of the current layout (0 = unset)
 };
 
 cudaError_t launch_wave_step(const Model* mp, int ns, const GridDev& g, const WaveBufs& wb,

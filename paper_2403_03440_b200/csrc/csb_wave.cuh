@@ -12,48 +12,56 @@
 // (s = j >> 5, r = j & 31).  At wavefront step t of strip s, row r processes
 // column i = t - r.  A record group with NG planes stores plane p of cell
 // (i, j) at ((s*T + t)*NG + p)*32 + r with t = i + r (T = ni + 31 rounded up
-// to a multiple of WK).  WK consecutive steps of one strip are therefore one
-// contiguous block of WK*NG*32 doubles: the sweep streams each group with a
-// single TMA bulk copy per WK steps into an mbarrier ring.  The backward sweep
-// visits the same physical steps in reverse (backward slot t holds the same
-// cells), so it streams the same blocks in reverse order.
+// to a multiple of 16).  A run of WK consecutive steps of one strip is one
+// contiguous block, so each sweep streams ONE TMA bulk copy per ring slot
+// (measured on B200: a CTA's bulk copies complete at ~one request per ~830
+// cycles whatever their size up to 64 KiB, scripts/tma_probe.cu).  Slots
+// outside the grid (t - r outside [0, ni), rows beyond nj) are padding: their
+// records are zero (set once at workspace setup, never written), so padding
+// cells carry exactly zero through the chains.
 //
-// Record groups: C (both sweeps) = invd, invs[nsI], w[5], b[5], u, v, hr;
-// F (forward) = rhs[nv], upper-i face (Sx, Sy, lam, lamsp), upper-j face;
-// B (backward) = lower-i face, lower-j face; Q = dq* (forward output,
-// backward input); W = dq (backward output).
-//
-// One CTA per strip (dynamic ticket => deadlock-free ordering):
-//   warp 0: flow chain (5 components, rank-2 half-block products),
-//   warp 1: species chain (ns scalar chains),
-//   warp 2: producer (TMA bulk copies + the upstream strip's hand-off values,
-//           polled from L2),
-//   warp 3: publisher (this strip's hand-off row to L2 + progress flag).
-// Row r hands its j-direction contribution to row r+1 (r-1 backward) with a
-// warp shuffle; strip boundaries go through L2.
+// The split (CS) operator decouples the flow and species subsystems inside
+// the sweeps (implicit.py:329-403), so every strip runs two independent CTAs:
+//   flow    : FF (forward, 30 planes)  invd, w[5], b[5], rhs[5], and per upper
+//             face (i, j) a[3] = (-U hr, Sx hr, Sy hr), e[3] = (Sx, Sy, U)/2,
+//             sig = (U + lam)/2;
+//             FB (backward, 30 planes) invd, w, b, per lower face a, e,
+//             sig = (U - lam)/2, dq*[5] (written by the forward chain);
+//             FW (5 planes) dq;
+//   species : SF (nsI + NSB + 2) invs[nsI], rhs[NSB], c_i, c_j with
+//             c = sp_scale (U + lam_sp) at the upper faces;
+//             SB (nsI + 2 + NSB) invs, c_i, c_j at the lower faces
+//             (sp_scale (U - lam_sp)), dq*[NSB]; SW (NSB planes) dq.
+// The half-block products through a face are then (rank-2 form of
+// implicit.py:350-380)  sa = a . dq[0:3],  sb = b . dq,
+//   o = w sa + e sb + sig dq  (e acting on components 1, 2, 4).
+// Each CTA: warp 0 chain (one lane per row; the j-direction contribution goes
+// to the next row by warp shuffle), warp 1 producer (TMA ring + the upstream
+// strip's hand-off row polled from L2), warp 2 publisher.
 #pragma once
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "csb_common.cuh"
 #include "csb_kernels.cuh"
 
 namespace csb {
 
-constexpr int WK = 4;          // wavefront steps per ring slot
-constexpr int HRING = 64;      // hand-off ring (columns)
+constexpr int HRING = 64;  // hand-off ring (columns)
+// signalling NaN marking a hand-off word not yet written (see the chains)
+constexpr unsigned long long HAND_SENTINEL = 0x7FF4DEADBEEF0001ull;
+constexpr int NFF = 30, NFB = 30, FB_DQ = 25;
+constexpr int WKF = 8;     // flow slot: 8 steps x 30 planes = 60 KiB
 
-struct RecMap {
-  int nv, nsI;
-  // group C
-  CSB_DEV int invd() const { return 0; }
-  CSB_DEV int invs() const { return 1; }
-  CSB_DEV int w() const { return 1 + nsI; }
-  CSB_DEV int b() const { return w() + 5; }
-  CSB_DEV int uv() const { return w() + 10; }
-  CSB_DEV int hr() const { return w() + 12; }
-  CSB_DEV int nc() const { return w() + 13; }
-  // group F: rhs[nv], fi[4], fj[4]; group B: fi[4], fj[4]
-  CSB_DEV int nf() const { return nv + 8; }
-};
+// species slot length: <= 64 KiB per slot at the widest layout (nsI = NSB)
+template <int NSB>
+constexpr int wave_wks() {
+  int w = 16;
+  while (w > 1 && w * (2 * NSB + 2) * 256 > 64 * 1024) w /= 2;
+  return w;
+}
 
 // ---------------------------------------------------------------- PTX helpers
 CSB_DEV unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -62,11 +70,6 @@ CSB_DEV void mbar_init(unsigned long long* b, unsigned count) {
 }
 CSB_DEV void mbar_arrive(unsigned long long* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-CSB_DEV void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
 }
 CSB_DEV void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)),
@@ -109,40 +112,71 @@ CSB_DEV long long gaddr(const Skew& k, int NG, int s, int t, int p, int r) {
 }
 
 // ============================================================== records
-// Tile = one strip (32 rows) x C columns.  Phase A: per cell (tile + 1-cell
-// halo) decode + transport (face quantities); interior cells also get dtau,
-// the diagonals and the Jacobian ingredients.  Phase B: face radii (max of
-// the two adjacent cells at the face metric).  Phase C: skewed stores.
+// Tile = one strip (32 rows) x C wavefront steps, i.e. a parallelogram in
+// (i, j): element (tt, r) is cell (i = t0 + tt - r, j = j0 + r).  In these
+// skew coordinates the face neighbours of (tt, r) are (tt +- 1, r) in i and
+// (tt +- 1, r +- 1) in j, so a 1-element halo in tt and r covers them.  A warp
+// handles one step (32 rows), so every record store is one contiguous 256-byte
+// row of the step-major layout; the strided q/R loads hit L1 (the four cells
+// of a 32-byte sector are (tt..tt+3, r..r+3), all in the same tile).
+// Phase A: per cell of tile + halo decode + transport (face quantities);
+// interior cells also get dtau, the diagonals, the Jacobian ingredients and
+// -R.  Phase B: per interior cell, face radii (max of the two adjacent cells
+// at the face metric), face coefficients, and all record stores.
 template <int NSB>
 __global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp, GridDev g, Skew sk,
                                                    const double* __restrict__ q,
                                                    const double* __restrict__ R, double cfl,
                                                    const double* __restrict__ lamS,
                                                    const double* __restrict__ domd, int dom_stride,
-                                                   int per_species, double* __restrict__ recC,
-                                                   double* __restrict__ recF,
-                                                   double* __restrict__ recB, int C,
-                                                   unsigned long long* flags) {
+                                                   int per_species, double sp_scale, WaveBufs wb,
+                                                   int C, unsigned long long* flags) {
   extern __shared__ double sm[];
   const Model& m = *mp;
-  const int ns = m.ns, nv = 5 + ns, nsI = per_species ? ns : 1;
-  RecMap rm{nv, nsI};
-  const int NC = rm.nc(), NF = rm.nf();
-  const int ncb = (g.ni + C - 1) / C;
+  const int ns = m.ns, nsI = per_species ? NSB : 1;  // species-diagonal planes
+  const int NSF = nsI + NSB + 2;  // = SB group planes
+  const int ncb = sk.T / C;
   const int s = blockIdx.x / ncb, ib = blockIdx.x % ncb;
-  const int i0 = ib * C, j0 = s * 32;
+  const int t0 = ib * C, j0 = s * 32;
   const int HX = C + 2, HY = 34, NH = HX * HY;
   const int CT = C * 32;
-  double* A = sm;            // [7][NH]: u, v, w, c, nf, nsp, V
-  double* BC = sm + 7 * NH;  // [NC][CT] | [NF][CT] | [8][CT]
-  double* BF = BC + (long long)NC * CT;
-  double* BB = BF + (long long)NF * CT;
+  const int NCP = 16 + nsI + NSB;              // cell planes: invd w b rhs | invs rhs_s
+  double* A = sm;                              // [12][NH]: u, v, w, c, nf, nsp, V, hr,
+                                               //   lower-i face Sx Sy, lower-j face Sx Sy
+  double* TC = sm + 12 * NH;                   // [NCP][CT]
   const long long N = g.N;
-  // ---------------- phase A: halo-extended per-cell quantities
-  for (int l = threadIdx.x; l < NH; l += blockDim.x) {
-    const int hx = l / HY, hy = l % HY;
-    const int i = i0 - 1 + hx, j = j0 - 1 + hy;
-    if (i < 0 || i >= g.ni || j < 0 || j >= g.nj) continue;
+  {
+    // reset both sweeps' hand-off buffers to the sentinel (csb_wave.cuh chains)
+    const long long nh = 2LL * sk.nstrip * g.ni * (5 + NSB);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nh;
+         e += (long long)gridDim.x * blockDim.x)
+      wb.hand[e] = __longlong_as_double((long long)HAND_SENTINEL);
+  }
+  // ---------------- phase A: halo-extended per-cell quantities.  Enumerated
+  // column by column (fixed i, consecutive j) so that the loads of a warp are
+  // contiguous runs of up to C + 2 cells: i' = tt - r in [-33, C + 1],
+  // r in [max(-1, -1 - i'), min(32, C - i')].
+  const int CW = C + 2;
+  for (int l = threadIdx.x; l < (C + 35) * CW; l += blockDim.x) {
+    const int ip = -33 + l / CW;
+    const int r = max(-1, -1 - ip) + l % CW;
+    if (r > min(32, C - ip)) continue;
+    const int tt = ip + r;
+    const int hl = (tt + 1) * HY + (r + 1);
+    const int i = t0 + ip, j = j0 + r;
+    if (i < 0 || j < 0 || i > g.ni || j > g.nj) continue;
+    // lower faces of (i, j) (these include the upper boundary faces i = ni, j = nj)
+    if (j < g.nj) {
+      const long long f = face_index(g, 0, i, j, 0);
+      A[8 * NH + hl] = __ldg(g.S[0] + f);
+      A[9 * NH + hl] = __ldg(g.S[0] + g.NF[0] + f);
+    }
+    if (i < g.ni) {
+      const long long f = face_index(g, 1, i, j, 0);
+      A[10 * NH + hl] = __ldg(g.S[1] + f);
+      A[11 * NH + hl] = __ldg(g.S[1] + g.NF[1] + f);
+    }
+    if (i >= g.ni || j >= g.nj) continue;
     const long long c = (long long)i * g.nj + j;
     Cell<NSB> cs;
     const bool ok = decode<NSB>(m, q + c, N, cs);
@@ -150,17 +184,18 @@ __global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp,
     transport<NSB>(m, cs.T, cs.Y, cs.rho, mu, kc, D);
     diffusivities(mu, kc, D, cs.rho, cs.cp - cs.R, nf, nsp, nu);
     const double V = __ldg(g.vol + c);
-    A[0 * NH + l] = cs.u[0];
-    A[1 * NH + l] = cs.u[1];
-    A[2 * NH + l] = cs.u[2];
-    A[3 * NH + l] = cs.c;
-    A[4 * NH + l] = nf;
-    A[5 * NH + l] = nsp;
-    A[6 * NH + l] = V;
-    const bool inner = hx >= 1 && hx <= C && hy >= 1 && hy <= 32;
+    A[0 * NH + hl] = cs.u[0];
+    A[1 * NH + hl] = cs.u[1];
+    A[2 * NH + hl] = cs.u[2];
+    A[3 * NH + hl] = cs.c;
+    A[4 * NH + hl] = nf;
+    A[5 * NH + hl] = nsp;
+    A[6 * NH + hl] = V;
+    A[7 * NH + hl] = 0.5 / cs.rho;
+    const bool inner = tt >= 0 && tt < C && r >= 0 && r < 32;
     if (!inner) continue;
     if (!ok) raise_flag(flags, EB_DECODE, c);
-    const int e = (hx - 1) * 32 + (hy - 1);  // tile-local cell (column-major by i)
+    const int e = tt * 32 + r;  // tile element (tt, r)
     // cell radii at the cell-averaged metric, dtau (implicit.py:152-163, 33-44)
     double li[3], lv[3], rf = 0.0, rsp = 0.0;
 #pragma unroll
@@ -191,58 +226,82 @@ __global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp,
     const double base = V / dtau;
     const double dflow = base + rf;
     bool bad = !(fabs(dflow) >= 1e-300) || !isfinite(dflow);
-    BC[rm.invd() * CT + e] = 1.0 / dflow;
     const double dsp0 = base + rsp;
+    double* ts = TC + 16 * CT;
     if (per_species) {
       for (int sp = 0; sp < ns; ++sp) {
         const double v = dsp0 - domd[(long long)sp * dom_stride * N + c] * V;
         bad |= !(fabs(v) >= 1e-300) || !isfinite(v);
-        BC[(rm.invs() + sp) * CT + e] = 1.0 / v;
+        ts[sp * CT + e] = 1.0 / v;
       }
+      for (int sp = ns; sp < NSB; ++sp) ts[sp * CT + e] = 0.0;  // padding species
     } else {
       bad |= !(fabs(dsp0) >= 1e-300) || !isfinite(dsp0);
-      BC[rm.invs() * CT + e] = 1.0 / dsp0;
+      ts[0 * CT + e] = 1.0 / dsp0;
     }
     if (bad) raise_flag(flags, EB_SINGULAR, c);
-    for (int k = 0; k < nv; ++k) BF[k * CT + e] = -R[(long long)k * N + c];
+#pragma unroll
+    for (int k = 0; k < NSB; ++k)
+      ts[(nsI + k) * CT + e] = k < ns ? -R[(long long)(5 + k) * N + c] : 0.0;
+    for (int k = 0; k < 5; ++k) TC[(11 + k) * CT + e] = -R[(long long)k * N + c];
     const double beta = cs.gamma - 1.0;
-    const int pw = rm.w(), pb = rm.b();
-    BC[(pw + 0) * CT + e] = cs.rho;
-    BC[(pw + 1) * CT + e] = cs.rho * cs.u[0];
-    BC[(pw + 2) * CT + e] = cs.rho * cs.u[1];
-    BC[(pw + 3) * CT + e] = cs.rho * cs.u[2];
-    BC[(pw + 4) * CT + e] = cs.rho * cs.h;
-    BC[(pb + 0) * CT + e] = beta * cs.Ek;
-    BC[(pb + 1) * CT + e] = -beta * cs.u[0];
-    BC[(pb + 2) * CT + e] = -beta * cs.u[1];
-    BC[(pb + 3) * CT + e] = -beta * cs.u[2];
-    BC[(pb + 4) * CT + e] = beta;
-    BC[(rm.uv() + 0) * CT + e] = cs.u[0];
-    BC[(rm.uv() + 1) * CT + e] = cs.u[1];
-    BC[rm.hr() * CT + e] = 0.5 / cs.rho;
+    TC[0 * CT + e] = 1.0 / dflow;
+    TC[1 * CT + e] = cs.rho;
+    TC[2 * CT + e] = cs.rho * cs.u[0];
+    TC[3 * CT + e] = cs.rho * cs.u[1];
+    TC[4 * CT + e] = cs.rho * cs.u[2];
+    TC[5 * CT + e] = cs.rho * cs.h;
+    TC[6 * CT + e] = beta * cs.Ek;
+    TC[7 * CT + e] = -beta * cs.u[0];
+    TC[8 * CT + e] = -beta * cs.u[1];
+    TC[9 * CT + e] = -beta * cs.u[2];
+    TC[10 * CT + e] = beta;
   }
   __syncthreads();
-  // ---------------- phase B: face radii of the 4 faces of every tile cell
+  // ---------------- phase B: faces + all record stores, one cell per thread
   for (int e = threadIdx.x; e < CT; e += blockDim.x) {
-    const int ii = e / 32, jj = e % 32;
-    const int i = i0 + ii, j = j0 + jj;
-    if (i >= g.ni || j >= g.nj) continue;
-    const int hc = (ii + 1) * HY + (jj + 1);
+    const int tt = e / 32, r = e % 32;
+    const int t = t0 + tt;
+    const int i = t - r, j = j0 + r;
+    // cells outside the grid are padding slots: zeroed once at workspace
+    // setup, never written
+    if (i < 0 || i >= g.ni || j >= g.nj) continue;
+    const int hc = (tt + 1) * HY + (r + 1);
+    const double u = A[0 * NH + hc], v = A[1 * NH + hc], hr = A[7 * NH + hc];
+    double* ff = wb.ff + gaddr(sk, NFF, s, t, 0, r);
+    double* fb = wb.fb + gaddr(sk, NFB, s, t, 0, r);
+    double* sf = wb.sf + gaddr(sk, NSF, s, t, 0, r);
+    double* sb = wb.sb + gaddr(sk, NSF, s, t, 0, r);
+    for (int p = 0; p < 11; ++p) {
+      const double x = TC[p * CT + e];
+      ff[p * 32] = x;
+      fb[p * 32] = x;
+    }
+    for (int p = 11; p < 16; ++p) ff[p * 32] = TC[p * CT + e];
+    for (int p = 0; p < nsI; ++p) {
+      const double x = TC[(16 + p) * CT + e];
+      sf[p * 32] = x;
+      sb[p * 32] = x;
+    }
+#pragma unroll
+    for (int p = 0; p < NSB; ++p) sf[(nsI + p) * 32] = TC[(16 + nsI + p) * CT + e];
     // faces: 0 upper-i (i+1), 1 upper-j (j+1), 2 lower-i (i), 3 lower-j (j)
 #pragma unroll
     for (int f = 0; f < 4; ++f) {
       const int d = f & 1;
       const bool upper = f < 2;
-      int fi = i, fj = j;
-      if (upper) {
-        if (d == 0) fi += 1;
-        else fj += 1;
-      }
+      // face metric from the halo: upper-i = lower-i face of (tt+1, r),
+      // upper-j = lower-j face of (tt+1, r+1); S_z = 0 on i/j faces of a
+      // 2-D grid (csb_implicit.cu k_check_2d)
+      const int hf = upper ? (d == 0 ? hc + HY : hc + HY + 1) : hc;
       double S[3];
-      load_S(g, d, face_index(g, d, fi, fj, 0), S);
+      S[0] = A[(8 + 2 * d) * NH + hf];
+      S[1] = A[(9 + 2 * d) * NH + hf];
+      S[2] = 0.0;
       const double a2 = (S[0] * S[0] + S[1] * S[1]) + S[2] * S[2];
       const double ar = sqrt(a2);
-      const int nb = upper ? (d == 0 ? hc + HY : hc + 1) : (d == 0 ? hc - HY : hc - 1);
+      // neighbour across the face, in skew coordinates
+      const int nb = upper ? (d == 0 ? hc + HY : hc + HY + 1) : (d == 0 ? hc - HY : hc - HY - 1);
       const bool nb_in = upper ? (d == 0 ? i + 1 < g.ni : j + 1 < g.nj) : (d == 0 ? i > 0 : j > 0);
       const int lo = upper ? hc : nb, hi = upper ? nb : hc;  // lower/upper cell of the face
       auto lam = [&](int h, bool sp) {
@@ -258,321 +317,413 @@ __global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp,
         lf = lam(hc, false);
         ls = lam(hc, true);
       }
-      double* dst = upper ? BF + (long long)(nv + 4 * d) * CT : BB + (long long)(4 * d) * CT;
-      dst[0 * CT + e] = S[0];
-      dst[1 * CT + e] = S[1];
-      dst[2 * CT + e] = lf;
-      dst[3 * CT + e] = ls;
+      const double sgn_lf = upper ? lf : -lf, sgn_ls = upper ? ls : -ls;
+      const double U = u * S[0] + v * S[1];
+      double* fd = upper ? ff + (16 + 7 * d) * 32 : fb + (11 + 7 * d) * 32;
+      fd[0 * 32] = -U * hr;
+      fd[1 * 32] = S[0] * hr;
+      fd[2 * 32] = S[1] * hr;
+      fd[3 * 32] = 0.5 * S[0];
+      fd[4 * 32] = 0.5 * S[1];
+      fd[5 * 32] = 0.5 * U;
+      fd[6 * 32] = 0.5 * (U + sgn_lf);
+      const double csp = sp_scale * (U + sgn_ls);
+      if (upper) sf[(nsI + NSB + d) * 32] = csp;
+      else sb[(nsI + d) * 32] = csp;
     }
-  }
-  __syncthreads();
-  // ---------------- phase C: skewed step-major stores
-  // tile steps tt in [0, C + 31): element (tt, r) <-> cell (i0 + tt - r, j0 + r)
-  const int nt = C + 31;
-  for (int e = threadIdx.x; e < nt * 32; e += blockDim.x) {
-    const int tt = e / 32, r = e % 32;
-    const int ii = tt - r;
-    if (ii < 0 || ii >= C) continue;
-    const int i = i0 + ii, j = j0 + r;
-    // cells outside the grid are padding slots: zeroed once at workspace
-    // setup and never written (i >= ni would also step past the strip)
-    if (i >= g.ni || j >= g.nj) continue;
-    const int t = i + r;
-    const int el = ii * 32 + r;
-    for (int p = 0; p < NC; ++p) recC[gaddr(sk, NC, s, t, p, r)] = BC[p * CT + el];
-    for (int p = 0; p < NF; ++p) recF[gaddr(sk, NF, s, t, p, r)] = BF[p * CT + el];
-    for (int p = 0; p < 8; ++p) recB[gaddr(sk, 8, s, t, p, r)] = BB[p * CT + el];
   }
 }
 
 // ============================================================== wavefront
-struct WaveArgs {
-  Skew sk;
-  int ni, nj, ns, nv, nsI, nslots, D;
-  const double* recC;
-  const double* recX;  // forward: F group; backward: Q (dq*)
-  const double* recB;  // backward faces
-  double* out;         // forward: dq* (Q); backward: dq (W), step-major [nv]
-  double* hand;        // [nstrip][ni][nv]
-  int* prog;           // [nstrip]
+struct WaveRole {
+  const double* in;  // streamed group
+  int ng;            // its planes per step
+  int D;             // ring depth
+  double* out;       // chain output group
+  int ngo, po;       // its planes per step, first output plane
+  double* hand;      // [nstrip][ni][nh] hand-off rows (sentinel-initialised)
   int* ticket;
-  double sp_scale;
 };
 
-template <int NSB, bool BWD>
-__global__ void __launch_bounds__(128, 1) k_wave2d(WaveArgs a) {
-  extern __shared__ __align__(128) double wsm[];
-  __shared__ unsigned long long full_bar[8], empty_bar[8];
-  __shared__ int s_strip, done_cnt[2];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nv = a.nv, ns = a.ns, D = a.D;
-  RecMap rm{nv, a.nsI};
-  const int NC = rm.nc();
-  const int NX = BWD ? nv : rm.nf();  // planes of the X group (rhs+faces | dq*)
-  const int NB = BWD ? 8 : 0;
-  const long long slotC = (long long)WK * NC * 32, slotX = (long long)WK * NX * 32,
-                  slotB = (long long)WK * NB * 32;
-  double* ringC = wsm;                // [D][WK][NC][32]
-  double* ringX = ringC + D * slotC;  // [D][WK][NX][32]
-  double* ringB = ringX + D * slotX;  // [D][WK][8][32] (backward)
-  double* hin = ringB + D * slotB;    // [D][WK][nv]
-  double* hout = hin + D * WK * nv;   // [HRING][nv]
-  if (threadIdx.x == 0) {
-    const int tk = atomicAdd(a.ticket, 1);
-    s_strip = BWD ? a.sk.nstrip - 1 - tk : tk;
-    for (int b = 0; b < D; ++b) {
-      mbar_init(&full_bar[b], 32);
-      mbar_init(&empty_bar[b], 2);
-    }
-    done_cnt[0] = done_cnt[1] = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const int s = s_strip;
-  const int j0 = s * 32;
-  const int rt = min(31, a.nj - 1 - j0);  // highest valid row of this strip
-  const int nslots = a.nslots;
-  const int T = a.sk.T;
-  const int up = BWD ? s + 1 : s - 1;
-  const bool has_up = BWD ? (s + 1 < a.sk.nstrip) : (s > 0);
-  const bool has_down = BWD ? (s > 0) : (s + 1 < a.sk.nstrip);
+struct WaveArgs {
+  Skew sk;
+  int ni, nj, nsI;
+  int only;          // -1: both roles (production); 0/1: one role (timing probe)
+  unsigned long long* dbg;  // timing probe: [CTA][4] globaltimer stamps (or null)
+  WaveRole role[2];  // 0 flow, 1 species
+};
 
-  if (warp == 2) {
-    // ---------------------------------------------------- producer
-    for (int ks = 0; ks < nslots; ++ks) {
-      const int k = BWD ? nslots - 1 - ks : ks;
-      const int buf = ks % D;
-      if (ks >= D) mbar_wait(&empty_bar[buf], ((ks / D) - 1) & 1);
-      if (lane == 0) {
-        // bulk copies first: they do not depend on the upstream strip
-        const unsigned bC = (unsigned)(slotC * 8), bX = (unsigned)(slotX * 8),
-                       bB = (unsigned)(slotB * 8);
-        mbar_expect_tx(&full_bar[buf], bC + bX + bB);
-        const long long st = (long long)s * T + (long long)k * WK;
-        bulk_g2s(ringC + buf * slotC, a.recC + st * NC * 32, bC, &full_bar[buf]);
-        bulk_g2s(ringX + buf * slotX, a.recX + st * NX * 32, bX, &full_bar[buf]);
-        if (BWD) bulk_g2s(ringB + buf * slotB, a.recB + st * 8 * 32, bB, &full_bar[buf]);
-      }
-      // upstream hand-off for this slot's WK steps (first row's columns)
-      double* hb = hin + buf * WK * nv;
-      if (has_up) {
-        int need;
-        if (!BWD) need = min(k * WK + WK - 1, a.ni - 1) + 1;  // first row 0: col = t
-        else need = a.ni - max(k * WK - rt, 0);               // first row rt: col = t - rt
-        need = max(0, min(need, a.ni));
-        while (ld_relaxed(a.prog + up) < need) __nanosleep(20);
-        (void)ld_acquire(a.prog + up);
-        for (int e = lane; e < WK * nv; e += 32) {
-          const int kk = e / nv, c = e % nv;
-          const int t = k * WK + kk;
-          const int col = BWD ? t - rt : t;
-          double v = 0.0;
-          if (col >= 0 && col < a.ni) v = __ldcg(a.hand + ((long long)up * a.ni + col) * nv + c);
-          hb[kk * nv + c] = v;
-        }
-      } else {
-        for (int e = lane; e < WK * nv; e += 32) hb[e] = 0.0;
-      }
-      __syncwarp();
-      mbar_arrive(&full_bar[buf]);  // all 32 lanes, after their hand-off writes
-    }
-    return;
-  }
+// ------------------------------------------------------------------ chains
+// Hand-off between strips, in "sequence" space q (the order in which a strip
+// produces / consumes its boundary columns): forward q = col, backward
+// q = ni - 1 - col.  The last row of a strip stores its outgoing j-face
+// products for column q straight into the L2 hand-off buffer
+// hand[strip][q][nh] (one relaxed 8-byte store per value); the buffer is
+// reset to a signalling-NaN sentinel before the sweep, and since every
+// hand-off value is the result of a floating-point operation (which never
+// yields a signalling NaN), a word != sentinel is final.  The receiver warp
+// of the next strip polls those words, copies complete columns into the
+// smem ring hin[HRING][nh] and bumps recv_cnt; the chain checks recv_cnt
+// once per group of G steps.
+constexpr int GSTEP = 4;  // steps per hand-off check
 
-  if (warp == 3) {
-    // ---------------------------------------------------- publisher
-    if (!has_down) return;
-    int next = 0;
-    while (next < a.ni) {
-      const int d0 = ld_volatile_s(&done_cnt[0]), d1 = ld_volatile_s(&done_cnt[1]);
-      __threadfence_block();
-      const int dn = min(d0, d1);
-      int cnt;
-      if (!BWD) cnt = dn * WK - rt;          // cols < cnt done (top row rt: t = col + rt)
-      else cnt = a.ni - (nslots - dn) * WK;  // bottom row 0: cols >= (nslots-dn)*WK done
-      cnt = max(0, min(cnt, a.ni));
-      if (cnt > next) {
-        for (int e = lane; e < (cnt - next) * nv; e += 32) {
-          const int co = next + e / nv, c = e % nv;
-          const int col = BWD ? a.ni - 1 - co : co;
-          a.hand[((long long)s * a.ni + col) * nv + c] = hout[(col % HRING) * nv + c];
-        }
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release(a.prog + s, cnt);
-        next = cnt;
-      } else {
-        __nanosleep(20);
-      }
-    }
-    return;
-  }
+struct ChainCtx {
+  const WaveArgs* a;
+  int s, nslots, D, rt;
+  bool has_up, has_down, first, last;
+  const double* ring;
+  const double* hin;
+  double* hand_out;     // this strip's row of the hand-off buffer
+  unsigned long long* full_bar;
+  unsigned long long* empty_bar;
+  int* consumed;        // q consumed by the chain (chain -> receiver)
+  const int* recv_cnt;  // q received from upstream (receiver -> chain)
+  unsigned long long* t_first;  // timing probe
+};
 
-  // -------------------------------------------------------- chains
+// predicated store without a branch (a branch would end the scheduling region
+// of the unrolled step loop)
+CSB_DEV void st_pred_cg_f64(double* p, double v, bool pred) {
+  asm("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.cg.f64 [%0], %1;\n}" ::"l"(p), "d"(v),
+      "r"((int)pred));
+}
+CSB_DEV unsigned long long ld_relaxed_u64(const double* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// group check: all upstream columns needed by steps [t_a, t_b] are in hin
+template <bool BWD>
+CSB_DEV void chain_group_wait(const ChainCtx& x, int t_first, int t_last, int& avail) {
+  if (!x.has_up) return;
+  // q grows with t forward and shrinks with t backward; need the larger end
+  const int qa = BWD ? x.a->ni - 1 - t_first + x.rt : t_first;
+  const int qb = BWD ? x.a->ni - 1 - t_last + x.rt : t_last;
+  const int qmax = min(max(qa, qb), x.a->ni - 1);
+  if (qmax < 0) return;
+  if (x.first) *(volatile int*)x.consumed = min(qa, qb);  // q below are consumed
+  if (avail <= qmax) {
+    do {
+      avail = ld_volatile_s(x.recv_cnt);
+    } while (avail <= qmax);
+    __threadfence_block();
+  }
+  if (x.a->dbg && *x.t_first == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *x.t_first = t;
+  }
+}
+
+// flow chain: 5 coupled components per row (rank-2 half blocks)
+template <bool BWD>
+CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
+  constexpr int WK = WKF, NG = 30;
+  constexpr int FQ = BWD ? 11 : 16;                         // first face plane
+  constexpr int NGO = BWD ? 5 : NFB, PO = BWD ? 0 : FB_DQ;  // output: FW | FB dq* planes
   const unsigned FULL = 0xffffffffu;
-  const double sgn = BWD ? -1.0 : 1.0;
-  const bool first = BWD ? (lane == rt) : (lane == 0);  // receives the upstream hand-off
-  const bool last = BWD ? (lane == 0) : (lane == rt);   // sends the downstream hand-off
-  const bool row_ok = j0 + lane < a.nj;
-  auto real = [&](int t) { return row_ok && t - lane >= 0 && t - lane < a.ni; };
-  // plane pointers inside a slot: C group, X group (rhs|dq*), faces (F tail | B)
-  auto slot_ptrs = [&](int buf, int kk, const double*& pc, const double*& px, const double*& pfc) {
-    pc = ringC + buf * slotC + (long long)kk * NC * 32 + lane;
-    px = ringX + buf * slotX + (long long)kk * NX * 32 + lane;
-    pfc = BWD ? ringB + buf * slotB + (long long)kk * 8 * 32 + lane : px + (long long)nv * 32;
-  };
-  if (warp == 0) {
-    // ------------------------------ flow chain: 5 components per row
-    double oi[5] = {0, 0, 0, 0, 0}, oj[5] = {0, 0, 0, 0, 0};
-    for (int ks = 0; ks < nslots; ++ks) {
-      const int k = BWD ? nslots - 1 - ks : ks;
-      const int buf = ks % D;
-      mbar_wait(&full_bar[buf], (ks / D) & 1);
-      const double* hb = hin + buf * WK * nv;
+  const int lane = threadIdx.x & 31;
+  const WaveArgs& a = *x.a;
+  const long long slot = (long long)WK * NG * 32;
+  int avail = 0;
+  double oi[5] = {0, 0, 0, 0, 0}, oj[5] = {0, 0, 0, 0, 0};
+  int buf = 0, phase = 0;
+  for (int ks = 0; ks < x.nslots; ++ks) {
+    const int k = BWD ? x.nslots - 1 - ks : ks;
+    mbar_wait(&x.full_bar[buf], phase);
+    const double* base = x.ring + buf * slot + lane;
+    double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO) * 32 + lane;
 #pragma unroll
-      for (int mstep = 0; mstep < WK; ++mstep) {
-        const int kk = BWD ? WK - 1 - mstep : mstep;
+    for (int g = 0; g < WK / GSTEP; ++g) {
+      {
+        const int ma = g * GSTEP, mb = ma + GSTEP - 1;
+        chain_group_wait<BWD>(x, k * WK + (BWD ? WK - 1 - ma : ma),
+                              k * WK + (BWD ? WK - 1 - mb : mb), avail);
+      }
+#pragma unroll
+      for (int mm = 0; mm < GSTEP; ++mm) {
+        const int m = g * GSTEP + mm;
+        const int kk = BWD ? WK - 1 - m : m;
         const int t = k * WK + kk;
-        const double *pc, *px, *pf;
-        slot_ptrs(buf, kk, pc, px, pf);
+        const double* p = base + kk * NG * 32;
+        const int qn = BWD ? a.ni - 1 - t + x.rt : t;
+        const bool hin_ok = x.first && x.has_up && qn >= 0 && qn < a.ni;
         double ij[5];
 #pragma unroll
-        for (int c = 0; c < 5; ++c)
-          ij[c] = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
-        if (first) {
-#pragma unroll
-          for (int c = 0; c < 5; ++c) ij[c] = hb[kk * nv + c];
+        for (int c = 0; c < 5; ++c) {
+          const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
+          ij[c] = x.first ? (hin_ok ? x.hin[(qn % HRING) * 5 + c] : 0.0) : sh;
         }
-        const double invd = pc[rm.invd() * 32];
+        const double invd = p[0];
         double dq[5];
 #pragma unroll
         for (int c = 0; c < 5; ++c) {
-          if (BWD) dq[c] = px[c * 32] - (oi[c] + ij[c]) * invd;
-          else dq[c] = ((px[c * 32] + oi[c]) + ij[c]) * invd;
-          if (!real(t)) dq[c] = 0.0;  // padding cells carry exactly nothing
+          if (BWD) dq[c] = p[(FB_DQ + c) * 32] - (oi[c] + ij[c]) * invd;
+          else dq[c] = ((p[(11 + c) * 32] + oi[c]) + ij[c]) * invd;
+          ob[(kk * NGO + c) * 32] = dq[c];
         }
-        if (t < T) {
-#pragma unroll
-          for (int c = 0; c < 5; ++c) a.out[gaddr(a.sk, nv, s, t, c, lane)] = dq[c];
-        }
-        // outgoing half-block products through the two faces (rank-2 form)
-        const int pw = rm.w(), pb = rm.b();
-        const double w0 = pc[pw * 32], w1 = pc[(pw + 1) * 32], w2 = pc[(pw + 2) * 32],
-                     w3 = pc[(pw + 3) * 32], w4 = pc[(pw + 4) * 32];
-        const double sb = pc[pb * 32] * dq[0] + pc[(pb + 1) * 32] * dq[1] +
-                          pc[(pb + 2) * 32] * dq[2] + pc[(pb + 3) * 32] * dq[3] +
-                          pc[(pb + 4) * 32] * dq[4];
-        const double u = pc[rm.uv() * 32], v = pc[(rm.uv() + 1) * 32], hr = pc[rm.hr() * 32];
+        const double w0 = p[1 * 32], w1 = p[2 * 32], w2 = p[3 * 32], w3 = p[4 * 32],
+                     w4 = p[5 * 32];
+        // balanced sums: short dependency chains behind dq
+        const double sb = ((p[6 * 32] * dq[0] + p[7 * 32] * dq[1]) +
+                           (p[8 * 32] * dq[2] + p[9 * 32] * dq[3])) + p[10 * 32] * dq[4];
 #pragma unroll
         for (int f = 0; f < 2; ++f) {
-          const double Sx = pf[(4 * f) * 32], Sy = pf[(4 * f + 1) * 32], lam = pf[(4 * f + 2) * 32];
-          const double U = u * Sx + v * Sy;
-          const double sa = (-U * hr) * dq[0] + (Sx * hr) * dq[1] + (Sy * hr) * dq[2];
-          const double sig = 0.5 * (U + sgn * lam);
+          const double* pf = p + (FQ + 7 * f) * 32;
+          const double sa = pf[0] * dq[0] + (pf[32] * dq[1] + pf[64] * dq[2]);
+          const double sig = pf[6 * 32];
           double* o = f == 0 ? oi : oj;
           o[0] = w0 * sa + sig * dq[0];
-          o[1] = w1 * sa + (0.5 * Sx) * sb + sig * dq[1];
-          o[2] = w2 * sa + (0.5 * Sy) * sb + sig * dq[2];
+          o[1] = w1 * sa + pf[3 * 32] * sb + sig * dq[1];
+          o[2] = w2 * sa + pf[4 * 32] * sb + sig * dq[2];
           o[3] = w3 * sa + sig * dq[3];
-          o[4] = w4 * sa + (0.5 * U) * sb + sig * dq[4];
+          o[4] = w4 * sa + pf[5 * 32] * sb + sig * dq[4];
         }
-        const int col = t - lane;
-        if (last && col >= 0 && col < a.ni) {
+        const int qo = BWD ? a.ni - 1 - t : t - x.rt;
+        const bool ho = x.has_down && x.last && qo >= 0 && qo < a.ni;
 #pragma unroll
-          for (int c = 0; c < 5; ++c) hout[(col % HRING) * nv + c] = oj[c];
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&empty_bar[buf]);
-        __threadfence_block();
-        *(volatile int*)&done_cnt[0] = ks + 1;
+        for (int c = 0; c < 5; ++c) st_pred_cg_f64(x.hand_out + qo * 5 + c, oj[c], ho);
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------ species chain: ns scalar chains per row
-    double oi[NSB], oj[NSB];
-#pragma unroll
-    for (int c = 0; c < NSB; ++c) oi[c] = oj[c] = 0.0;
-    const int per = a.nsI > 1;
-    for (int ks = 0; ks < nslots; ++ks) {
-      const int k = BWD ? nslots - 1 - ks : ks;
-      const int buf = ks % D;
-      mbar_wait(&full_bar[buf], (ks / D) & 1);
-      const double* hb = hin + buf * WK * nv;
-#pragma unroll
-      for (int mstep = 0; mstep < WK; ++mstep) {
-        const int kk = BWD ? WK - 1 - mstep : mstep;
-        const int t = k * WK + kk;
-        const double *pc, *px, *pf;
-        slot_ptrs(buf, kk, pc, px, pf);
-        const double u = pc[rm.uv() * 32], v = pc[(rm.uv() + 1) * 32];
-        const double U1 = u * pf[0] + v * pf[32];
-        const double U2 = u * pf[4 * 32] + v * pf[5 * 32];
-        const double c1 = a.sp_scale * (U1 + sgn * pf[3 * 32]);
-        const double c2 = a.sp_scale * (U2 + sgn * pf[7 * 32]);
-        const int col = t - lane;
-        const bool rl = real(t);
-        const double inv0 = pc[rm.invs() * 32];
-#pragma unroll
-        for (int c = 0; c < NSB; ++c) {
-          if (c < ns) {
-            double ijc = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
-            if (first) ijc = hb[kk * nv + 5 + c];
-            const double inv = per ? pc[(rm.invs() + c) * 32] : inv0;
-            double dq;
-            if (BWD) dq = px[(5 + c) * 32] - (oi[c] + ijc) * inv;
-            else dq = ((px[(5 + c) * 32] + oi[c]) + ijc) * inv;
-            if (!rl) dq = 0.0;
-            if (t < T) a.out[gaddr(a.sk, nv, s, t, 5 + c, lane)] = dq;
-            oi[c] = c1 * dq;
-            oj[c] = c2 * dq;
-            if (last && col >= 0 && col < a.ni) hout[(col % HRING) * nv + 5 + c] = oj[c];
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&empty_bar[buf]);
-        __threadfence_block();
-        *(volatile int*)&done_cnt[1] = ks + 1;
-      }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&x.empty_bar[buf]);
+    if (++buf == x.D) {
+      buf = 0;
+      phase ^= 1;
     }
   }
 }
 
+// species chain: NSB independent scalar chains per row (padding species carry
+// zero records, so they stay exactly zero).  PER: one diagonal per species
+// (chemistry) instead of one shared diagonal.
+template <int NSB, bool BWD, bool PER>
+CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro) {
+  constexpr int WK = wave_wks<NSB>();
+  constexpr int NI = PER ? NSB : 1, NG = NI + NSB + 2;
+  constexpr int PC = BWD ? NI : NI + NSB;   // c_i, c_j planes
+  constexpr int PV = BWD ? NI + 2 : NI;     // dq* (backward) | rhs (forward) planes
+  constexpr int NGO = BWD ? NSB : NG, PO = BWD ? 0 : NI + 2;  // output: SW | SB dq* planes
+  constexpr int G = WK < GSTEP ? WK : GSTEP;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const WaveArgs& a = *x.a;
+  const long long slot = (long long)WK * NG * 32;
+  int avail = 0;
+  double oi[NSB], oj[NSB];
+#pragma unroll
+  for (int c = 0; c < NSB; ++c) oi[c] = oj[c] = 0.0;
+  int buf = 0, phase = 0;
+  for (int ks = 0; ks < x.nslots; ++ks) {
+    const int k = BWD ? x.nslots - 1 - ks : ks;
+    mbar_wait(&x.full_bar[buf], phase);
+    const double* base = x.ring + buf * slot + lane;
+    double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO) * 32 + lane;
+#pragma unroll
+    for (int g = 0; g < WK / G; ++g) {
+      {
+        const int ma = g * G, mb = ma + G - 1;
+        chain_group_wait<BWD>(x, k * WK + (BWD ? WK - 1 - ma : ma),
+                              k * WK + (BWD ? WK - 1 - mb : mb), avail);
+      }
+#pragma unroll
+      for (int mm = 0; mm < G; ++mm) {
+        const int m = g * G + mm;
+        const int kk = BWD ? WK - 1 - m : m;
+        const int t = k * WK + kk;
+        const double* p = base + kk * NG * 32;
+        const int qn = BWD ? a.ni - 1 - t + x.rt : t;
+        const bool hin_ok = x.first && x.has_up && qn >= 0 && qn < a.ni;
+        double ij[NSB];
+#pragma unroll
+        for (int c = 0; c < NSB; ++c) {
+          const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
+          ij[c] = x.first ? (hin_ok ? x.hin[(qn % HRING) * NSB + c] : 0.0) : sh;
+        }
+        const double ci = p[PC * 32], cj = p[(PC + 1) * 32];
+#pragma unroll
+        for (int c = 0; c < NSB; ++c) {
+          const double inv = p[(PER ? c : 0) * 32];
+          const double v = p[(PV + c) * 32];
+          const double dq = BWD ? v - (oi[c] + ij[c]) * inv : ((v + oi[c]) + ij[c]) * inv;
+          ob[(kk * NGO + c) * 32] = dq;
+          oi[c] = ci * dq;
+          oj[c] = cj * dq;
+        }
+        const int qo = BWD ? a.ni - 1 - t : t - x.rt;
+        const bool ho = x.has_down && x.last && qo >= 0 && qo < a.ni;
+#pragma unroll
+        for (int c = 0; c < NSB; ++c) st_pred_cg_f64(x.hand_out + qo * NSB + c, oj[c], ho);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&x.empty_bar[buf]);
+    if (++buf == x.D) {
+      buf = 0;
+      phase ^= 1;
+    }
+  }
+}
+
+template <int NSB, bool BWD, bool PER>
+__global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
+  extern __shared__ __align__(128) double wsm[];
+  __shared__ unsigned long long full_bar[8], empty_bar[8];
+  __shared__ int s_strip, consumed, recv_cnt;
+  __shared__ unsigned long long t_first;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kind = a.only >= 0 ? a.only : (blockIdx.x & 1);  // 0 flow, 1 species
+  const WaveRole ro = kind ? a.role[1] : a.role[0];
+  const int WK = kind ? wave_wks<NSB>() : WKF;
+  const int nh = kind ? NSB : 5;
+  const int D = ro.D, NG = ro.ng;
+  const long long slot = (long long)WK * NG * 32;
+  double* ring = wsm;                     // [D][WK][NG][32]
+  double* hin = ring + D * slot;          // [HRING][nh]
+  if (threadIdx.x == 0) {
+    const int tk = atomicAdd(ro.ticket, 1);
+    s_strip = BWD ? a.sk.nstrip - 1 - tk : tk;
+    for (int b = 0; b < D; ++b) {
+      mbar_init(&full_bar[b], 1);
+      mbar_init(&empty_bar[b], 1);
+    }
+    consumed = 0;
+    recv_cnt = 0;
+    t_first = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  ChainCtx x;
+  x.a = &a;
+  x.s = s_strip;
+  x.D = D;
+  x.rt = min(31, a.nj - 1 - x.s * 32);  // highest valid row of this strip
+  const int T = a.sk.T;
+  x.nslots = T / WK;
+  x.has_up = BWD ? (x.s + 1 < a.sk.nstrip) : (x.s > 0);
+  x.has_down = BWD ? (x.s > 0) : (x.s + 1 < a.sk.nstrip);
+  x.first = BWD ? (lane == x.rt) : (lane == 0);  // receives the upstream hand-off
+  x.last = BWD ? (lane == 0) : (lane == x.rt);   // sends the downstream hand-off
+  x.ring = ring;
+  x.hin = hin;
+  x.hand_out = ro.hand + (long long)x.s * a.ni * nh;
+  x.full_bar = full_bar;
+  x.empty_bar = empty_bar;
+  x.consumed = &consumed;
+  x.recv_cnt = &recv_cnt;
+  x.t_first = &t_first;
+  const int s = x.s;
+  const int up = BWD ? s + 1 : s - 1;
+
+  if (warp == 1) {
+    // ---------------------------------------------------- producer (TMA)
+    if (lane == 0) {
+      for (int ks = 0; ks < x.nslots; ++ks) {
+        const int k = BWD ? x.nslots - 1 - ks : ks;
+        const int buf = ks % D;
+        if (ks >= D) mbar_wait(&empty_bar[buf], ((ks / D) - 1) & 1);
+        const unsigned bytes = (unsigned)(slot * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         smem_u32(&full_bar[buf])),
+                     "r"(bytes)
+                     : "memory");
+        bulk_g2s(ring + buf * slot, ro.in + ((long long)s * T + (long long)k * WK) * NG * 32, bytes,
+                 &full_bar[buf]);
+      }
+    }
+    return;
+  }
+
+  if (warp == 2) {
+    // ---------------------------------------------------- receiver
+    // lane l polls column next + l of the upstream strip; the complete prefix
+    // of columns is copied into hin (bounded by what the chain consumed)
+    if (!x.has_up) return;
+    const int ni = a.ni;
+    const double* src = ro.hand + (long long)up * ni * nh;
+    int next = 0;
+    while (next < ni) {
+      const int lim = min(ni, ld_volatile_s(&consumed) + HRING);
+      const int q = next + lane;
+      bool ok = q < lim;
+      if (ok)
+        for (int c = 0; c < nh; ++c) ok &= ld_relaxed_u64(src + (long long)q * nh + c) != HAND_SENTINEL;
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      const int n = __ffs(~bal) ? __ffs(~bal) - 1 : 32;  // complete prefix length
+      if (n > 0) {
+        if (lane < n)
+          for (int c = 0; c < nh; ++c)
+            hin[(q % HRING) * nh + c] = __longlong_as_double(
+                (long long)ld_relaxed_u64(src + (long long)q * nh + c));
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          *(volatile int*)&recv_cnt = next + n;
+        }
+        next += n;
+      } else {
+        __nanosleep(16);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------- chain (warp 0)
+  unsigned long long t0 = 0;
+  if (a.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  if (kind == 0) chain_flow<BWD>(x, ro);
+  else chain_species<NSB, BWD, PER>(x, ro);
+  if (a.dbg && lane == 0) {
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    unsigned long long* d = a.dbg + 4 * (2 * s + kind);
+    d[0] = t0;
+    d[1] = t1;
+    d[2] = t_first;
+  }
+}
+
 // ============================================================== epilogue
+// Tile = one strip x C steps (a parallelogram in (i, j), as in k_records2d).
+// Phase A: the step-major dq rows -> smem (a warp reads one contiguous row);
+// phase B: closure + gate column by column, so the q / q_new accesses of a
+// warp are contiguous runs of up to C cells.
 template <int NSB>
 __global__ void __launch_bounds__(256) k_epilogue2d(const Model* __restrict__ mp, GridDev g, Skew sk,
                                                     int scheme, const double* __restrict__ q,
-                                                    const double* __restrict__ dqw,
+                                                    const double* __restrict__ fw,
+                                                    const double* __restrict__ sw,
                                                     double* __restrict__ qn,
                                                     double* __restrict__ dq_std, int C,
                                                     unsigned long long* flags) {
   extern __shared__ double es[];
   const Model& m = *mp;
   const int ns = m.ns, nv = 5 + ns;
-  const int ncb = (g.ni + C - 1) / C;
+  const int ncb = sk.T / C;
   const int s = blockIdx.x / ncb, ib = blockIdx.x % ncb;
-  const int i0 = ib * C, j0 = s * 32;
+  const int t0 = ib * C, j0 = s * 32;
   const int CT = C * 32;
   const long long N = g.N;
-  // phase A: skewed dq -> smem (tile-local column-major)
-  const int nt = C + 31;
-  for (int e = threadIdx.x; e < nt * 32; e += blockDim.x) {
+  for (int e = threadIdx.x; e < CT; e += blockDim.x) {
     const int tt = e / 32, r = e % 32;
-    const int ii = tt - r;
-    if (ii < 0 || ii >= C || i0 + ii >= g.ni || j0 + r >= g.nj) continue;
-    const int t = i0 + ii + r;
-    for (int c = 0; c < nv; ++c) es[c * CT + ii * 32 + r] = dqw[gaddr(sk, nv, s, t, c, r)];
+    const int t = t0 + tt;
+    const int i = t - r;
+    if (i < 0 || i >= g.ni || j0 + r >= g.nj) continue;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) es[k * CT + e] = fw[gaddr(sk, 5, s, t, k, r)];
+    for (int k = 0; k < ns; ++k) es[(5 + k) * CT + e] = sw[gaddr(sk, NSB, s, t, k, r)];
   }
   __syncthreads();
-  // phase B: closure + gate in standard order (coalesced over j)
   unsigned long long bad_count = 0, first1 = ~0ull, first2 = ~0ull;
-  for (int e = threadIdx.x; e < CT; e += blockDim.x) {
-    const int ii = e / 32, r = e % 32;
-    const int i = i0 + ii, j = j0 + r;
-    if (i >= g.ni || j >= g.nj) continue;
+  // i' = tt - r in [-31, C - 1], r in [max(0, -i'), min(31, C - 1 - i')]
+  for (int l = threadIdx.x; l < (C + 31) * C; l += blockDim.x) {
+    const int ip = -31 + l / C;
+    const int r = max(0, -ip) + l % C;
+    if (r > min(31, C - 1 - ip)) continue;
+    const int e = (ip + r) * 32 + r;
+    const int i = t0 + ip, j = j0 + r;
+    if (i < 0 || i >= g.ni || j >= g.nj) continue;
     const long long c = (long long)i * g.nj + j;
     double d[5 + NSB];
 #pragma unroll
@@ -650,16 +801,13 @@ __global__ void __launch_bounds__(256) k_epilogue2d(const Model* __restrict__ mp
 }
 
 // ============================================================== launcher
-inline size_t wave_smem(int D, int NC, int NX, int NB, int nv) {
-  return ((size_t)D * WK * 32 * (NC + NX + NB) + (size_t)D * WK * nv + (size_t)HRING * nv) *
-         sizeof(double);
+inline size_t wave_role_smem(int D, int WK, int NG, int nh) {
+  return ((size_t)D * WK * NG * 32 + (size_t)HRING * nh) * sizeof(double);
 }
-
-inline int wave_ring_depth(int NC, int nv) {
-  const int NX = nv + 8;  // forward is the larger of the two layouts
-  for (int D = 6; D >= 2; --D)
-    if (wave_smem(D, NC, NX, 0, nv) <= 215 * 1024 && wave_smem(D, NC, nv, 8, nv) <= 215 * 1024)
-      return D;
+// deepest ring (2..4) that fits the shared-memory budget, 0 if none
+inline int wave_depth(int WK, int NG, int nh) {
+  for (int D = 4; D >= 2; --D)
+    if (wave_role_smem(D, WK, NG, nh) <= 210 * 1024) return D;
   return 0;
 }
 
@@ -670,61 +818,90 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
                                      double* dq_std, unsigned long long* flags, cudaStream_t st,
                                      cudaEvent_t* ev) {
   CSB_NS_DISPATCH(ns, {
-    const int nv = 5 + ns, nsI = per_species ? ns : 1;
+    const int nsI = per_species ? NSB : 1;
     const Skew& sk = wb.sk;
-    const int NC = 14 + nsI, NF = nv + 8;
-    const int D = wave_ring_depth(NC, nv);
-    if (D == 0) return cudaErrorInvalidConfiguration;
-    // records
+    const int NSF = nsI + NSB + 2;
+    constexpr int WKS = wave_wks<NSB>();
+    const int Df = wave_depth(WKF, NFF, 5), Ds = wave_depth(WKS, NSF, NSB);
+    if (!Df || !Ds) return cudaErrorInvalidConfiguration;
+    // ---------------- records
     int C = 8;
+    if (const char* ev_c = getenv("CSB_REC_C")) C = atoi(ev_c);  // tuning probe
     auto rsm_of = [&](int c) {
-      return ((size_t)(NC + NF + 8) * c * 32 + 7 * (size_t)(c + 2) * 34) * sizeof(double);
+      return ((size_t)(16 + nsI + NSB) * c * 32 + 12 * (size_t)(c + 2) * 34) * sizeof(double);
     };
     while (C > 1 && rsm_of(C) > 200 * 1024) C /= 2;
     const size_t rsm = rsm_of(C);
     cudaFuncSetAttribute(k_records2d<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
-    const int ncb = (g.ni + C - 1) / C;
+    const int ncb = sk.T / C;
     if (ev) cudaEventRecord(ev[0], st);
     k_records2d<NSB><<<sk.nstrip * ncb, 256, rsm, st>>>(mp, g, sk, q, R, cfl, lamS, domd,
-                                                        dom_stride, per_species, wb.recC, wb.recF,
-                                                        wb.recB, C, flags);
+                                                        dom_stride, per_species, sp_scale, wb, C,
+                                                        flags);
     if (ev) cudaEventRecord(ev[1], st);
-    // sweeps
-    WaveArgs wa;
-    wa.sk = sk;
-    wa.ni = g.ni;
-    wa.nj = g.nj;
-    wa.ns = ns;
-    wa.nv = nv;
-    wa.nsI = nsI;
-    wa.nslots = sk.T / WK;
-    wa.D = D;
-    wa.recC = wb.recC;
-    wa.hand = wb.hand;
-    wa.prog = wb.prog;
-    wa.ticket = wb.prog + sk.nstrip;
-    wa.sp_scale = sp_scale;
-    const size_t fsm = wave_smem(D, NC, NF, 0, nv), bsm = wave_smem(D, NC, nv, 8, nv);
-    cudaFuncSetAttribute(k_wave2d<NSB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
-    cudaFuncSetAttribute(k_wave2d<NSB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
-    cudaMemsetAsync(wb.prog, 0, sizeof(int) * (sk.nstrip + 1), st);
-    wa.recX = wb.recF;
-    wa.recB = nullptr;
-    wa.out = wb.dqs;
-    k_wave2d<NSB, false><<<sk.nstrip, 128, fsm, st>>>(wa);
-    if (ev) cudaEventRecord(ev[2], st);
-    cudaMemsetAsync(wb.prog, 0, sizeof(int) * (sk.nstrip + 1), st);
-    wa.recX = wb.dqs;
-    wa.recB = wb.recB;
-    wa.out = wb.dqw;
-    k_wave2d<NSB, true><<<sk.nstrip, 128, bsm, st>>>(wa);
-    if (ev) cudaEventRecord(ev[3], st);
-    // epilogue
-    const int CE = 8;
-    const size_t esm = (size_t)nv * CE * 32 * sizeof(double);
+    // ---------------- sweeps: one flow and one species CTA per strip
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool bwd = pass == 1;
+      WaveArgs wa;
+      wa.sk = sk;
+      wa.ni = g.ni;
+      wa.nj = g.nj;
+      wa.nsI = nsI;
+      wa.only = -1;
+      if (const char* ev_o = getenv("CSB_WAVE_ONLY")) wa.only = atoi(ev_o);  // timing probe
+      static unsigned long long* dbg = nullptr;
+      wa.dbg = nullptr;
+      if (getenv("CSB_WAVE_DBG")) {
+        if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 4 * 2 * 4096);
+        cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 4 * 2 * sk.nstrip, st);
+        wa.dbg = dbg;
+      }
+      WaveRole& rf = wa.role[0];
+      WaveRole& rs = wa.role[1];
+      rf.in = bwd ? wb.fb : wb.ff;
+      rf.ng = bwd ? NFB : NFF;
+      rf.D = Df;
+      rf.out = bwd ? wb.fw : wb.fb;
+      rf.ngo = bwd ? 5 : NFB;
+      rf.po = bwd ? 0 : FB_DQ;
+      const long long hsz = (long long)sk.nstrip * g.ni * (5 + NSB);  // one sweep
+      rf.hand = wb.hand + (bwd ? hsz : 0);
+      rf.ticket = wb.prog;
+      rs.in = bwd ? wb.sb : wb.sf;
+      rs.ng = NSF;
+      rs.D = Ds;
+      rs.out = bwd ? wb.sw : wb.sb;
+      rs.ngo = bwd ? NSB : NSF;
+      rs.po = bwd ? 0 : nsI + 2;
+      rs.hand = wb.hand + (bwd ? hsz : 0) + (long long)sk.nstrip * g.ni * 5;
+      rs.ticket = wb.prog + 1;
+      const size_t smem = std::max(wave_role_smem(Df, WKF, NFF, 5), wave_role_smem(Ds, WKS, NSF, NSB));
+      auto kfn = bwd ? (per_species ? k_wave2d<NSB, true, true> : k_wave2d<NSB, true, false>)
+                     : (per_species ? k_wave2d<NSB, false, true> : k_wave2d<NSB, false, false>);
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaMemsetAsync(wb.prog, 0, sizeof(int) * 2, st);
+      kfn<<<(wa.only >= 0 ? 1 : 2) * sk.nstrip, 96, smem, st>>>(wa);
+      if (wa.dbg) {
+        std::vector<unsigned long long> h(4 * 2 * sk.nstrip);
+        cudaMemcpyAsync(h.data(), wa.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        unsigned long long tmin = ~0ull;
+        for (int e = 0; e < 2 * sk.nstrip; ++e)
+          if (h[4 * e]) tmin = std::min(tmin, h[4 * e]);
+        for (int e = 0; e < 2 * sk.nstrip; ++e)
+          if (h[4 * e])
+            fprintf(stderr, "wave%s strip %d kind %d: start %.2f first %.2f end %.2f us\n",
+                    bwd ? "B" : "F", e / 2, e % 2, (h[4 * e] - tmin) * 1e-3,
+                    h[4 * e + 2] ? (h[4 * e + 2] - tmin) * 1e-3 : -1.0, (h[4 * e + 1] - tmin) * 1e-3);
+      }
+      if (ev) cudaEventRecord(ev[2 + pass], st);
+    }
+    // ---------------- epilogue
+    const int CE = 16;
+    const size_t esm = (size_t)(5 + ns) * CE * 32 * sizeof(double);
     cudaFuncSetAttribute(k_epilogue2d<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
-    k_epilogue2d<NSB><<<sk.nstrip * ((g.ni + CE - 1) / CE), 256, esm, st>>>(
-        mp, g, sk, scheme, q, wb.dqw, qn, dq_std, CE, flags);
+    k_epilogue2d<NSB><<<sk.nstrip * (sk.T / CE), 256, esm, st>>>(mp, g, sk, scheme, q, wb.fw,
+                                                                 wb.sw, qn, dq_std, CE, flags);
     if (ev) cudaEventRecord(ev[4], st);
   });
   return cudaGetLastError();

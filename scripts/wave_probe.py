@@ -22,7 +22,7 @@ from paper_2403_03440_b200.device import get_engine  # noqa: E402
 from paper_2403_03440_b200.spatial import residual_device  # noqa: E402
 
 
-def probe(ni, nj, ns=5, reps=5):
+def probe(ni, nj, ns=5, reps=int(os.environ.get("REPS", 5))):
     spec = C.config0(seed=1, dims=(ni, nj, 1)) if ns == 5 else C.config3(ns, dims=(ni, nj, 1))
     grid, model, bcs, mech = build_case(spec)
     eng = get_engine(grid, model)
@@ -42,7 +42,7 @@ def probe(ni, nj, ns=5, reps=5):
                 acc[k] += ms5[k] / reps
     eng.status()
     nstrip = (nj + 31) // 32
-    T = ((ni + 31 + 3) // 4) * 4
+    T = ((ni + 31 + 15) // 16) * 16
     fwd = acc[2]
     print(f"{ni:5d}x{nj:<5d} ns={ns:2d} strips={nstrip:3d} T={T:5d}  records {acc[1]*1e3:8.1f} us  "
           f"fwd {fwd*1e3:8.1f} us  bwd {acc[3]*1e3:8.1f} us  epi {acc[4]*1e3:7.1f} us  "
@@ -55,4 +55,5 @@ if __name__ == "__main__":
         (512, 32), (2048, 32), (512, 64), (512, 128), (512, 256), (512, 512), (1024, 1024)]
     for ni, nj in shapes:
         probe(ni, nj)
-    probe(512, 512, ns=11)
+    if not args:
+        probe(512, 512, ns=11)
