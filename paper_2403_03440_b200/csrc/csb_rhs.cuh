@@ -192,122 +192,134 @@ CSB_DEV bool face_state(const Model& m, const double* W, double& T, double& c, d
   return ok;
 }
 
-// Total flux through one face into F[c*ldF] (c < nv).  sP: staged padded
-// primitives, component plane stride ldP; cell offsets im/ip (the two
-// adjacent cells), imm/ipp (MUSCL outer cells), tangential strides st[2].
+// Face flux = convective part (face_conv, writes F) + viscous part
+// (face_visc, adds to F), evaluated in two passes so that their register
+// footprints do not add up.  sP: staged padded primitives, component plane
+// stride ldP; cell offsets im/ip (the two adjacent cells), imm/ipp (MUSCL
+// outer cells), tangential strides st[2].
+
+// Convective part: Rusanov on MUSCL-minmod states (spatial.py:217-226,
+// rusanov_flux 171-204).
 template <int NSB>
-CSB_DEV bool face_flux(const Model& m, const double* sP, int ldP, int imm, int im, int ip, int ipp,
-                       const int st[2], const FaceGeom& fg, bool first_order, double* F, int ldF) {
+CSB_DEV bool face_conv(const Model& m, const double* sP, int ldP, int imm, int im, int ip, int ipp,
+                       const double S[3], bool first_order, double* F, int ldF) {
   const int ns = m.ns;
   const int nv = 5 + ns;
   bool ok = true;
-  // ---------------- convective part (Rusanov on MUSCL states)
-  {
-    double WL[5 + NSB], WR[5 + NSB];
+  double WL[5 + NSB], WR[5 + NSB];
 #pragma unroll
-    for (int c = 0; c < 5 + NSB; ++c) {
-      if (c < nv) {
-        const double vm = sP[c * ldP + im];
-        const double vp = sP[c * ldP + ip];
-        if (first_order) {
-          WL[c] = vm;
-          WR[c] = vp;
-        } else {
-          const double vmm = sP[c * ldP + imm];
-          const double vpp = sP[c * ldP + ipp];
-          const double dc = vp - vm;
-          WL[c] = vm + 0.5 * minmod(vm - vmm, dc);
-          WR[c] = vp - 0.5 * minmod(dc, vpp - vp);
-        }
+  for (int c = 0; c < 5 + NSB; ++c) {
+    if (c < nv) {
+      const double vm = sP[c * ldP + im];
+      const double vp = sP[c * ldP + ip];
+      if (first_order) {
+        WL[c] = vm;
+        WR[c] = vp;
+      } else {
+        const double vmm = sP[c * ldP + imm];
+        const double vpp = sP[c * ldP + ipp];
+        const double dc = vp - vm;
+        WL[c] = vm + 0.5 * minmod(vm - vmm, dc);
+        WR[c] = vp - 0.5 * minmod(dc, vpp - vp);
       }
-    }
-    double TL, cL, eL, TR, cR, eR;
-    ok &= face_state<NSB>(m, WL, TL, cL, eL);
-    ok &= face_state<NSB>(m, WR, TR, cR, eR);
-    const double* S = fg.S;
-    const double UL = WL[1] * S[0] + WL[2] * S[1] + WL[3] * S[2];
-    const double UR = WR[1] * S[0] + WR[2] * S[1] + WR[3] * S[2];
-    const double area = sqrt((S[0] * S[0] + S[1] * S[1]) + S[2] * S[2]);
-    const double lam = npmax(fabs(UL) + cL * area, fabs(UR) + cR * area);
-    const double hl = 0.5 * lam;
-    // c = 0
-    {
-      const double qL = WL[0], qR = WR[0];
-      F[0] = 0.5 * (UL * qL + UR * qR) - hl * (qR - qL);
-    }
-#pragma unroll
-    for (int x = 0; x < 3; ++x) {
-      const double qL = WL[0] * WL[1 + x], qR = WR[0] * WR[1 + x];
-      const double fl = UL * qL + WL[4] * S[x];
-      const double fr = UR * qR + WR[4] * S[x];
-      F[(1 + x) * ldF] = 0.5 * (fl + fr) - hl * (qR - qL);
-    }
-    {
-      const double qL = WL[0] * eL, qR = WR[0] * eR;
-      const double fl = UL * qL + WL[4] * UL;
-      const double fr = UR * qR + WR[4] * UR;
-      F[4 * ldF] = 0.5 * (fl + fr) - hl * (qR - qL);
-    }
-#pragma unroll
-    for (int s = 0; s < NSB; ++s) {
-      if (s < ns) {
-        const double qL = WL[0] * WL[5 + s], qR = WR[0] * WR[5 + s];
-        F[(5 + s) * ldF] = 0.5 * (UL * qL + UR * qR) - hl * (qR - qL);
-      }
+    } else {
+      WL[c] = WR[c] = 0.0;
     }
   }
-  // ---------------- viscous part (spatial.py:227-256, viscous_flux 143-168)
+  double TL, cL, eL, TR, cR, eR;
+  ok &= face_state<NSB>(m, WL, TL, cL, eL);
+  ok &= face_state<NSB>(m, WR, TR, cR, eR);
+  const double UL = WL[1] * S[0] + WL[2] * S[1] + WL[3] * S[2];
+  const double UR = WR[1] * S[0] + WR[2] * S[1] + WR[3] * S[2];
+  const double area = sqrt((S[0] * S[0] + S[1] * S[1]) + S[2] * S[2]);
+  const double lam = npmax(fabs(UL) + cL * area, fabs(UR) + cR * area);
+  const double hl = 0.5 * lam;
   {
-    const int iT = 5 + ns;
-    double Wf[5 + NSB];
+    const double qL = WL[0], qR = WR[0];
+    F[0] = 0.5 * (UL * qL + UR * qR) - hl * (qR - qL);
+  }
 #pragma unroll
-    for (int c = 0; c < 5 + NSB; ++c)
-      if (c < nv) Wf[c] = 0.5 * (sP[c * ldP + im] + sP[c * ldP + ip]);
-    double Tf, cf, ef;
-    ok &= face_state<NSB>(m, Wf, Tf, cf, ef);
-    const double rho = Wf[0];
-    double mu, kc, D;
-    transport<NSB>(m, Tf, Wf + 5, rho, mu, kc, D);
-    // gradient of component c, in the reference's summation order
-    // grad = grads[0] + grads[1] + grads[2] with grads[d] the normal part.
-    auto grad = [&](int c, double g[3]) {
-      const double dn = sP[c * ldP + ip] - sP[c * ldP + im];
-      double part[3][3];
-      int filled[3] = {0, 0, 0};
-      // normal direction: axis id is the one not in ta
-      int d = 3 - fg.ta[0] - fg.ta[1];
+  for (int x = 0; x < 3; ++x) {
+    const double qL = WL[0] * WL[1 + x], qR = WR[0] * WR[1 + x];
+    const double fl = UL * qL + WL[4] * S[x];
+    const double fr = UR * qR + WR[4] * S[x];
+    F[(1 + x) * ldF] = 0.5 * (fl + fr) - hl * (qR - qL);
+  }
+  {
+    const double qL = WL[0] * eL, qR = WR[0] * eR;
+    const double fl = UL * qL + WL[4] * UL;
+    const double fr = UR * qR + WR[4] * UR;
+    F[4 * ldF] = 0.5 * (fl + fr) - hl * (qR - qL);
+  }
 #pragma unroll
-      for (int x = 0; x < 3; ++x) part[d][x] = dn * fg.xn[x];
-      filled[d] = 1;
+  for (int s = 0; s < NSB; ++s) {
+    if (s < ns) {
+      const double qL = WL[0] * WL[5 + s], qR = WR[0] * WR[5 + s];
+      F[(5 + s) * ldF] = 0.5 * (UL * qL + UR * qR) - hl * (qR - qL);
+    }
+  }
+  return ok;
+}
+
+// Gradient of staged component c at the face, in the reference's summation
+// order: grad = grads[0] + grads[1] + grads[2] with grads[d] the part along
+// axis d (spatial.py:227-248).
+CSB_DEV void face_grad(const double* sP, int ldP, int im, int ip, const int st[2],
+                       const FaceGeom& fg, int c, double g[3]) {
+  const double dn = sP[c * ldP + ip] - sP[c * ldP + im];
+  double part[3][3];
+  int filled[3] = {0, 0, 0};
+  const int d = 3 - fg.ta[0] - fg.ta[1];  // normal axis
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int a = fg.ta[t];
-        if (fg.use_t[t]) {
-          const int s = st[t];
-          const double cdm = 0.5 * (sP[c * ldP + im + s] - sP[c * ldP + im - s]);
-          const double cdp = 0.5 * (sP[c * ldP + ip + s] - sP[c * ldP + ip - s]);
-          const double dP = 0.5 * (cdm + cdp);
+  for (int x = 0; x < 3; ++x) part[d][x] = dn * fg.xn[x];
+  filled[d] = 1;
 #pragma unroll
-          for (int x = 0; x < 3; ++x) part[a][x] = dP * fg.xt[t][x];
-          filled[a] = 1;
-        }
-      }
+  for (int t = 0; t < 2; ++t) {
+    const int a = fg.ta[t];
+    if (fg.use_t[t]) {
+      const int s = st[t];
+      const double cdm = 0.5 * (sP[c * ldP + im + s] - sP[c * ldP + im - s]);
+      const double cdp = 0.5 * (sP[c * ldP + ip + s] - sP[c * ldP + ip - s]);
+      const double dP = 0.5 * (cdm + cdp);
 #pragma unroll
-      for (int x = 0; x < 3; ++x) {
-        double v = filled[0] ? part[0][x] : 0.0;
-        v = filled[1] ? (filled[0] ? v + part[1][x] : part[1][x]) : v;
-        v = filled[2] ? ((filled[0] || filled[1]) ? v + part[2][x] : part[2][x]) : v;
-        g[x] = v;
-      }
-    };
-    double gu[3][3], gT[3];
+      for (int x = 0; x < 3; ++x) part[a][x] = dP * fg.xt[t][x];
+      filled[a] = 1;
+    }
+  }
 #pragma unroll
-    for (int i = 0; i < 3; ++i) grad(1 + i, gu[i]);
-    grad(iT, gT);
+  for (int x = 0; x < 3; ++x) {
+    double v = filled[0] ? part[0][x] : 0.0;
+    v = filled[1] ? (filled[0] ? v + part[1][x] : part[1][x]) : v;
+    v = filled[2] ? ((filled[0] || filled[1]) ? v + part[2][x] : part[2][x]) : v;
+    g[x] = v;
+  }
+}
+
+// Viscous part (spatial.py:227-256, viscous_flux 143-168), added to F.
+// The species diffusion fluxes are formed twice (once for their zero-sum
+// correction, once for the fluxes) instead of being kept in registers.
+template <int NSB>
+CSB_DEV bool face_visc(const Model& m, const double* sP, int ldP, int im, int ip, const int st[2],
+                       const FaceGeom& fg, double* F, int ldF) {
+  const int ns = m.ns;
+  const int nv = 5 + ns;
+  const int iT = 5 + ns;
+  double Wf[5 + NSB];
+#pragma unroll
+  for (int c = 0; c < 5 + NSB; ++c) Wf[c] = c < nv ? 0.5 * (sP[c * ldP + im] + sP[c * ldP + ip]) : 0.0;
+  double Tf, cf, ef;
+  const bool ok = face_state<NSB>(m, Wf, Tf, cf, ef);
+  const double rho = Wf[0];
+  double mu, kc, D;
+  transport<NSB>(m, Tf, Wf + 5, rho, mu, kc, D);
+  const double* S = fg.S;
+  double tS[3];
+  {
+    double gu[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) face_grad(sP, ldP, im, ip, st, fg, 1 + i, gu[i]);
     const double div = (gu[0][0] + gu[1][1]) + gu[2][2];
     const double tdiv = 2.0 / 3.0 * mu * div;
-    double tS[3];
-    const double* S = fg.S;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
       double acc = 0.0;
@@ -319,48 +331,193 @@ CSB_DEV bool face_flux(const Model& m, const double* sP, int ldP, int imm, int i
       }
       tS[i] = acc;
     }
-    // species diffusion with zero-sum correction
-    double js[NSB][3];
-    double jsum[3] = {0.0, 0.0, 0.0};
-    const double nrd = -(rho * D);
-#pragma unroll
-    for (int s = 0; s < NSB; ++s) {
-      if (s < ns) {
-        double gy[3];
-        grad(5 + s, gy);
-#pragma unroll
-        for (int x = 0; x < 3; ++x) {
-          js[s][x] = nrd * gy[x];
-          jsum[x] += js[s][x];
-        }
-      }
-    }
-    double qv[3];
-    double hsj[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int s = 0; s < NSB; ++s) {
-      if (s < ns) {
-        const double hs = m.bs[s] + m.cp[s] * Tf;
-#pragma unroll
-        for (int x = 0; x < 3; ++x) {
-          js[s][x] -= Wf[5 + s] * jsum[x];
-          hsj[x] += hs * js[s][x];
-        }
-      }
-    }
-#pragma unroll
-    for (int x = 0; x < 3; ++x) qv[x] = -kc * gT[x] + hsj[x];
-    F[1 * ldF] += -tS[0];
-    F[2 * ldF] += -tS[1];
-    F[3 * ldF] += -tS[2];
-    const double utS = (Wf[1] * tS[0] + Wf[2] * tS[1]) + Wf[3] * tS[2];
-    const double qS = (qv[0] * S[0] + qv[1] * S[1]) + qv[2] * S[2];
-    F[4 * ldF] += -utS + qS;
-#pragma unroll
-    for (int s = 0; s < NSB; ++s)
-      if (s < ns) F[(5 + s) * ldF] += (js[s][0] * S[0] + js[s][1] * S[1]) + js[s][2] * S[2];
   }
+  // species diffusion with zero-sum correction
+  const double nrd = -(rho * D);
+  double jsum[3] = {0.0, 0.0, 0.0};
+  for (int s = 0; s < ns; ++s) {
+    double gy[3];
+    face_grad(sP, ldP, im, ip, st, fg, 5 + s, gy);
+#pragma unroll
+    for (int x = 0; x < 3; ++x) jsum[x] += nrd * gy[x];
+  }
+  double hsj[3] = {0.0, 0.0, 0.0};
+  for (int s = 0; s < ns; ++s) {
+    double gy[3], js[3];
+    face_grad(sP, ldP, im, ip, st, fg, 5 + s, gy);
+    const double hs = m.bs[s] + m.cp[s] * Tf;
+    const double ys = sP[(5 + s) * ldP + im], yp = sP[(5 + s) * ldP + ip];
+    const double yf = 0.5 * (ys + yp);
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      js[x] = nrd * gy[x] - yf * jsum[x];
+      hsj[x] += hs * js[x];
+    }
+    F[(5 + s) * ldF] += (js[0] * S[0] + js[1] * S[1]) + js[2] * S[2];
+  }
+  double gT[3];
+  face_grad(sP, ldP, im, ip, st, fg, iT, gT);
+  double qv[3];
+#pragma unroll
+  for (int x = 0; x < 3; ++x) qv[x] = -kc * gT[x] + hsj[x];
+  F[1 * ldF] += -tS[0];
+  F[2 * ldF] += -tS[1];
+  F[3 * ldF] += -tS[2];
+  const double utS = (Wf[1] * tS[0] + Wf[2] * tS[1]) + Wf[3] * tS[2];
+  const double qS = (qv[0] * S[0] + qv[1] * S[1]) + qv[2] * S[2];
+  F[4 * ldF] += -utS + qS;
   return ok;
+}
+
+// 2-D (K2D) viscous face of direction D (0: i-face, 1: j-face): the same
+// arithmetic as face_grad/face_visc with the axis bookkeeping resolved at
+// compile time.  grad = part_0 + part_1 (axis order), the normal part along
+// axis D and the central tangential part along the other in-plane axis.
+template <int D>
+CSB_DEV void face_grad2d(const double* sP, int ldP, int im, int ip, int st, const double xn[3],
+                         const double xt[3], int c, double g[3]) {
+  const double dn = sP[c * ldP + ip] - sP[c * ldP + im];
+  const double cdm = 0.5 * (sP[c * ldP + im + st] - sP[c * ldP + im - st]);
+  const double cdp = 0.5 * (sP[c * ldP + ip + st] - sP[c * ldP + ip - st]);
+  const double dP = 0.5 * (cdm + cdp);
+#pragma unroll
+  for (int x = 0; x < 3; ++x) {
+    const double pn = dn * xn[x], pt = dP * xt[x];
+    g[x] = D == 0 ? pn + pt : pt + pn;
+  }
+}
+
+template <int NSB, int D>
+CSB_DEV bool face_visc2d(const Model& m, const double* sP, int ldP, int im, int ip, int st,
+                         const double S[3], const double xn[3], const double xt[3], double* F,
+                         int ldF) {
+  const int ns = m.ns;
+  const int nv = 5 + ns;
+  double Wf[5 + NSB];
+#pragma unroll
+  for (int c = 0; c < 5 + NSB; ++c) Wf[c] = c < nv ? 0.5 * (sP[c * ldP + im] + sP[c * ldP + ip]) : 0.0;
+  double Tf, cf, ef;
+  const bool ok = face_state<NSB>(m, Wf, Tf, cf, ef);
+  const double rho = Wf[0];
+  double mu, kc, Dm;
+  transport<NSB>(m, Tf, Wf + 5, rho, mu, kc, Dm);
+  double tS[3];
+  {
+    double gu[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) face_grad2d<D>(sP, ldP, im, ip, st, xn, xt, 1 + i, gu[i]);
+    const double div = (gu[0][0] + gu[1][1]) + gu[2][2];
+    const double tdiv = 2.0 / 3.0 * mu * div;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        double tau = mu * (gu[i][x] + gu[x][i]);
+        if (x == i) tau -= tdiv;
+        acc = (x == 0) ? tau * S[0] : acc + tau * S[x];
+      }
+      tS[i] = acc;
+    }
+  }
+  const double nrd = -(rho * Dm);
+  double jsum[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int s = 0; s < NSB; ++s) {
+    if (s < ns) {
+      double gy[3];
+      face_grad2d<D>(sP, ldP, im, ip, st, xn, xt, 5 + s, gy);
+#pragma unroll
+      for (int x = 0; x < 3; ++x) jsum[x] += nrd * gy[x];
+    }
+  }
+  double hsj[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int s = 0; s < NSB; ++s) {
+    if (s < ns) {
+      double gy[3], js[3];
+      face_grad2d<D>(sP, ldP, im, ip, st, xn, xt, 5 + s, gy);
+      const double hs = m.bs[s] + m.cp[s] * Tf;
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        js[x] = nrd * gy[x] - Wf[5 + s] * jsum[x];
+        hsj[x] += hs * js[x];
+      }
+      F[(5 + s) * ldF] += (js[0] * S[0] + js[1] * S[1]) + js[2] * S[2];
+    }
+  }
+  double gT[3];
+  face_grad2d<D>(sP, ldP, im, ip, st, xn, xt, 5 + ns, gT);
+  double qv[3];
+#pragma unroll
+  for (int x = 0; x < 3; ++x) qv[x] = -kc * gT[x] + hsj[x];
+  F[1 * ldF] += -tS[0];
+  F[2 * ldF] += -tS[1];
+  F[3 * ldF] += -tS[2];
+  const double utS = (Wf[1] * tS[0] + Wf[2] * tS[1]) + Wf[3] * tS[2];
+  const double qS = (qv[0] * S[0] + qv[1] * S[1]) + qv[2] * S[2];
+  F[4 * ldF] += -utS + qS;
+  return ok;
+}
+
+// Metric terms of a 2-D face of direction D at global face (gi, gj):
+// xn = S / Vf, xt = face average of the tangential axis' cell-averaged
+// Sc * J (spatial.py:236-248).
+template <int D>
+CSB_DEV void face_metric2d(const GridDev& g, int gi, int gj, const double S[3], double xn[3],
+                           double xt[3], bool& hasm, bool& hasp, long long& cellm,
+                           long long& cellp) {
+  constexpr int A = 1 - D;  // tangential in-plane axis
+  const int nd = D == 0 ? g.ni : g.nj;
+  const int pos = D == 0 ? gi : gj;
+  const int mi = D == 0 ? gi - 1 : gi, mj = D == 0 ? gj : gj - 1;
+  hasm = pos > 0;
+  hasp = pos < nd;
+  cellm = hasm ? cell_index(g, mi, mj, 0) : -1;
+  cellp = hasp ? cell_index(g, gi, gj, 0) : -1;
+  const double Vm = hasm ? __ldg(g.vol + cellm) : 0.0;
+  const double Vp = hasp ? __ldg(g.vol + cellp) : 0.0;
+  const double Vf = (hasm && hasp) ? 0.5 * (Vp + Vm) : (hasm ? Vm : Vp);
+#pragma unroll
+  for (int x = 0; x < 3; ++x) xn[x] = S[x] / Vf;
+  double xc[2][3];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const bool has = side == 0 ? hasm : hasp;
+    if (!has) continue;
+    const int ci = side == 0 ? mi : gi, cj = side == 0 ? mj : gj;
+    double Slo[3], Shi[3];
+    load_S(g, A, face_index(g, A, ci, cj, 0), Slo);
+    load_S(g, A, face_index(g, A, ci + (A == 0), cj + (A == 1), 0), Shi);
+    const double J = 1.0 / (side == 0 ? Vm : Vp);
+#pragma unroll
+    for (int x = 0; x < 3; ++x) xc[side][x] = (0.5 * (Slo[x] + Shi[x])) * J;
+  }
+#pragma unroll
+  for (int x = 0; x < 3; ++x)
+    xt[x] = (hasm && hasp) ? 0.5 * (xc[1][x] + xc[0][x]) : (hasm ? xc[0][x] : xc[1][x]);
+}
+
+template <int NSB, int D>
+CSB_DEV void visc_pass2d(const Model& m, const GridDev& g, const double* sP, int ldP, double* sF,
+                         int maxf, int i0, int j0, int ci, int cj, int BY,
+                         unsigned long long* flags) {
+  const int fx = ci + (D == 0), fy = cj + (D == 1);
+  const int nf = fx * fy;
+  const int sd = D == 0 ? BY : 1, st = D == 0 ? 1 : BY;
+  for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+    const int fj = f % fy, fi = f / fy;
+    const int ip = (fi + NG) * BY + (fj + NG);
+    const int im = ip - sd;
+    const int gi = i0 + fi, gj = j0 + fj;
+    double S[3], xn[3], xt[3];
+    load_S(g, D, face_index(g, D, gi, gj, 0), S);
+    bool hasm, hasp;
+    long long cellm, cellp;
+    face_metric2d<D>(g, gi, gj, S, xn, xt, hasm, hasp, cellm, cellp);
+    if (!face_visc2d<NSB, D>(m, sP, ldP, im, ip, st, S, xn, xt, sF + f, maxf))
+      raise_flag(flags, EB_FACE_T, hasp ? cellp : cellm);
+  }
 }
 
 // Net chemical production of one cell (chemistry.py:46-65).
@@ -408,7 +565,7 @@ CSB_DEV void omega_cell(const Model& m, const Mech& mech, double T, const double
 // ----------------------------------------------------------------------------
 
 template <int NSB, bool K2D>
-__global__ void __launch_bounds__(256) k_residual(const Model* __restrict__ mp, GridDev g, BCDev bc,
+__global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ mp, GridDev g, BCDev bc,
                                                   Mech mech, const double* __restrict__ q,
                                                   double* __restrict__ R, int first_order, int TI,
                                                   int TJ, int TK, unsigned long long* flags) {
@@ -445,33 +602,36 @@ __global__ void __launch_bounds__(256) k_residual(const Model* __restrict__ mp, 
     const int ly = K2D ? l % BY : (l / BZ) % BY;
     const int lx = K2D ? l / BY : l / (BZ * BY);
     const int pi = i0 + lx, pj = j0 + ly, pk = K2D ? NG : k0 + lz;
-    double v[6 + NSB];
     const bool inside_pad = pi < g.ni + 2 * NG && pj < g.nj + 2 * NG && pk < g.nk + 2 * NG;
-    if (!inside_pad) {
-      for (int c = 0; c < nc; ++c) v[c] = 0.0;
-    } else {
-      const bool interior = pi >= NG && pi < g.ni + NG && pj >= NG && pj < g.nj + NG &&
-                            pk >= NG && pk < g.nk + NG;
-      if (interior) {
-        const long long cell = cell_index(g, pi - NG, pj - NG, pk - NG);
-        Cell<NSB> cs;
-        if (!decode<NSB>(m, q + cell, g.N, cs)) raise_flag(flags, EB_DECODE, cell);
-        if (K2D && bc.kind[4] == BC_SYMMETRY && q[cell + 3 * g.N] != 0.0)
-          raise_flag(flags, EB_KSKIP, cell);
-        v[0] = cs.rho;
-        v[1] = cs.u[0];
-        v[2] = cs.u[1];
-        v[3] = cs.u[2];
-        v[4] = cs.p;
+    const bool interior = inside_pad && pi >= NG && pi < g.ni + NG && pj >= NG &&
+                          pj < g.nj + NG && pk >= NG && pk < g.nk + NG;
+    if (interior) {
+      const long long cell = cell_index(g, pi - NG, pj - NG, pk - NG);
+      Cell<NSB> cs;
+      if (!decode<NSB>(m, q + cell, g.N, cs)) raise_flag(flags, EB_DECODE, cell);
+      if (K2D && bc.kind[4] == BC_SYMMETRY && q[cell + 3 * g.N] != 0.0)
+        raise_flag(flags, EB_KSKIP, cell);
+      sP[0 * ldP + l] = cs.rho;
+      sP[1 * ldP + l] = cs.u[0];
+      sP[2 * ldP + l] = cs.u[1];
+      sP[3 * ldP + l] = cs.u[2];
+      sP[4 * ldP + l] = cs.p;
 #pragma unroll
-        for (int s = 0; s < NSB; ++s)
-          if (s < ns) v[5 + s] = cs.Y[s];
-        v[5 + ns] = cs.T;
+      for (int s = 0; s < NSB; ++s)
+        if (s < ns) sP[(5 + s) * ldP + l] = cs.Y[s];
+      sP[(5 + ns) * ldP + l] = cs.T;
+    } else {
+      double v[6 + NSB];
+      if (!inside_pad) {
+#pragma unroll
+        for (int c = 0; c < 6 + NSB; ++c) v[c] = 0.0;
       } else {
         padded_value<NSB>(m, g, bc, q, pi, pj, pk, v, flags);
       }
+#pragma unroll
+      for (int c = 0; c < 6 + NSB; ++c)
+        if (c < nc) sP[c * ldP + l] = v[c];
     }
-    for (int c = 0; c < nc; ++c) sP[c * ldP + l] = v[c];
   }
   __syncthreads();
 
@@ -493,6 +653,31 @@ __global__ void __launch_bounds__(256) k_residual(const Model* __restrict__ mp, 
       const int ip = lidx(lx, ly, lz);
       const int im = ip - sd, imm = ip - 2 * sd, ipp = ip + sd;
       // global face and the two adjacent cells
+      const int gi = i0 + fi, gj = j0 + fj, gk = k0 + fk;
+      double S[3];
+      load_S(g, d, face_index(g, d, gi, gj, gk), S);
+      if (!face_conv<NSB>(m, sP, ldP, imm, im, ip, ipp, S, first_order != 0, sF + f, maxf)) {
+        const int nd = d == 0 ? g.ni : (d == 1 ? g.nj : g.nk);
+        const int pos = d == 0 ? gi : (d == 1 ? gj : gk);
+        int cm[3] = {gi, gj, gk};
+        cm[d] -= 1;
+        raise_flag(flags, EB_FACE_T,
+                   pos < nd ? cell_index(g, gi, gj, gk) : cell_index(g, cm[0], cm[1], cm[2]));
+      }
+    }
+    // viscous pass over the same faces (same thread -> face map: no barrier)
+    if (K2D) {
+      if (d == 0) visc_pass2d<NSB, 0>(m, g, sP, ldP, sF, maxf, i0, j0, ci, cj, BY, flags);
+      else visc_pass2d<NSB, 1>(m, g, sP, ldP, sF, maxf, i0, j0, ci, cj, BY, flags);
+    } else {
+    for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+      const int fk = f % fz;
+      const int fj = (f / fz) % fy;
+      const int fi = f / (fz * fy);
+      int lx = fi + NG, ly = fj + NG, lz = K2D ? 0 : fk + NG;
+      const int sd = d == 0 ? strideX : (d == 1 ? strideY : strideZ);
+      const int ip = lidx(lx, ly, lz);
+      const int im = ip - sd;
       const int gi = i0 + fi, gj = j0 + fj, gk = k0 + fk;
       FaceGeom fg;
       const long long fidx = face_index(g, d, gi, gj, gk);
@@ -537,8 +722,9 @@ __global__ void __launch_bounds__(256) k_residual(const Model* __restrict__ mp, 
         }
         ++t;
       }
-      if (!face_flux<NSB>(m, sP, ldP, imm, im, ip, ipp, st, fg, first_order != 0, sF + f, maxf))
+      if (!face_visc<NSB>(m, sP, ldP, im, ip, st, fg, sF + f, maxf))
         raise_flag(flags, EB_FACE_T, hasp ? cellp : cellm);
+    }
     }
     __syncthreads();
     // difference into R (R = 0 + dR_0 + dR_1 + dR_2, spatial.py:258-259)
