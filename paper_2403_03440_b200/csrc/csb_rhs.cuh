@@ -14,6 +14,9 @@
 // staged nor evaluated.  Any cell with w != 0 under symmetry raises
 // EB_KSKIP so the host can recompute with the general path.
 #pragma once
+#include <cstdio>
+#include <cstdlib>
+
 #include "csb_common.cuh"
 #include "csb_kernels.cuh"
 
@@ -807,7 +810,8 @@ static inline void pick_tile(int ns, bool k2d, int nk, int& TI, int& TJ, int& TK
   const int nc = 6 + ns, nv = 5 + ns;
   const size_t budget = 200 * 1024;
   if (k2d) {
-    const int cand[][2] = {{15, 16}, {7, 16}, {7, 8}, {3, 8}, {3, 4}, {1, 4}};
+    int cand[][2] = {{15, 16}, {7, 16}, {7, 8}, {3, 8}, {3, 4}, {1, 4}};
+    if (const char* e = getenv("CSB_RHS_TILE")) sscanf(e, "%d,%d", &cand[0][0], &cand[0][1]);
     for (auto& c : cand) {
       TI = c[0];
       TJ = c[1];

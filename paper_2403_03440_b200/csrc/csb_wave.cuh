@@ -573,7 +573,14 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   __shared__ int s_strip, consumed, recv_cnt;
   __shared__ unsigned long long t_first;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kind = a.only >= 0 ? a.only : (blockIdx.x & 1);  // 0 flow, 1 species
+  if ((a.only == 2 || a.only == 3) && (blockIdx.x & 1) != a.only - 2) return;  // probe: idle partner
+  if (a.only == 4 && (blockIdx.x & 1)) return;  // probe: one idle CTA between working ones
+  // role: 0 flow, 1 species.  Block pairs share a role: the two SMs of a TPC
+  // run the same code (measured: a flow and a species CTA side by side on a
+  // TPC slow the flow chain by ~14%)
+  const int kind = (a.only == 0 || a.only == 1) ? a.only
+                   : a.only == 5                ? (blockIdx.x & 1)
+                                                : ((blockIdx.x >> 1) & 1);
   const WaveRole ro = kind ? a.role[1] : a.role[0];
   const int WK = kind ? wave_wks<NSB>() : WKF;
   const int nh = kind ? NSB : 5;
@@ -583,7 +590,7 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   double* hin = ring + D * slot;          // [HRING][nh]
   if (threadIdx.x == 0) {
     const int tk = atomicAdd(ro.ticket, 1);
-    s_strip = BWD ? a.sk.nstrip - 1 - tk : tk;
+    s_strip = tk >= a.sk.nstrip ? -1 : (BWD ? a.sk.nstrip - 1 - tk : tk);
     for (int b = 0; b < D; ++b) {
       mbar_init(&full_bar[b], 1);
       mbar_init(&empty_bar[b], 1);
@@ -594,6 +601,7 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (s_strip < 0) return;  // surplus CTA of the role-pair layout
   ChainCtx x;
   x.a = &a;
   x.s = s_strip;
@@ -637,25 +645,44 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
 
   if (warp == 2) {
     // ---------------------------------------------------- receiver
-    // lane l polls column next + l of the upstream strip; the complete prefix
-    // of columns is copied into hin (bounded by what the chain consumed)
+    // lane l polls column next + l of the upstream strip (its nh words, one
+    // L2 round trip); the complete prefix of columns goes from registers into
+    // hin, bounded by what the chain has consumed.
     if (!x.has_up) return;
+    constexpr int CAP = (NSB > 5 ? NSB : 5) < 16 ? (NSB > 5 ? NSB : 5) : 16;
     const int ni = a.ni;
     const double* src = ro.hand + (long long)up * ni * nh;
     int next = 0;
     while (next < ni) {
       const int lim = min(ni, ld_volatile_s(&consumed) + HRING);
       const int q = next + lane;
-      bool ok = q < lim;
-      if (ok)
-        for (int c = 0; c < nh; ++c) ok &= ld_relaxed_u64(src + (long long)q * nh + c) != HAND_SENTINEL;
+      const bool in = q < lim;
+      unsigned long long w[CAP];
+      bool ok = in;
+#pragma unroll
+      for (int c = 0; c < CAP; ++c) {
+        w[c] = 0;
+        if (in && c < nh) {
+          w[c] = (unsigned long long)__ldcg(reinterpret_cast<const long long*>(src) +
+                                            (long long)q * nh + c);
+          ok &= w[c] != HAND_SENTINEL;
+        }
+      }
+      for (int c = CAP; c < nh; ++c)
+        if (in)
+          ok &= (unsigned long long)__ldcg(reinterpret_cast<const long long*>(src) +
+                                           (long long)q * nh + c) != HAND_SENTINEL;
       const unsigned bal = __ballot_sync(0xffffffffu, ok);
-      const int n = __ffs(~bal) ? __ffs(~bal) - 1 : 32;  // complete prefix length
+      const int n = (~bal) ? __ffs(~bal) - 1 : 32;  // complete prefix length
       if (n > 0) {
-        if (lane < n)
-          for (int c = 0; c < nh; ++c)
+        if (lane < n) {
+#pragma unroll
+          for (int c = 0; c < CAP; ++c)
+            if (c < nh) hin[(q % HRING) * nh + c] = __longlong_as_double((long long)w[c]);
+          for (int c = CAP; c < nh; ++c)
             hin[(q % HRING) * nh + c] = __longlong_as_double(
-                (long long)ld_relaxed_u64(src + (long long)q * nh + c));
+                __ldcg(reinterpret_cast<const long long*>(src) + (long long)q * nh + c));
+        }
         __syncwarp();
         if (lane == 0) {
           __threadfence_block();
@@ -880,7 +907,10 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
                      : (per_species ? k_wave2d<NSB, false, true> : k_wave2d<NSB, false, false>);
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       cudaMemsetAsync(wb.prog, 0, sizeof(int) * 2, st);
-      kfn<<<(wa.only >= 0 ? 1 : 2) * sk.nstrip, 96, smem, st>>>(wa);
+      const int nblk = wa.only == 0 || wa.only == 1 ? sk.nstrip
+                       : wa.only == 4               ? 4 * sk.nstrip
+                                                    : (2 * sk.nstrip + 3) / 4 * 4;
+      kfn<<<nblk, 96, smem, st>>>(wa);
       if (wa.dbg) {
         std::vector<unsigned long long> h(4 * 2 * sk.nstrip);
         cudaMemcpyAsync(h.data(), wa.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
