@@ -371,6 +371,7 @@ struct ChainCtx {
   const WaveArgs* a;
   int s, nslots, D, rt;
   bool has_up, has_down, first, last;
+  double mul;           // 0 on the first row (takes the hand-off), 1 elsewhere
   const double* ring;
   const double* hin;
   double* hand_out;     // this strip's row of the hand-off buffer
@@ -449,11 +450,15 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
         const double* p = base + kk * NG * 32;
         const int qn = BWD ? a.ni - 1 - t + x.rt : t;
         const bool hin_ok = x.first && x.has_up && qn >= 0 && qn < a.ni;
+        // the first row takes the upstream hand-off (or zero) instead of the
+        // shuffled value: ij = sh * mul + hv with mul = 0 and hv the hand-off
+        // there, mul = 1 and hv = +0 (a zero row of hin) elsewhere
+        const double* hv = x.hin + (hin_ok ? (qn % HRING) * 5 : HRING * 5);
         double ij[5];
 #pragma unroll
         for (int c = 0; c < 5; ++c) {
           const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
-          ij[c] = x.first ? (hin_ok ? x.hin[(qn % HRING) * 5 + c] : 0.0) : sh;
+          ij[c] = fma(sh, x.mul, hv[c]);
         }
         const double invd = p[0];
         double dq[5];
@@ -535,11 +540,12 @@ CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro) {
         const double* p = base + kk * NG * 32;
         const int qn = BWD ? a.ni - 1 - t + x.rt : t;
         const bool hin_ok = x.first && x.has_up && qn >= 0 && qn < a.ni;
+        const double* hv = x.hin + (hin_ok ? (qn % HRING) * NSB : HRING * NSB);
         double ij[NSB];
 #pragma unroll
         for (int c = 0; c < NSB; ++c) {
           const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
-          ij[c] = x.first ? (hin_ok ? x.hin[(qn % HRING) * NSB + c] : 0.0) : sh;
+          ij[c] = fma(sh, x.mul, hv[c]);
         }
         const double ci = p[PC * 32], cj = p[(PC + 1) * 32];
 #pragma unroll
@@ -587,7 +593,7 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   const int D = ro.D, NG = ro.ng;
   const long long slot = (long long)WK * NG * 32;
   double* ring = wsm;                     // [D][WK][NG][32]
-  double* hin = ring + D * slot;          // [HRING][nh]
+  double* hin = ring + D * slot;          // [HRING + 1][nh], row HRING = zeros
   if (threadIdx.x == 0) {
     const int tk = atomicAdd(ro.ticket, 1);
     s_strip = tk >= a.sk.nstrip ? -1 : (BWD ? a.sk.nstrip - 1 - tk : tk);
@@ -597,6 +603,7 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
     }
     consumed = 0;
     recv_cnt = 0;
+    for (int c = 0; c < nh; ++c) hin[HRING * nh + c] = 0.0;
     t_first = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -613,6 +620,7 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   x.has_down = BWD ? (x.s > 0) : (x.s + 1 < a.sk.nstrip);
   x.first = BWD ? (lane == x.rt) : (lane == 0);  // receives the upstream hand-off
   x.last = BWD ? (lane == 0) : (lane == x.rt);   // sends the downstream hand-off
+  x.mul = x.first ? 0.0 : 1.0;
   x.ring = ring;
   x.hin = hin;
   x.hand_out = ro.hand + (long long)x.s * a.ni * nh;
@@ -829,7 +837,7 @@ __global__ void __launch_bounds__(256) k_epilogue2d(const Model* __restrict__ mp
 
 // ============================================================== launcher
 inline size_t wave_role_smem(int D, int WK, int NG, int nh) {
-  return ((size_t)D * WK * NG * 32 + (size_t)HRING * nh) * sizeof(double);
+  return ((size_t)D * WK * NG * 32 + (size_t)(HRING + 1) * nh) * sizeof(double);
 }
 // deepest ring (2..4) that fits the shared-memory budget, 0 if none
 inline int wave_depth(int WK, int NG, int nh) {
