@@ -327,6 +327,21 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- replicas
+def replica_aggregate(local_ms, cells_per_rank, steps, dist=None, device="cpu"):
+    """Whole-job throughput of N independent replicas: the timed region's
+    device time is the MAX over ranks, value = cells all ranks processed /
+    that time.  Returns (value, max_ms).  Works with any torch.distributed
+    backend (nccl on the GPU box, gloo in the CPU tests)."""
+    import torch
+    world = dist.get_world_size() if dist is not None else 1
+    t = torch.tensor([float(local_ms)], device=device, dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    return world * cells_per_rank * steps / (max_ms * 1e-3), max_ms
+
+
 # ---------------------------------------------------------------- main
 def main():
     args = parse()
@@ -362,14 +377,10 @@ def main():
     if dist:
         dist.barrier()
     clk = clocks.stop()
-    t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
     fl, cell, gate = run.eng.status()
     N = run.eng.N
     nv = run.eng.nv
-    value = world * N * args.steps / (total_ms * 1e-3)
+    value, total_ms = replica_aggregate(total_ms, N, args.steps, dist, device="cuda")
 
     extras = {}
     if not args.no_extras:
