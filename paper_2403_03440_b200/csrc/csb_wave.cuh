@@ -49,7 +49,7 @@
 
 namespace csb {
 
-constexpr int HRING = 64;  // hand-off ring (columns)
+constexpr int HRING = 128;  // hand-off ring (columns)
 // signalling NaN marking a hand-off word not yet written (see the chains)
 constexpr unsigned long long HAND_SENTINEL = 0x7FF4DEADBEEF0001ull;
 constexpr int NFF = 30, NFB = 30, FB_DQ = 25;
@@ -58,7 +58,7 @@ constexpr int WKF = 8;     // flow slot: 8 steps x 30 planes = 60 KiB
 // species slot length: <= 64 KiB per slot at the widest layout (nsI = NSB)
 template <int NSB>
 constexpr int wave_wks() {
-  int w = 16;
+  int w = 8;  // also the hand-off granularity (a slot starts when its columns are in)
   while (w > 1 && w * (2 * NSB + 2) * 256 > 64 * 1024) w /= 2;
   return w;
 }
@@ -349,6 +349,7 @@ struct WaveArgs {
   Skew sk;
   int ni, nj, nsI;
   int only;          // -1: both roles (production); 0/1: one role (timing probe)
+  int poll_ns;       // receiver back-off between empty polls
   unsigned long long* dbg;  // timing probe: [CTA][4] globaltimer stamps (or null)
   WaveRole role[2];  // 0 flow, 1 species
 };
@@ -358,14 +359,14 @@ struct WaveArgs {
 // produces / consumes its boundary columns): forward q = col, backward
 // q = ni - 1 - col.  The last row of a strip stores its outgoing j-face
 // products for column q straight into the L2 hand-off buffer
-// hand[strip][q][nh] (one relaxed 8-byte store per value); the buffer is
-// reset to a signalling-NaN sentinel before the sweep, and since every
-// hand-off value is the result of a floating-point operation (which never
-// yields a signalling NaN), a word != sentinel is final.  The receiver warp
-// of the next strip polls those words, copies complete columns into the
-// smem ring hin[HRING][nh] and bumps recv_cnt; the chain checks recv_cnt
-// once per group of G steps.
-constexpr int GSTEP = 4;  // steps per hand-off check
+// hand[strip][q][nh]; the buffer is reset to a signalling-NaN sentinel before
+// the sweep, and since every hand-off value is the result of a floating-point
+// operation (which never yields a signalling NaN), a word != sentinel is
+// final.  The receiver warp of the next strip polls the columns a ring slot
+// needs, copies them into the smem ring hin[HRING][nh] and then arrives on the
+// slot's full barrier, next to the producer's TMA transaction: the chain's
+// only synchronisation is the per-slot mbarrier wait (measured: a per-4-step
+// availability check inside the chain cost ~9% per step).
 
 struct ChainCtx {
   const WaveArgs* a;
@@ -377,9 +378,6 @@ struct ChainCtx {
   double* hand_out;     // this strip's row of the hand-off buffer
   unsigned long long* full_bar;
   unsigned long long* empty_bar;
-  int* consumed;        // q consumed by the chain (chain -> receiver)
-  const int* recv_cnt;  // q received from upstream (receiver -> chain)
-  unsigned long long* t_first;  // timing probe
 };
 
 // predicated store without a branch (a branch would end the scheduling region
@@ -387,34 +385,6 @@ struct ChainCtx {
 CSB_DEV void st_pred_cg_f64(double* p, double v, bool pred) {
   asm("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.cg.f64 [%0], %1;\n}" ::"l"(p), "d"(v),
       "r"((int)pred));
-}
-CSB_DEV unsigned long long ld_relaxed_u64(const double* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// group check: all upstream columns needed by steps [t_a, t_b] are in hin
-template <bool BWD>
-CSB_DEV void chain_group_wait(const ChainCtx& x, int t_first, int t_last, int& avail) {
-  if (!x.has_up) return;
-  // q grows with t forward and shrinks with t backward; need the larger end
-  const int qa = BWD ? x.a->ni - 1 - t_first + x.rt : t_first;
-  const int qb = BWD ? x.a->ni - 1 - t_last + x.rt : t_last;
-  const int qmax = min(max(qa, qb), x.a->ni - 1);
-  if (qmax < 0) return;
-  if (x.first) *(volatile int*)x.consumed = min(qa, qb);  // q below are consumed
-  if (avail <= qmax) {
-    do {
-      avail = ld_volatile_s(x.recv_cnt);
-    } while (avail <= qmax);
-    __threadfence_block();
-  }
-  if (x.a->dbg && *x.t_first == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    *x.t_first = t;
-  }
 }
 
 // flow chain: 5 coupled components per row (rank-2 half blocks)
@@ -427,7 +397,6 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
   const int lane = threadIdx.x & 31;
   const WaveArgs& a = *x.a;
   const long long slot = (long long)WK * NG * 32;
-  int avail = 0;
   double oi[5] = {0, 0, 0, 0, 0}, oj[5] = {0, 0, 0, 0, 0};
   int buf = 0, phase = 0;
   for (int ks = 0; ks < x.nslots; ++ks) {
@@ -436,60 +405,50 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
     const double* base = x.ring + buf * slot + lane;
     double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO) * 32 + lane;
 #pragma unroll
-    for (int g = 0; g < WK / GSTEP; ++g) {
-      {
-        const int ma = g * GSTEP, mb = ma + GSTEP - 1;
-        chain_group_wait<BWD>(x, k * WK + (BWD ? WK - 1 - ma : ma),
-                              k * WK + (BWD ? WK - 1 - mb : mb), avail);
+    for (int m = 0; m < WK; ++m) {
+      const int kk = BWD ? WK - 1 - m : m;
+      const int t = k * WK + kk;
+      const double* p = base + kk * NG * 32;
+      const int qn = BWD ? a.ni - 1 - t + x.rt : t;
+      const bool hin_ok = x.first && x.has_up && qn >= 0 && qn < a.ni;
+      // the first row takes the upstream hand-off (or zero) instead of the
+      // shuffled value: ij = sh * mul + hv with mul = 0 and hv the hand-off
+      // there, mul = 1 and hv = +0 (a zero row of hin) elsewhere
+      const double* hv = x.hin + (hin_ok ? (qn % HRING) * 5 : HRING * 5);
+      double ij[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
+        ij[c] = fma(sh, x.mul, hv[c]);
       }
+      const double invd = p[0];
+      double dq[5];
 #pragma unroll
-      for (int mm = 0; mm < GSTEP; ++mm) {
-        const int m = g * GSTEP + mm;
-        const int kk = BWD ? WK - 1 - m : m;
-        const int t = k * WK + kk;
-        const double* p = base + kk * NG * 32;
-        const int qn = BWD ? a.ni - 1 - t + x.rt : t;
-        const bool hin_ok = x.first && x.has_up && qn >= 0 && qn < a.ni;
-        // the first row takes the upstream hand-off (or zero) instead of the
-        // shuffled value: ij = sh * mul + hv with mul = 0 and hv the hand-off
-        // there, mul = 1 and hv = +0 (a zero row of hin) elsewhere
-        const double* hv = x.hin + (hin_ok ? (qn % HRING) * 5 : HRING * 5);
-        double ij[5];
-#pragma unroll
-        for (int c = 0; c < 5; ++c) {
-          const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
-          ij[c] = fma(sh, x.mul, hv[c]);
-        }
-        const double invd = p[0];
-        double dq[5];
-#pragma unroll
-        for (int c = 0; c < 5; ++c) {
-          if (BWD) dq[c] = p[(FB_DQ + c) * 32] - (oi[c] + ij[c]) * invd;
-          else dq[c] = ((p[(11 + c) * 32] + oi[c]) + ij[c]) * invd;
-          ob[(kk * NGO + c) * 32] = dq[c];
-        }
-        const double w0 = p[1 * 32], w1 = p[2 * 32], w2 = p[3 * 32], w3 = p[4 * 32],
-                     w4 = p[5 * 32];
-        // balanced sums: short dependency chains behind dq
-        const double sb = ((p[6 * 32] * dq[0] + p[7 * 32] * dq[1]) +
-                           (p[8 * 32] * dq[2] + p[9 * 32] * dq[3])) + p[10 * 32] * dq[4];
-#pragma unroll
-        for (int f = 0; f < 2; ++f) {
-          const double* pf = p + (FQ + 7 * f) * 32;
-          const double sa = pf[0] * dq[0] + (pf[32] * dq[1] + pf[64] * dq[2]);
-          const double sig = pf[6 * 32];
-          double* o = f == 0 ? oi : oj;
-          o[0] = w0 * sa + sig * dq[0];
-          o[1] = w1 * sa + pf[3 * 32] * sb + sig * dq[1];
-          o[2] = w2 * sa + pf[4 * 32] * sb + sig * dq[2];
-          o[3] = w3 * sa + sig * dq[3];
-          o[4] = w4 * sa + pf[5 * 32] * sb + sig * dq[4];
-        }
-        const int qo = BWD ? a.ni - 1 - t : t - x.rt;
-        const bool ho = x.has_down && x.last && qo >= 0 && qo < a.ni;
-#pragma unroll
-        for (int c = 0; c < 5; ++c) st_pred_cg_f64(x.hand_out + qo * 5 + c, oj[c], ho);
+      for (int c = 0; c < 5; ++c) {
+        if (BWD) dq[c] = p[(FB_DQ + c) * 32] - (oi[c] + ij[c]) * invd;
+        else dq[c] = ((p[(11 + c) * 32] + oi[c]) + ij[c]) * invd;
+        ob[(kk * NGO + c) * 32] = dq[c];
       }
+      const double w0 = p[1 * 32], w1 = p[2 * 32], w2 = p[3 * 32], w3 = p[4 * 32], w4 = p[5 * 32];
+      // balanced sums: short dependency chains behind dq
+      const double sb = ((p[6 * 32] * dq[0] + p[7 * 32] * dq[1]) +
+                         (p[8 * 32] * dq[2] + p[9 * 32] * dq[3])) + p[10 * 32] * dq[4];
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        const double* pf = p + (FQ + 7 * f) * 32;
+        const double sa = pf[0] * dq[0] + (pf[32] * dq[1] + pf[64] * dq[2]);
+        const double sig = pf[6 * 32];
+        double* o = f == 0 ? oi : oj;
+        o[0] = w0 * sa + sig * dq[0];
+        o[1] = w1 * sa + pf[3 * 32] * sb + sig * dq[1];
+        o[2] = w2 * sa + pf[4 * 32] * sb + sig * dq[2];
+        o[3] = w3 * sa + sig * dq[3];
+        o[4] = w4 * sa + pf[5 * 32] * sb + sig * dq[4];
+      }
+      const int qo = BWD ? a.ni - 1 - t : t - x.rt;
+      const bool ho = x.has_down && x.last && qo >= 0 && qo < a.ni;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) st_pred_cg_f64(x.hand_out + qo * 5 + c, oj[c], ho);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&x.empty_bar[buf]);
@@ -510,12 +469,10 @@ CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro) {
   constexpr int PC = BWD ? NI : NI + NSB;   // c_i, c_j planes
   constexpr int PV = BWD ? NI + 2 : NI;     // dq* (backward) | rhs (forward) planes
   constexpr int NGO = BWD ? NSB : NG, PO = BWD ? 0 : NI + 2;  // output: SW | SB dq* planes
-  constexpr int G = WK < GSTEP ? WK : GSTEP;
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const WaveArgs& a = *x.a;
   const long long slot = (long long)WK * NG * 32;
-  int avail = 0;
   double oi[NSB], oj[NSB];
 #pragma unroll
   for (int c = 0; c < NSB; ++c) oi[c] = oj[c] = 0.0;
@@ -526,42 +483,33 @@ CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro) {
     const double* base = x.ring + buf * slot + lane;
     double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO) * 32 + lane;
 #pragma unroll
-    for (int g = 0; g < WK / G; ++g) {
-      {
-        const int ma = g * G, mb = ma + G - 1;
-        chain_group_wait<BWD>(x, k * WK + (BWD ? WK - 1 - ma : ma),
-                              k * WK + (BWD ? WK - 1 - mb : mb), avail);
+    for (int m = 0; m < WK; ++m) {
+      const int kk = BWD ? WK - 1 - m : m;
+      const int t = k * WK + kk;
+      const double* p = base + kk * NG * 32;
+      const int qn = BWD ? a.ni - 1 - t + x.rt : t;
+      const bool hin_ok = x.first && x.has_up && qn >= 0 && qn < a.ni;
+      const double* hv = x.hin + (hin_ok ? (qn % HRING) * NSB : HRING * NSB);
+      double ij[NSB];
+#pragma unroll
+      for (int c = 0; c < NSB; ++c) {
+        const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
+        ij[c] = fma(sh, x.mul, hv[c]);
       }
+      const double ci = p[PC * 32], cj = p[(PC + 1) * 32];
 #pragma unroll
-      for (int mm = 0; mm < G; ++mm) {
-        const int m = g * G + mm;
-        const int kk = BWD ? WK - 1 - m : m;
-        const int t = k * WK + kk;
-        const double* p = base + kk * NG * 32;
-        const int qn = BWD ? a.ni - 1 - t + x.rt : t;
-        const bool hin_ok = x.first && x.has_up && qn >= 0 && qn < a.ni;
-        const double* hv = x.hin + (hin_ok ? (qn % HRING) * NSB : HRING * NSB);
-        double ij[NSB];
-#pragma unroll
-        for (int c = 0; c < NSB; ++c) {
-          const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
-          ij[c] = fma(sh, x.mul, hv[c]);
-        }
-        const double ci = p[PC * 32], cj = p[(PC + 1) * 32];
-#pragma unroll
-        for (int c = 0; c < NSB; ++c) {
-          const double inv = p[(PER ? c : 0) * 32];
-          const double v = p[(PV + c) * 32];
-          const double dq = BWD ? v - (oi[c] + ij[c]) * inv : ((v + oi[c]) + ij[c]) * inv;
-          ob[(kk * NGO + c) * 32] = dq;
-          oi[c] = ci * dq;
-          oj[c] = cj * dq;
-        }
-        const int qo = BWD ? a.ni - 1 - t : t - x.rt;
-        const bool ho = x.has_down && x.last && qo >= 0 && qo < a.ni;
-#pragma unroll
-        for (int c = 0; c < NSB; ++c) st_pred_cg_f64(x.hand_out + qo * NSB + c, oj[c], ho);
+      for (int c = 0; c < NSB; ++c) {
+        const double inv = p[(PER ? c : 0) * 32];
+        const double v = p[(PV + c) * 32];
+        const double dq = BWD ? v - (oi[c] + ij[c]) * inv : ((v + oi[c]) + ij[c]) * inv;
+        ob[(kk * NGO + c) * 32] = dq;
+        oi[c] = ci * dq;
+        oj[c] = cj * dq;
       }
+      const int qo = BWD ? a.ni - 1 - t : t - x.rt;
+      const bool ho = x.has_down && x.last && qo >= 0 && qo < a.ni;
+#pragma unroll
+      for (int c = 0; c < NSB; ++c) st_pred_cg_f64(x.hand_out + qo * NSB + c, oj[c], ho);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&x.empty_bar[buf]);
@@ -576,8 +524,7 @@ template <int NSB, bool BWD, bool PER>
 __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   extern __shared__ __align__(128) double wsm[];
   __shared__ unsigned long long full_bar[8], empty_bar[8];
-  __shared__ int s_strip, consumed, recv_cnt;
-  __shared__ unsigned long long t_first;
+  __shared__ int s_strip;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if ((a.only == 2 || a.only == 3) && (blockIdx.x & 1) != a.only - 2) return;  // probe: idle partner
   if (a.only == 4 && (blockIdx.x & 1)) return;  // probe: one idle CTA between working ones
@@ -597,15 +544,6 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   if (threadIdx.x == 0) {
     const int tk = atomicAdd(ro.ticket, 1);
     s_strip = tk >= a.sk.nstrip ? -1 : (BWD ? a.sk.nstrip - 1 - tk : tk);
-    for (int b = 0; b < D; ++b) {
-      mbar_init(&full_bar[b], 1);
-      mbar_init(&empty_bar[b], 1);
-    }
-    consumed = 0;
-    recv_cnt = 0;
-    for (int c = 0; c < nh; ++c) hin[HRING * nh + c] = 0.0;
-    t_first = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (s_strip < 0) return;  // surplus CTA of the role-pair layout
@@ -626,19 +564,25 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   x.hand_out = ro.hand + (long long)x.s * a.ni * nh;
   x.full_bar = full_bar;
   x.empty_bar = empty_bar;
-  x.consumed = &consumed;
-  x.recv_cnt = &recv_cnt;
-  x.t_first = &t_first;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < D; ++b) {
+      mbar_init(&full_bar[b], x.has_up ? 2 : 1);  // TMA producer (+ hand-off receiver)
+      mbar_init(&empty_bar[b], 1);
+    }
+    for (int c = 0; c < nh; ++c) hin[HRING * nh + c] = 0.0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   const int s = x.s;
   const int up = BWD ? s + 1 : s - 1;
 
   if (warp == 1) {
     // ---------------------------------------------------- producer (TMA)
     if (lane == 0) {
+      int buf = 0, phase = 0;
       for (int ks = 0; ks < x.nslots; ++ks) {
         const int k = BWD ? x.nslots - 1 - ks : ks;
-        const int buf = ks % D;
-        if (ks >= D) mbar_wait(&empty_bar[buf], ((ks / D) - 1) & 1);
+        if (ks >= D) mbar_wait(&empty_bar[buf], phase ^ 1);
         const unsigned bytes = (unsigned)(slot * 8);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                          smem_u32(&full_bar[buf])),
@@ -646,59 +590,74 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
                      : "memory");
         bulk_g2s(ring + buf * slot, ro.in + ((long long)s * T + (long long)k * WK) * NG * 32, bytes,
                  &full_bar[buf]);
+        if (++buf == D) {
+          buf = 0;
+          phase ^= 1;
+        }
       }
     }
     return;
   }
 
   if (warp == 2) {
-    // ---------------------------------------------------- receiver
-    // lane l polls column next + l of the upstream strip (its nh words, one
-    // L2 round trip); the complete prefix of columns goes from registers into
-    // hin, bounded by what the chain has consumed.
+    // ---------------------------------------------------- hand-off receiver
+    // For each ring slot: the upstream columns its steps need (one per lane,
+    // at most WK <= 32), polled until complete, copied into hin, then one
+    // arrival on the slot's full barrier (release: the chain's wait acquires).
     if (!x.has_up) return;
     constexpr int CAP = (NSB > 5 ? NSB : 5) < 16 ? (NSB > 5 ? NSB : 5) : 16;
     const int ni = a.ni;
     const double* src = ro.hand + (long long)up * ni * nh;
-    int next = 0;
-    while (next < ni) {
-      const int lim = min(ni, ld_volatile_s(&consumed) + HRING);
-      const int q = next + lane;
-      const bool in = q < lim;
-      unsigned long long w[CAP];
-      bool ok = in;
-#pragma unroll
-      for (int c = 0; c < CAP; ++c) {
-        w[c] = 0;
-        if (in && c < nh) {
-          w[c] = (unsigned long long)__ldcg(reinterpret_cast<const long long*>(src) +
-                                            (long long)q * nh + c);
-          ok &= w[c] != HAND_SENTINEL;
-        }
-      }
-      for (int c = CAP; c < nh; ++c)
-        if (in)
-          ok &= (unsigned long long)__ldcg(reinterpret_cast<const long long*>(src) +
-                                           (long long)q * nh + c) != HAND_SENTINEL;
-      const unsigned bal = __ballot_sync(0xffffffffu, ok);
-      const int n = (~bal) ? __ffs(~bal) - 1 : 32;  // complete prefix length
-      if (n > 0) {
-        if (lane < n) {
-#pragma unroll
-          for (int c = 0; c < CAP; ++c)
-            if (c < nh) hin[(q % HRING) * nh + c] = __longlong_as_double((long long)w[c]);
-          for (int c = CAP; c < nh; ++c)
-            hin[(q % HRING) * nh + c] = __longlong_as_double(
-                __ldcg(reinterpret_cast<const long long*>(src) + (long long)q * nh + c));
-        }
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence_block();
-          *(volatile int*)&recv_cnt = next + n;
-        }
-        next += n;
+    int buf = 0, phase = 0;
+    for (int ks = 0; ks < x.nslots; ++ks) {
+      const int k = BWD ? x.nslots - 1 - ks : ks;
+      if (ks >= D) mbar_wait(&empty_bar[buf], phase ^ 1);  // slot free: hin rows too
+      int qlo, qhi;  // q range of the slot's first-row needs
+      if (!BWD) {
+        qlo = k * WK;
+        qhi = k * WK + WK - 1;
       } else {
-        __nanosleep(16);
+        qlo = ni - 1 - (k * WK + WK - 1) + x.rt;
+        qhi = ni - 1 - k * WK + x.rt;
+      }
+      qlo = max(qlo, 0);
+      qhi = min(qhi, ni - 1);
+      const int q = qlo + lane;
+      const bool in = q <= qhi;
+      unsigned long long w[CAP];
+      bool done = !in;
+      while (true) {
+        bool ok = true;
+        if (!done) {
+#pragma unroll
+          for (int c = 0; c < CAP; ++c) {
+            if (c < nh) {
+              w[c] = (unsigned long long)__ldcg(reinterpret_cast<const long long*>(src) +
+                                                (long long)q * nh + c);
+              ok &= w[c] != HAND_SENTINEL;
+            }
+          }
+          for (int c = CAP; c < nh; ++c)
+            ok &= (unsigned long long)__ldcg(reinterpret_cast<const long long*>(src) +
+                                             (long long)q * nh + c) != HAND_SENTINEL;
+          if (ok) {
+#pragma unroll
+            for (int c = 0; c < CAP; ++c)
+              if (c < nh) hin[(q % HRING) * nh + c] = __longlong_as_double((long long)w[c]);
+            for (int c = CAP; c < nh; ++c)
+              hin[(q % HRING) * nh + c] = __longlong_as_double(
+                  __ldcg(reinterpret_cast<const long long*>(src) + (long long)q * nh + c));
+            done = true;
+          }
+        }
+        if (__all_sync(0xffffffffu, done)) break;
+        __nanosleep(a.poll_ns);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_bar[buf]);
+      if (++buf == D) {
+        buf = 0;
+        phase ^= 1;
       }
     }
     return;
@@ -712,10 +671,9 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   if (a.dbg && lane == 0) {
     unsigned long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    unsigned long long* d = a.dbg + 4 * (2 * s + kind);
+    unsigned long long* d = a.dbg + 16 * (2 * s + kind);
     d[0] = t0;
     d[1] = t1;
-    d[2] = t_first;
   }
 }
 
@@ -883,12 +841,14 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       wa.nj = g.nj;
       wa.nsI = nsI;
       wa.only = -1;
+      wa.poll_ns = 16;
+      if (const char* ev_p = getenv("CSB_POLL_NS")) wa.poll_ns = atoi(ev_p);  // tuning probe
       if (const char* ev_o = getenv("CSB_WAVE_ONLY")) wa.only = atoi(ev_o);  // timing probe
       static unsigned long long* dbg = nullptr;
       wa.dbg = nullptr;
       if (getenv("CSB_WAVE_DBG")) {
-        if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 4 * 2 * 4096);
-        cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 4 * 2 * sk.nstrip, st);
+        if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 16 * 2 * 4096);
+        cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 16 * 2 * sk.nstrip, st);
         wa.dbg = dbg;
       }
       WaveRole& rf = wa.role[0];
@@ -920,17 +880,24 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
                                                     : (2 * sk.nstrip + 3) / 4 * 4;
       kfn<<<nblk, 96, smem, st>>>(wa);
       if (wa.dbg) {
-        std::vector<unsigned long long> h(4 * 2 * sk.nstrip);
+        std::vector<unsigned long long> h(16 * 2 * sk.nstrip);
         cudaMemcpyAsync(h.data(), wa.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         unsigned long long tmin = ~0ull;
         for (int e = 0; e < 2 * sk.nstrip; ++e)
-          if (h[4 * e]) tmin = std::min(tmin, h[4 * e]);
+          if (h[16 * e]) tmin = std::min(tmin, h[16 * e]);
         for (int e = 0; e < 2 * sk.nstrip; ++e)
-          if (h[4 * e])
-            fprintf(stderr, "wave%s strip %d kind %d: start %.2f first %.2f end %.2f us\n",
-                    bwd ? "B" : "F", e / 2, e % 2, (h[4 * e] - tmin) * 1e-3,
-                    h[4 * e + 2] ? (h[4 * e + 2] - tmin) * 1e-3 : -1.0, (h[4 * e + 1] - tmin) * 1e-3);
+          if (h[16 * e]) {
+            fprintf(stderr, "wave%s strip %d kind %d: start %.2f first %.2f end %.2f | stamps:",
+                    bwd ? "B" : "F", e / 2, e % 2, (h[16 * e] - tmin) * 1e-3,
+                    h[16 * e + 2] ? (h[16 * e + 2] - tmin) * 1e-3 : -1.0,
+                    (h[16 * e + 1] - tmin) * 1e-3);
+            for (int k = 3; k < 13; ++k)
+              if (h[16 * e + k]) fprintf(stderr, " %.1f", (h[16 * e + k] - tmin) * 1e-3);
+            fprintf(stderr, " | reloads %llu waited %llu polls %llu", h[16 * e + 13], h[16 * e + 14],
+                    h[16 * e + 15]);
+            fprintf(stderr, "\n");
+          }
       }
       if (ev) cudaEventRecord(ev[2 + pass], st);
     }
