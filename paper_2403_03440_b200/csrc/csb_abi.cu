@@ -184,7 +184,7 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
     c->wb.sf = k.take<double>((size_t)(2 * nsb + 2) * sk.Np);
     c->wb.sb = k.take<double>((size_t)(2 * nsb + 2) * sk.Np);
     c->wb.sw = k.take<double>((size_t)nsb * sk.Np);
-    c->wb.hand = k.take<double>((size_t)2 * sk.nstrip * sk.ni * (5 + nsb));
+    c->wb.hand = k.take<double>((size_t)2 * sk.nstrip * (sk.T + 2 * HPAD) * (5 + nsb));
     c->wb.prog = k.take<int>(2);
     c->wb.nsI = 0;
     c->wave_ok = true;

@@ -38,6 +38,7 @@ struct OpDev {
 // Strip-skewed 2-D layout of the wavefront path (csb_wave.cuh): cell (i, j)
 // at ((j>>5)*T + i + (j&31))*32 + (j&31).
 constexpr int TQ = 16;  // T is a multiple of TQ; wavefront slot lengths divide TQ
+constexpr int HPAD = 32;  // zero rows either side of a strip's hand-off rows
 
 struct Skew {
   int ni, nj, nstrip, T;
@@ -54,7 +55,7 @@ struct WaveBufs {
   double* sf;     // species forward group (nsI + NSB + 2 planes)
   double* sb;     // species backward group (nsI + 2 + NSB planes, incl. dq*)
   double* sw;     // species dq (NSB planes)
-  double* hand;   // strip hand-off rows [2 sweeps][flow nstrip*ni*5 | species nstrip*ni*NSB]
+  double* hand;   // strip hand-off rows [2 sweeps][flow nstrip*(T+2*HPAD)*5 | species ..*NSB]
   int* prog;      // [2]: flow and species CTA tickets
   int nsI;        // species-diagonal planes of the current layout (0 = unset)
 };

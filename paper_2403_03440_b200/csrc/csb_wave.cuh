@@ -49,7 +49,7 @@
 
 namespace csb {
 
-constexpr int HRING = 128;  // hand-off ring (columns)
+constexpr int HRING = 128;  // hand-off ring (steps)
 // signalling NaN marking a hand-off word not yet written (see the chains)
 constexpr unsigned long long HAND_SENTINEL = 0x7FF4DEADBEEF0001ull;
 constexpr int NFF = 30, NFB = 30, FB_DQ = 25;
@@ -146,11 +146,18 @@ __global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp,
   double* TC = sm + 12 * NH;                   // [NCP][CT]
   const long long N = g.N;
   {
-    // reset both sweeps' hand-off buffers to the sentinel (csb_wave.cuh chains)
-    const long long nh = 2LL * sk.nstrip * g.ni * (5 + NSB);
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nh;
-         e += (long long)gridDim.x * blockDim.x)
-      wb.hand[e] = __longlong_as_double((long long)HAND_SENTINEL);
+    // reset both sweeps' hand-off buffers: sentinel, zero in the pad rows
+    const long long rows = (long long)sk.T + 2 * HPAD;
+    const long long per_sweep = (long long)sk.nstrip * rows * (5 + NSB);
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < 2 * per_sweep;
+         e += (long long)gridDim.x * blockDim.x) {
+      const long long w = e % per_sweep;
+      const long long flow_words = (long long)sk.nstrip * rows * 5;
+      const int nh = w < flow_words ? 5 : NSB;
+      const long long r = (w < flow_words ? w : w - flow_words) / nh % rows;
+      wb.hand[e] = (r < HPAD || r >= rows - HPAD) ? 0.0
+                                                  : __longlong_as_double((long long)HAND_SENTINEL);
+    }
   }
   // ---------------- phase A: halo-extended per-cell quantities.  Enumerated
   // column by column (fixed i, consecutive j) so that the loads of a warp are
@@ -372,10 +379,12 @@ struct ChainCtx {
   const WaveArgs* a;
   int s, nslots, D, rt;
   bool has_up, has_down, first, last;
+  bool recv;            // first row of a strip with an upstream strip
+  bool send;            // last row of a strip with a downstream strip
   double mul;           // 0 on the first row (takes the hand-off), 1 elsewhere
   const double* ring;
   const double* hin;
-  double* hand_out;     // this strip's row of the hand-off buffer
+  double* hand_out;     // this strip's row of the hand-off buffer, at its step 0
   unsigned long long* full_bar;
   unsigned long long* empty_bar;
 };
@@ -404,17 +413,16 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
     mbar_wait(&x.full_bar[buf], phase);
     const double* base = x.ring + buf * slot + lane;
     double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO) * 32 + lane;
+    const double* hb = x.recv ? x.hin + ((k * WK) % HRING) * 5 : x.hin + HRING * 5;
+    double* ho = x.hand_out + (long long)k * WK * 5;
 #pragma unroll
     for (int m = 0; m < WK; ++m) {
       const int kk = BWD ? WK - 1 - m : m;
-      const int t = k * WK + kk;
       const double* p = base + kk * NG * 32;
-      const int qn = BWD ? a.ni - 1 - t + x.rt : t;
-      const bool hin_ok = x.first && x.has_up && qn >= 0 && qn < a.ni;
-      // the first row takes the upstream hand-off (or zero) instead of the
-      // shuffled value: ij = sh * mul + hv with mul = 0 and hv the hand-off
-      // there, mul = 1 and hv = +0 (a zero row of hin) elsewhere
-      const double* hv = x.hin + (hin_ok ? (qn % HRING) * 5 : HRING * 5);
+      // the first row takes the upstream hand-off instead of the shuffled
+      // value: ij = sh * mul + hv with mul = 0 and hv the hand-off there,
+      // mul = 1 and hv = +0 (the zero block of hin) elsewhere
+      const double* hv = hb + kk * 5;
       double ij[5];
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
@@ -445,10 +453,8 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
         o[3] = w3 * sa + sig * dq[3];
         o[4] = w4 * sa + pf[5 * 32] * sb + sig * dq[4];
       }
-      const int qo = BWD ? a.ni - 1 - t : t - x.rt;
-      const bool ho = x.has_down && x.last && qo >= 0 && qo < a.ni;
 #pragma unroll
-      for (int c = 0; c < 5; ++c) st_pred_cg_f64(x.hand_out + qo * 5 + c, oj[c], ho);
+      for (int c = 0; c < 5; ++c) st_pred_cg_f64(ho + kk * 5 + c, oj[c], x.send);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&x.empty_bar[buf]);
@@ -482,14 +488,13 @@ CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro) {
     mbar_wait(&x.full_bar[buf], phase);
     const double* base = x.ring + buf * slot + lane;
     double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO) * 32 + lane;
+    const double* hb = x.recv ? x.hin + ((k * WK) % HRING) * NSB : x.hin + HRING * NSB;
+    double* ho = x.hand_out + (long long)k * WK * NSB;
 #pragma unroll
     for (int m = 0; m < WK; ++m) {
       const int kk = BWD ? WK - 1 - m : m;
-      const int t = k * WK + kk;
       const double* p = base + kk * NG * 32;
-      const int qn = BWD ? a.ni - 1 - t + x.rt : t;
-      const bool hin_ok = x.first && x.has_up && qn >= 0 && qn < a.ni;
-      const double* hv = x.hin + (hin_ok ? (qn % HRING) * NSB : HRING * NSB);
+      const double* hv = hb + kk * NSB;
       double ij[NSB];
 #pragma unroll
       for (int c = 0; c < NSB; ++c) {
@@ -506,10 +511,8 @@ CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro) {
         oi[c] = ci * dq;
         oj[c] = cj * dq;
       }
-      const int qo = BWD ? a.ni - 1 - t : t - x.rt;
-      const bool ho = x.has_down && x.last && qo >= 0 && qo < a.ni;
 #pragma unroll
-      for (int c = 0; c < NSB; ++c) st_pred_cg_f64(x.hand_out + qo * NSB + c, oj[c], ho);
+      for (int c = 0; c < NSB; ++c) st_pred_cg_f64(ho + kk * NSB + c, oj[c], x.send);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&x.empty_bar[buf]);
@@ -540,7 +543,7 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   const int D = ro.D, NG = ro.ng;
   const long long slot = (long long)WK * NG * 32;
   double* ring = wsm;                     // [D][WK][NG][32]
-  double* hin = ring + D * slot;          // [HRING + 1][nh], row HRING = zeros
+  double* hin = ring + D * slot;          // [HRING + WK][nh], rows >= HRING zero
   if (threadIdx.x == 0) {
     const int tk = atomicAdd(ro.ticket, 1);
     s_strip = tk >= a.sk.nstrip ? -1 : (BWD ? a.sk.nstrip - 1 - tk : tk);
@@ -559,9 +562,13 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   x.first = BWD ? (lane == x.rt) : (lane == 0);  // receives the upstream hand-off
   x.last = BWD ? (lane == 0) : (lane == x.rt);   // sends the downstream hand-off
   x.mul = x.first ? 0.0 : 1.0;
+  x.recv = x.first && x.has_up;
+  x.send = x.last && x.has_down;
   x.ring = ring;
   x.hin = hin;
-  x.hand_out = ro.hand + (long long)x.s * a.ni * nh;
+  // hand-off rows are indexed by the producing strip's step, with HPAD
+  // zero rows on both sides (steps whose partner column lies outside the grid)
+  x.hand_out = ro.hand + ((long long)x.s * (T + 2 * HPAD) + HPAD) * nh;
   x.full_bar = full_bar;
   x.empty_bar = empty_bar;
   if (threadIdx.x == 0) {
@@ -569,7 +576,7 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
       mbar_init(&full_bar[b], x.has_up ? 2 : 1);  // TMA producer (+ hand-off receiver)
       mbar_init(&empty_bar[b], 1);
     }
-    for (int c = 0; c < nh; ++c) hin[HRING * nh + c] = 0.0;
+    for (int c = 0; c < WK * nh; ++c) hin[HRING * nh + c] = 0.0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -606,24 +613,18 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
     // arrival on the slot's full barrier (release: the chain's wait acquires).
     if (!x.has_up) return;
     constexpr int CAP = (NSB > 5 ? NSB : 5) < 16 ? (NSB > 5 ? NSB : 5) : 16;
-    const int ni = a.ni;
-    const double* src = ro.hand + (long long)up * ni * nh;
+    // upstream row u of the hand-off buffer holds what the upstream strip's
+    // sending row produced at its step u; this strip's first row needs, at
+    // its step t, the upstream step t + 31 (forward: upstream row 31 -> our
+    // row 0) or t - 31 (backward: upstream row 0 -> our row 31)
+    const double* src = ro.hand + ((long long)up * (T + 2 * HPAD) + HPAD) * nh;
     int buf = 0, phase = 0;
     for (int ks = 0; ks < x.nslots; ++ks) {
       const int k = BWD ? x.nslots - 1 - ks : ks;
       if (ks >= D) mbar_wait(&empty_bar[buf], phase ^ 1);  // slot free: hin rows too
-      int qlo, qhi;  // q range of the slot's first-row needs
-      if (!BWD) {
-        qlo = k * WK;
-        qhi = k * WK + WK - 1;
-      } else {
-        qlo = ni - 1 - (k * WK + WK - 1) + x.rt;
-        qhi = ni - 1 - k * WK + x.rt;
-      }
-      qlo = max(qlo, 0);
-      qhi = min(qhi, ni - 1);
-      const int q = qlo + lane;
-      const bool in = q <= qhi;
+      const int t = k * WK + lane;                          // our step
+      const long long u = BWD ? t - 31 : t + 31;            // upstream step
+      const bool in = lane < WK;
       unsigned long long w[CAP];
       bool done = !in;
       while (true) {
@@ -633,20 +634,20 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
           for (int c = 0; c < CAP; ++c) {
             if (c < nh) {
               w[c] = (unsigned long long)__ldcg(reinterpret_cast<const long long*>(src) +
-                                                (long long)q * nh + c);
+                                                u * nh + c);
               ok &= w[c] != HAND_SENTINEL;
             }
           }
           for (int c = CAP; c < nh; ++c)
-            ok &= (unsigned long long)__ldcg(reinterpret_cast<const long long*>(src) +
-                                             (long long)q * nh + c) != HAND_SENTINEL;
+            ok &= (unsigned long long)__ldcg(reinterpret_cast<const long long*>(src) + u * nh +
+                                             c) != HAND_SENTINEL;
           if (ok) {
 #pragma unroll
             for (int c = 0; c < CAP; ++c)
-              if (c < nh) hin[(q % HRING) * nh + c] = __longlong_as_double((long long)w[c]);
+              if (c < nh) hin[(t % HRING) * nh + c] = __longlong_as_double((long long)w[c]);
             for (int c = CAP; c < nh; ++c)
-              hin[(q % HRING) * nh + c] = __longlong_as_double(
-                  __ldcg(reinterpret_cast<const long long*>(src) + (long long)q * nh + c));
+              hin[(t % HRING) * nh + c] = __longlong_as_double(
+                  __ldcg(reinterpret_cast<const long long*>(src) + u * nh + c));
             done = true;
           }
         }
@@ -795,7 +796,7 @@ __global__ void __launch_bounds__(256) k_epilogue2d(const Model* __restrict__ mp
 
 // ============================================================== launcher
 inline size_t wave_role_smem(int D, int WK, int NG, int nh) {
-  return ((size_t)D * WK * NG * 32 + (size_t)(HRING + 1) * nh) * sizeof(double);
+  return ((size_t)D * WK * NG * 32 + (size_t)(HRING + WK) * nh) * sizeof(double);
 }
 // deepest ring (2..4) that fits the shared-memory budget, 0 if none
 inline int wave_depth(int WK, int NG, int nh) {
@@ -859,7 +860,8 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       rf.out = bwd ? wb.fw : wb.fb;
       rf.ngo = bwd ? 5 : NFB;
       rf.po = bwd ? 0 : FB_DQ;
-      const long long hsz = (long long)sk.nstrip * g.ni * (5 + NSB);  // one sweep
+      const long long hrows = (long long)sk.T + 2 * HPAD;
+      const long long hsz = (long long)sk.nstrip * hrows * (5 + NSB);  // one sweep
       rf.hand = wb.hand + (bwd ? hsz : 0);
       rf.ticket = wb.prog;
       rs.in = bwd ? wb.sb : wb.sf;
@@ -868,7 +870,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       rs.out = bwd ? wb.sw : wb.sb;
       rs.ngo = bwd ? NSB : NSF;
       rs.po = bwd ? 0 : nsI + 2;
-      rs.hand = wb.hand + (bwd ? hsz : 0) + (long long)sk.nstrip * g.ni * 5;
+      rs.hand = wb.hand + (bwd ? hsz : 0) + (long long)sk.nstrip * hrows * 5;
       rs.ticket = wb.prog + 1;
       const size_t smem = std::max(wave_role_smem(Df, WKF, NFF, 5), wave_role_smem(Ds, WKS, NSF, NSB));
       auto kfn = bwd ? (per_species ? k_wave2d<NSB, true, true> : k_wave2d<NSB, true, false>)
