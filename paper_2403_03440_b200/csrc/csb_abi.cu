@@ -35,6 +35,9 @@ struct csb_ctx {
   OpDev op{};
   double *dtau = nullptr, *R = nullptr, *dq = nullptr, *partial = nullptr, *norms = nullptr;
   double* dom_scratch = nullptr;
+  double* norm_partial = nullptr;
+  unsigned int* norm_counter = nullptr;
+  int npart_cap = 0;
   int assembled_scheme = -1;
   WaveBufs wb{};
   bool wave_ok = false;
@@ -166,6 +169,11 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
   c->R = k.take<double>((size_t)nv * N);
   c->dq = k.take<double>((size_t)nv * N);
   c->partial = k.take<double>(3 * 512);
+  // fused residual-norm partials: one per residual tile (tiles hold >= 64 cells
+  // except on tiny grids; larger tile counts fall back to the norms kernels)
+  c->npart_cap = (int)std::max<long long>(4096, N / 64 + 1);
+  c->norm_partial = k.take<double>((size_t)3 * c->npart_cap);
+  c->norm_counter = k.take<unsigned int>(64);
   c->norms = k.take<double>(4);
   // 2-D wavefront path buffers (csb_wave.cuh): strip-skewed planes
   c->wave_ok = false;
@@ -397,6 +405,8 @@ int csb_set_workspace(csb_ctx* c, void* dev, size_t bytes) {
   c->ws_bytes = bytes;
   c->has_ws = true;
   c->assembled_scheme = -1;
+  if (cudaMemset(c->norm_counter, 0, 64 * sizeof(unsigned int)) != cudaSuccess)
+    return fail(c, CSB_E_CUDA, "zero norm counter");
   if (c->wave_ok) {
     // wavefront padding slots (t - r outside [0, ni), rows beyond nj) are never
     // written by the records kernel: they must hold zeros so that padding
@@ -717,9 +727,14 @@ int csb_iteration(csb_ctx* c, const double* q, double cfl, int scheme, int offdi
   if ((r = sync_fs(c))) return r;
   cudaStream_t st = S(stream);
   double* R = R_out ? R_out : c->R;
+  bool fused = false;
   cudaError_t e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
-                                  use_k2d(c), c->flags, st);
-  if (e == cudaSuccess) e = launch_norms(c->ns, c->g.N, R, c->partial, norms3 ? norms3 : c->norms, st);
+                                  use_k2d(c), c->flags, st,
+                                  NormsOut{c->norm_partial, c->npart_cap, c->norm_counter,
+                                           norms3 ? norms3 : c->norms},
+                                  &fused);
+  if (e == cudaSuccess && !fused)
+    e = launch_norms(c->ns, c->g.N, R, c->partial, norms3 ? norms3 : c->norms, st);
   if (e != cudaSuccess) return cuda_check(c, e, "iteration residual");
   return implicit_impl(c, q, R, cfl, scheme, offdiag_paper, nullptr, q_new, st);
 }

@@ -67,9 +67,22 @@ cudaError_t launch_wave_step(const Model* mp, int ns, const GridDev& g, const Wa
                              unsigned long long* flags, cudaStream_t st,
                              cudaEvent_t* ev = nullptr);
 
+// residual_norms fused into the residual kernel (driver.py:85-90): per-tile
+// partial sums + a last-block reduction in fixed order (deterministic).
+struct NormsOut {
+  double* partial;         // [3][cap]
+  int cap;                 // tiles the partial buffer can hold
+  unsigned int* counter;   // zero between launches (reset by the last block)
+  double* out;             // [3] flow, species, density (null: no norms)
+};
+
+// launch_residual returns with *fused = true when the norms were computed
+// in the same launch (nrm.out set and the tile count fits nrm.cap).
 cudaError_t launch_residual(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                             const Mech& mech, const double* q, double* R, int first_order, bool k2d,
-                            unsigned long long* flags, cudaStream_t st);
+                            unsigned long long* flags, cudaStream_t st,
+                            NormsOut nrm = NormsOut{nullptr, 0, nullptr, nullptr},
+                            bool* fused = nullptr);
 cudaError_t launch_padded(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                           const double* q, double* P, unsigned long long* flags, cudaStream_t st);
 

@@ -571,7 +571,8 @@ template <int NSB, bool K2D>
 __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ mp, GridDev g, BCDev bc,
                                                   Mech mech, const double* __restrict__ q,
                                                   double* __restrict__ R, int first_order, int TI,
-                                                  int TJ, int TK, unsigned long long* flags) {
+                                                  int TJ, int TK, unsigned long long* flags,
+                                                  NormsOut nrm) {
   extern __shared__ double smem[];
   __shared__ Model sm;
   {
@@ -756,7 +757,9 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
     __syncthreads();
   }
 
-  // chemistry source (spatial.py:261-267) and the finite check (269-271)
+  // chemistry source (spatial.py:261-267), the finite check (269-271) and,
+  // when requested, the residual norms (driver.py:85-90)
+  double n_flow = 0.0, n_sp = 0.0, n_rho = 0.0;
   const int ncell = ci * cj * ck;
   for (int l = threadIdx.x; l < ncell; l += blockDim.x) {
     const int kk = l % ck, jj = (l / ck) % cj, ii = l / (ck * cj);
@@ -778,8 +781,74 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
         }
     }
     bool fin = true;
-    for (int c = 0; c < nv; ++c) fin &= finite(R[(long long)c * g.N + cell]);
+    double rv[5 + NSB];
+#pragma unroll
+    for (int c = 0; c < 5 + NSB; ++c)
+      if (c < nv) {
+        rv[c] = R[(long long)c * g.N + cell];
+        fin &= finite(rv[c]);
+      }
     if (!fin) raise_flag(flags, EB_RES_NONFINITE, cell);
+    if (nrm.out) {
+      // residual_norms terms (driver.py:85-90), as k_norms_partial
+      double f = rv[0] * rv[0];
+#pragma unroll
+      for (int c = 1; c < 5; ++c) f += rv[c] * rv[c];
+      double sp = 0.0;
+#pragma unroll
+      for (int c = 0; c < NSB; ++c)
+        if (c < ns) sp += rv[5 + c];
+      n_flow += f;
+      n_sp += sp * sp;
+      n_rho += rv[0] * rv[0];
+    }
+  }
+  if (nrm.out) {
+    // block partials, then the last block reduces all partials in fixed order
+    __shared__ double red[3][8];
+    __shared__ bool last_block;
+    double v3[3] = {n_flow, n_sp, n_rho};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double v = v3[k];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < 3; ++k) {
+        double v = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[k][w];
+        nrm.partial[k * nrm.cap + blockIdx.x] = v;
+      }
+      __threadfence();
+      last_block = atomicAdd(nrm.counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last_block) {
+      __threadfence();
+      const int nb = gridDim.x;
+      double acc[3] = {0.0, 0.0, 0.0};
+      for (int b = threadIdx.x; b < nb; b += blockDim.x)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[k] += __ldcg(nrm.partial + k * nrm.cap + b);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double v = acc[k];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int k = 0; k < 3; ++k) {
+          double v = 0.0;
+          for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[k][w];
+          nrm.out[k] = sqrt(v);
+        }
+        *nrm.counter = 0u;
+      }
+    }
   }
 }
 
@@ -838,22 +907,26 @@ static inline void pick_tile(int ns, bool k2d, int nk, int& TI, int& TJ, int& TK
 
 cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                             const Mech& mech, const double* q, double* R, int first_order, bool k2d,
-                            unsigned long long* flags, cudaStream_t st) {
+                            unsigned long long* flags, cudaStream_t st, NormsOut nrm, bool* fused) {
   int TI, TJ, TK;
   size_t smem;
   pick_tile(ns, k2d, g.nk, TI, TJ, TK, smem);
   const long long ntiles = (long long)((g.ni + TI - 1) / TI) * ((g.nj + TJ - 1) / TJ) *
                            (k2d ? 1 : (g.nk + TK - 1) / TK);
+  if (!(nrm.out && ntiles <= nrm.cap)) nrm.out = nullptr;
+  if (fused) *fused = nrm.out != nullptr;
   cudaError_t err = cudaSuccess;
   CSB_NS_DISPATCH(ns, {
     if (k2d) {
       auto kfn = k_residual<NSB, true>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kfn<<<(unsigned)ntiles, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags);
+      kfn<<<(unsigned)ntiles, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
+                                               nrm);
     } else {
       auto kfn = k_residual<NSB, false>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kfn<<<(unsigned)ntiles, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags);
+      kfn<<<(unsigned)ntiles, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
+                                               nrm);
     }
     err = cudaGetLastError();
   });

@@ -193,3 +193,40 @@ def test_wavefront_matches_generic_ogrid_and_chemistry():
     _wave_vs_generic(C.config2(seed=2, dims=(48, 40, 1)), "CS1")
     _wave_vs_generic(C.config3(20, dims=(24, 40, 1), chemistry=True), "CS1")
     _wave_vs_generic(C.config3(40, dims=(24, 36, 1)), "CS2")
+
+
+# ---------------------------------------------------------------- fused iteration (bench path)
+
+@pytest.mark.parametrize("dims", [(96, 80, 1), (33, 70, 1)])
+def test_fused_iteration_matches_stages_and_oracle(dims):
+    """csb_iteration (residual with fused norms + implicit step, the bench's
+    per-step call) against the separate stage entry points and the oracle's
+    residual_norms (driver.py:85-90)."""
+    import ctypes
+
+    from paper_2403_03440_b200 import configs as C
+    from paper_2403_03440_b200.configs import build_case
+    from paper_2403_03440_b200.device import SCHEMES, get_engine
+    from paper_2403_03440_b200.driver import residual_norms
+
+    spec = C.config0(seed=5, dims=dims)
+    grid, model, bcs, mech = build_case(spec)
+    eng = get_engine(grid, model)
+    eng.set_bcs(bcs)
+    eng.set_mechanism(mech)
+    q = eng.to_soa(spec.q, eng.nv)
+    qn, R, n3 = eng.empty(eng.nv, eng.N), eng.empty(eng.nv, eng.N), eng.empty(4)
+    st = ctypes.c_void_p(eng.stream)
+    for _ in range(3):  # repeated launches: the last-block counter must reset
+        rc = eng.lib.csb_iteration(eng.ctx, q.data_ptr(), float(spec.cfl), SCHEMES["CS1"], 0, 0,
+                                   qn.data_ptr(), R.data_ptr(), n3.data_ptr(), st)
+        assert rc == 0, eng.lib.csb_last_error(eng.ctx)
+        eng.status()
+    n_fused = n3.cpu().numpy()[:3]
+    Raos = eng.from_soa(R, spec.q, spec.q.shape)
+    ref = residual_norms(Raos)
+    n_sep = np.array([ref.flow, ref.species, ref.density])
+    assert np.max(np.abs(n_fused - n_sep) / np.abs(n_sep)) <= 1e-12
+    th, og, obcs, omech = spec_oracle(spec)
+    on = np.array(O.norms(O.residual(spec.q, og, obcs, omech, th)))
+    assert np.max(np.abs(n_fused - on) / np.abs(on)) <= 1e-10
