@@ -124,7 +124,7 @@ CSB_DEV long long gaddr(const Skew& k, int NG, int s, int t, int p, int r) {
 // -R.  Phase B: per interior cell, face radii (max of the two adjacent cells
 // at the face metric), face coefficients, and all record stores.
 template <int NSB>
-__global__ void __launch_bounds__(256) k_records2d(const Model* __restrict__ mp, GridDev g, Skew sk,
+__global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ mp, GridDev g, Skew sk,
                                                    const double* __restrict__ q,
                                                    const double* __restrict__ R, double cfl,
                                                    const double* __restrict__ lamS,
@@ -684,7 +684,7 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
 // phase B: closure + gate column by column, so the q / q_new accesses of a
 // warp are contiguous runs of up to C cells.
 template <int NSB>
-__global__ void __launch_bounds__(256) k_epilogue2d(const Model* __restrict__ mp, GridDev g, Skew sk,
+__global__ void __launch_bounds__(256, 2) k_epilogue2d(const Model* __restrict__ mp, GridDev g, Skew sk,
                                                     int scheme, const double* __restrict__ q,
                                                     const double* __restrict__ fw,
                                                     const double* __restrict__ sw,
@@ -819,7 +819,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     const int Df = wave_depth(WKF, NFF, 5), Ds = wave_depth(WKS, NSF, NSB);
     if (!Df || !Ds) return cudaErrorInvalidConfiguration;
     // ---------------- records
-    int C = 8;
+    int C = 4;  // measured: 4 steps per tile with 4 CTAs/SM beats 8 (1 CTA/SM less)
     if (const char* ev_c = getenv("CSB_REC_C")) C = atoi(ev_c);  // tuning probe
     auto rsm_of = [&](int c) {
       return ((size_t)(16 + nsI + NSB) * c * 32 + 12 * (size_t)(c + 2) * 34) * sizeof(double);
