@@ -186,8 +186,9 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
     sk.Np = (long long)sk.nstrip * sk.T * 32;  // cells per plane (step-major groups)
     c->wb.sk = sk;
     const int nsb = bucket_of(ns);
-    c->wb.ff = k.take<double>((size_t)30 * sk.Np);
-    c->wb.fb = k.take<double>((size_t)30 * sk.Np);
+    const int nff = std::max(30, 3 * (5 + nsb) + 10);  // CS flow or CI coupled records
+    c->wb.ff = k.take<double>((size_t)nff * sk.Np);
+    c->wb.fb = k.take<double>((size_t)nff * sk.Np);
     c->wb.fw = k.take<double>((size_t)5 * sk.Np);
     c->wb.sf = k.take<double>((size_t)(2 * nsb + 2) * sk.Np);
     c->wb.sb = k.take<double>((size_t)(2 * nsb + 2) * sk.Np);
@@ -206,7 +207,8 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
 int zero_wave_records(csb_ctx* c, cudaStream_t st) {
   const int nsb = bucket_of(c->ns);
   const WaveBufs& w = c->wb;
-  const std::pair<double*, int> groups[] = {{w.ff, 30},          {w.fb, 30},
+  const int nff = std::max(30, 3 * (5 + nsb) + 10);
+  const std::pair<double*, int> groups[] = {{w.ff, nff},         {w.fb, nff},
                                             {w.fw, 5},           {w.sf, 2 * nsb + 2},
                                             {w.sb, 2 * nsb + 2}, {w.sw, nsb}};
   for (const auto& gp : groups)
@@ -636,8 +638,9 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
   const bool chem = mech_of(c).nrx > 0;
   const bool full = chem && scheme == SCH_CI;
   if (full && !c->ws_block) return fail(c, CSB_E_STATE, "CI with chemistry needs block workspace");
-  const bool wave = path != 1 && c->wave_ok && !c->wave_disabled && scheme != SCH_CI &&
-                    c->geom2d_ok;
+  // the coupled operator takes the wavefront path when frozen and ns <= 16
+  const bool ci_wave = scheme != SCH_CI || (!chem && bucket_of(c->ns) <= 16);
+  const bool wave = path != 1 && c->wave_ok && !c->wave_disabled && ci_wave && c->geom2d_ok;
   if (path == 2 && !wave) return fail(c, CSB_E_STATE, "2-D wavefront path not applicable");
   if (wave) {
     cudaError_t e = cudaSuccess;
@@ -653,7 +656,7 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
       domd = op.dom;
       dstride = op.dom_full ? c->ns + 1 : 1;
     }
-    const int nsI = chem ? c->ns : 1;
+    const int nsI = scheme == SCH_CI ? -1 : chem ? c->ns : 1;  // record layout key
     if (e == cudaSuccess && c->wb.nsI != nsI) {
       // species record layout changes with nsI: re-zero the padding slots
       e = zero_wave_records(c, st) ? cudaErrorUnknown : cudaSuccess;

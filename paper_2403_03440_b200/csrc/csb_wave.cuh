@@ -55,6 +55,19 @@ constexpr unsigned long long HAND_SENTINEL = 0x7FF4DEADBEEF0001ull;
 constexpr int NFF = 30, NFB = 30, FB_DQ = 25;
 constexpr int WKF = 8;     // flow slot: 8 steps x 30 planes = 60 KiB
 
+// Coupled (CI, frozen chemistry) records, NV = 5 + NSB components:
+//   CF (forward)  invd, hr2, w[NV], b[NV], rhs[NV], upper faces (e[3], sig) x 2
+//   CB (backward) invd, hr2, w[NV], b[NV], lower faces (e[3], sig) x 2, dq*[NV]
+template <int NSB>
+constexpr int ci_planes() { return 3 * (5 + NSB) + 10; }
+template <int NSB>
+constexpr int ci_wk() {
+  int w = 8;
+  while (w > 1 && w * ci_planes<NSB>() * 256 > 64 * 1024) w /= 2;
+  return w;
+}
+constexpr int CI_MAXNSB = 16;  // larger species counts use the generic CI path
+
 // species slot length: <= 64 KiB per slot at the widest layout (nsI = NSB)
 template <int NSB>
 constexpr int wave_wks() {
@@ -123,7 +136,7 @@ CSB_DEV long long gaddr(const Skew& k, int NG, int s, int t, int p, int r) {
 // interior cells also get dtau, the diagonals, the Jacobian ingredients and
 // -R.  Phase B: per interior cell, face radii (max of the two adjacent cells
 // at the face metric), face coefficients, and all record stores.
-template <int NSB>
+template <int NSB, bool CI>
 __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ mp, GridDev g, Skew sk,
                                                    const double* __restrict__ q,
                                                    const double* __restrict__ R, double cfl,
@@ -140,7 +153,9 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
   const int t0 = ib * C, j0 = s * 32;
   const int HX = C + 2, HY = 34, NH = HX * HY;
   const int CT = C * 32;
-  const int NCP = 16 + nsI + NSB;              // cell planes: invd w b rhs | invs rhs_s
+  constexpr int NV = 5 + NSB;
+  // cell planes: CS invd w b rhs | invs rhs_s;  CI invd hr2 w[NV] b[NV] rhs[NV]
+  const int NCP = CI ? 2 + 3 * NV : 16 + nsI + NSB;
   double* A = sm;                              // [12][NH]: u, v, w, c, nf, nsp, V, hr,
                                                //   lower-i face Sx Sy, lower-j face Sx Sy
   double* TC = sm + 12 * NH;                   // [NCP][CT]
@@ -152,8 +167,8 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < 2 * per_sweep;
          e += (long long)gridDim.x * blockDim.x) {
       const long long w = e % per_sweep;
-      const long long flow_words = (long long)sk.nstrip * rows * 5;
-      const int nh = w < flow_words ? 5 : NSB;
+      const long long flow_words = CI ? per_sweep : (long long)sk.nstrip * rows * 5;
+      const int nh = CI ? 5 + NSB : w < flow_words ? 5 : NSB;
       const long long r = (w < flow_words ? w : w - flow_words) / nh % rows;
       wb.hand[e] = (r < HPAD || r >= rows - HPAD) ? 0.0
                                                   : __longlong_as_double((long long)HAND_SENTINEL);
@@ -231,6 +246,56 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
     if (!(den > 0.0)) raise_flag(flags, EB_ZERO_WAVE, c);
     const double dtau = cfl / den;
     const double base = V / dtau;
+    if constexpr (CI) {
+      // CI: one scalar diagonal with the unified radius (implicit.py:362-373)
+      double rci = 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        int hi[3] = {i, j, 0};
+        hi[d] += 1;
+        double a[3], b[3];
+        load_S(g, d, face_index(g, d, i, j, 0), a);
+        load_S(g, d, face_index(g, d, hi[0], hi[1], hi[2]), b);
+        double Sc[3];
+#pragma unroll
+        for (int x = 0; x < 3; ++x) Sc[x] = 0.5 * (a[x] + b[x]);
+        const double a2 = (Sc[0] * Sc[0] + Sc[1] * Sc[1]) + Sc[2] * Sc[2];
+        const double U = fabs(cs.u[0] * Sc[0] + cs.u[1] * Sc[1] + cs.u[2] * Sc[2]);
+        const double lu = (U + cs.c * sqrt(a2)) + 2.0 * nu * a2 / V;
+        rci = d == 0 ? lu : rci + lu;
+      }
+      const double dci = base + rci;
+      if (!(fabs(dci) >= 1e-300) || !isfinite(dci)) raise_flag(flags, EB_SINGULAR, c);
+      const double beta = cs.gamma - 1.0;
+      TC[0 * CT + e] = 1.0 / dci;
+      TC[1 * CT + e] = 1.0 / cs.rho;
+      double* tw = TC + 2 * CT;
+      double* tb = TC + (2 + NV) * CT;
+      double* tr = TC + (2 + 2 * NV) * CT;
+      tw[0 * CT + e] = cs.rho;
+      tw[1 * CT + e] = cs.rho * cs.u[0];
+      tw[2 * CT + e] = cs.rho * cs.u[1];
+      tw[3 * CT + e] = cs.rho * cs.u[2];
+      tw[4 * CT + e] = cs.rho * cs.h;
+      tb[0 * CT + e] = beta * cs.Ek;
+      tb[1 * CT + e] = -beta * cs.u[0];
+      tb[2 * CT + e] = -beta * cs.u[1];
+      tb[3 * CT + e] = -beta * cs.u[2];
+      tb[4 * CT + e] = beta;
+#pragma unroll
+      for (int sp = 0; sp < NSB; ++sp) {
+        // _w_column / _grad_p_row species entries (implicit.py:59-81)
+        const bool real = sp < ns;
+        const double RsT = real ? m.Rs[sp] * cs.T : 0.0;
+        const double hs = real ? m.bs[sp] + m.cp[sp] * cs.T : 0.0;
+        tw[(5 + sp) * CT + e] = real ? cs.rho * cs.Y[sp] : 0.0;
+        tb[(5 + sp) * CT + e] = real ? RsT - beta * (hs - RsT) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < NV; ++k)
+        tr[k * CT + e] = k < 5 + ns ? -R[(long long)k * N + c] : 0.0;
+      continue;
+    }
     const double dflow = base + rf;
     bool bad = !(fabs(dflow) >= 1e-300) || !isfinite(dflow);
     const double dsp0 = base + rsp;
@@ -275,6 +340,46 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
     if (i < 0 || i >= g.ni || j >= g.nj) continue;
     const int hc = (tt + 1) * HY + (r + 1);
     const double u = A[0 * NH + hc], v = A[1 * NH + hc], hr = A[7 * NH + hc];
+    if constexpr (CI) {
+      constexpr int NG = ci_planes<NSB>();
+      double* cf = wb.ff + gaddr(sk, NG, s, t, 0, r);
+      double* cb = wb.fb + gaddr(sk, NG, s, t, 0, r);
+      for (int p = 0; p < 2 + 2 * NV; ++p) {
+        const double xv = TC[p * CT + e];
+        cf[p * 32] = xv;
+        cb[p * 32] = xv;
+      }
+      for (int p = 2 + 2 * NV; p < 2 + 3 * NV; ++p) cf[p * 32] = TC[p * CT + e];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const int d = f & 1;
+        const bool upper = f < 2;
+        const int hf = upper ? (d == 0 ? hc + HY : hc + HY + 1) : hc;
+        double S[3];
+        S[0] = A[(8 + 2 * d) * NH + hf];
+        S[1] = A[(9 + 2 * d) * NH + hf];
+        S[2] = 0.0;
+        const double a2 = (S[0] * S[0] + S[1] * S[1]) + S[2] * S[2];
+        const double ar = sqrt(a2);
+        const int nb = upper ? (d == 0 ? hc + HY : hc + HY + 1) : (d == 0 ? hc - HY : hc - HY - 1);
+        const bool nb_in = upper ? (d == 0 ? i + 1 < g.ni : j + 1 < g.nj) : (d == 0 ? i > 0 : j > 0);
+        const int lo = upper ? hc : nb, hi = upper ? nb : hc;
+        // unified face radius (implicit.py:176-197 with nu = max(nu_flow, nu_sp))
+        auto lam = [&](int h) {
+          const double Uh = fabs(A[0 * NH + h] * S[0] + A[1 * NH + h] * S[1] + A[2 * NH + h] * S[2]);
+          const double nuh = npmax(A[4 * NH + h], A[5 * NH + h]);
+          return (Uh + A[3 * NH + h] * ar) + 2.0 * nuh * a2 / A[6 * NH + h];
+        };
+        const double lu = nb_in ? npmax(lam(lo), lam(hi)) : lam(hc);
+        const double U = u * S[0] + v * S[1];
+        double* fd = upper ? cf + (2 + 3 * NV + 4 * d) * 32 : cb + (2 + 2 * NV + 4 * d) * 32;
+        fd[0 * 32] = 0.5 * S[0];
+        fd[1 * 32] = 0.5 * S[1];
+        fd[2 * 32] = 0.5 * U;
+        fd[3 * 32] = 0.5 * (U + (upper ? lu : -lu));
+      }
+      continue;
+    }
     double* ff = wb.ff + gaddr(sk, NFF, s, t, 0, r);
     double* fb = wb.fb + gaddr(sk, NFB, s, t, 0, r);
     double* sf = wb.sf + gaddr(sk, NSF, s, t, 0, r);
@@ -347,6 +452,7 @@ struct WaveRole {
   int ng;            // its planes per step
   int D;             // ring depth
   double* out;       // chain output group
+  double* out2;      // CI backward: species components (SW); out gets the flow part (FW)
   int ngo, po;       // its planes per step, first output plane
   double* hand;      // [nstrip][ni][nh] hand-off rows (sentinel-initialised)
   int* ticket;
@@ -356,6 +462,7 @@ struct WaveArgs {
   Skew sk;
   int ni, nj, nsI;
   int only;          // -1: both roles (production); 0/1: one role (timing probe)
+  int ci;            // coupled operator: one CI chain per strip (role[0])
   int poll_ns;       // receiver back-off between empty polls
   unsigned long long* dbg;  // timing probe: [CTA][4] globaltimer stamps (or null)
   WaveRole role[2];  // 0 flow, 1 species
@@ -523,6 +630,89 @@ CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro) {
   }
 }
 
+// coupled (CI, frozen chemistry) chain: NV = 5 + NSB components per row with
+// the full rank-2 half blocks of lusgs.py:24-59 and the scalar diagonal
+// (lusgs.py:62-147); padding species carry zero records.
+template <int NSB, bool BWD>
+CSB_DEV void chain_ci(const ChainCtx& x, const WaveRole& ro) {
+  constexpr int NV = 5 + NSB, NG = ci_planes<NSB>(), WK = ci_wk<NSB>();
+  constexpr int PV = BWD ? 2 + 2 * NV + 8 : 2 + 2 * NV;  // dq* (backward) | rhs (forward)
+  constexpr int FQ = BWD ? 2 + 2 * NV : 2 + 3 * NV;      // first face plane
+  constexpr int NGO = BWD ? 5 : NG, PO = BWD ? 0 : 2 + 2 * NV + 8;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const WaveArgs& a = *x.a;
+  const long long slot = (long long)WK * NG * 32;
+  double oi[NV], oj[NV];
+#pragma unroll
+  for (int c = 0; c < NV; ++c) oi[c] = oj[c] = 0.0;
+  int buf = 0, phase = 0;
+  for (int ks = 0; ks < x.nslots; ++ks) {
+    const int k = BWD ? x.nslots - 1 - ks : ks;
+    mbar_wait(&x.full_bar[buf], phase);
+    const double* base = x.ring + buf * slot + lane;
+    const long long st0 = (long long)x.s * a.sk.T + (long long)k * WK;
+    double* ob = ro.out + (st0 * NGO + PO) * 32 + lane;
+    double* ob2 = BWD ? ro.out2 + st0 * NSB * 32 + lane : nullptr;
+    const double* hb = x.recv ? x.hin + ((k * WK) % HRING) * NV : x.hin + HRING * NV;
+    double* ho = x.hand_out + (long long)k * WK * NV;
+#pragma unroll
+    for (int m = 0; m < WK; ++m) {
+      const int kk = BWD ? WK - 1 - m : m;
+      const double* p = base + kk * NG * 32;
+      const double* hv = hb + kk * NV;
+      double ij[NV];
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
+        ij[c] = fma(sh, x.mul, hv[c]);
+      }
+      const double invd = p[0], hr2 = p[32];
+      double dq[NV];
+#pragma unroll
+      for (int c = 0; c < NV; ++c) {
+        const double v = p[(PV + c) * 32];
+        if (BWD) dq[c] = v - (oi[c] + ij[c]) * invd;
+        else dq[c] = ((v + oi[c]) + ij[c]) * invd;
+        if (!BWD) ob[(kk * NGO + c) * 32] = dq[c];
+        else if (c < 5) ob[(kk * 5 + c) * 32] = dq[c];
+        else ob2[(kk * NSB + c - 5) * 32] = dq[c];
+      }
+      // b . dq over all NV components, two interleaved partial sums
+      double sb0 = p[(2 + NV) * 32] * dq[0], sb1 = p[(3 + NV) * 32] * dq[1];
+#pragma unroll
+      for (int c = 2; c < NV; c += 2) {
+        sb0 = fma(p[(2 + NV + c) * 32], dq[c], sb0);
+        if (c + 1 < NV) sb1 = fma(p[(3 + NV + c) * 32], dq[c + 1], sb1);
+      }
+      const double sb = sb0 + sb1;
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        const double* pf = p + (FQ + 4 * f) * 32;
+        const double e0 = pf[0], e1 = pf[32], e2 = pf[64], sig = pf[96];
+        // a = (-U hr, Sx hr, Sy hr) = hr2 (-e2, e0, e1)
+        const double sa = hr2 * ((e0 * dq[1] + e1 * dq[2]) - e2 * dq[0]);
+        double* o = f == 0 ? oi : oj;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+          const double wc = p[(2 + c) * 32];
+          const double ec = c == 1 ? e0 : c == 2 ? e1 : c == 4 ? e2 : 0.0;
+          o[c] = (c == 1 || c == 2 || c == 4) ? wc * sa + ec * sb + sig * dq[c]
+                                              : wc * sa + sig * dq[c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NV; ++c) st_pred_cg_f64(ho + kk * NV + c, oj[c], x.send);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&x.empty_bar[buf]);
+    if (++buf == x.D) {
+      buf = 0;
+      phase ^= 1;
+    }
+  }
+}
+
 template <int NSB, bool BWD, bool PER>
 __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   extern __shared__ __align__(128) double wsm[];
@@ -534,12 +724,13 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   // role: 0 flow, 1 species.  Block pairs share a role: the two SMs of a TPC
   // run the same code (measured: a flow and a species CTA side by side on a
   // TPC slow the flow chain by ~14%)
-  const int kind = (a.only == 0 || a.only == 1) ? a.only
-                   : a.only == 5                ? (blockIdx.x & 1)
-                                                : ((blockIdx.x >> 1) & 1);
-  const WaveRole ro = kind ? a.role[1] : a.role[0];
-  const int WK = kind ? wave_wks<NSB>() : WKF;
-  const int nh = kind ? NSB : 5;
+  const int kind = a.ci ? 2
+                   : (a.only == 0 || a.only == 1) ? a.only
+                   : a.only == 5                  ? (blockIdx.x & 1)
+                                                  : ((blockIdx.x >> 1) & 1);
+  const WaveRole ro = kind == 1 ? a.role[1] : a.role[0];
+  const int WK = kind == 2 ? ci_wk<NSB>() : kind ? wave_wks<NSB>() : WKF;
+  const int nh = kind == 2 ? 5 + NSB : kind ? NSB : 5;
   const int D = ro.D, NG = ro.ng;
   const long long slot = (long long)WK * NG * 32;
   double* ring = wsm;                     // [D][WK][NG][32]
@@ -667,8 +858,13 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   // -------------------------------------------------------- chain (warp 0)
   unsigned long long t0 = 0;
   if (a.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  if (kind == 0) chain_flow<BWD>(x, ro);
-  else chain_species<NSB, BWD, PER>(x, ro);
+  if (kind == 0) {
+    chain_flow<BWD>(x, ro);
+  } else if (kind == 1) {
+    chain_species<NSB, BWD, PER>(x, ro);
+  } else {
+    if constexpr (NSB <= CI_MAXNSB && !PER) chain_ci<NSB, BWD>(x, ro);
+  }
   if (a.dbg && lane == 0) {
     unsigned long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
@@ -812,6 +1008,67 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
                                      double* dq_std, unsigned long long* flags, cudaStream_t st,
                                      cudaEvent_t* ev) {
   CSB_NS_DISPATCH(ns, {
+    if (scheme == SCH_CI) {
+      // ---------------- coupled operator (frozen chemistry): one chain per strip
+      if constexpr (NSB > CI_MAXNSB) {
+        return cudaErrorInvalidConfiguration;
+      } else {
+        if (per_species) return cudaErrorInvalidConfiguration;
+        const Skew& sk = wb.sk;
+        constexpr int NV = 5 + NSB, NG = ci_planes<NSB>(), WK = ci_wk<NSB>();
+        const int Dc = wave_depth(WK, NG, NV);
+        if (!Dc) return cudaErrorInvalidConfiguration;
+        int C = 4;
+        auto rsm_of = [&](int c) {
+          return ((size_t)(2 + 3 * NV) * c * 32 + 12 * (size_t)(c + 2) * 34) * sizeof(double);
+        };
+        while (C > 1 && rsm_of(C) > 200 * 1024) C /= 2;
+        const size_t rsm = rsm_of(C);
+        cudaFuncSetAttribute(k_records2d<NSB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)rsm);
+        if (ev) cudaEventRecord(ev[0], st);
+        k_records2d<NSB, true><<<sk.nstrip * (sk.T / C), 256, rsm, st>>>(
+            mp, g, sk, q, R, cfl, lamS, domd, dom_stride, 0, sp_scale, wb, C, flags);
+        if (ev) cudaEventRecord(ev[1], st);
+        for (int pass = 0; pass < 2; ++pass) {
+          const bool bwd = pass == 1;
+          WaveArgs wa{};
+          wa.sk = sk;
+          wa.ni = g.ni;
+          wa.nj = g.nj;
+          wa.nsI = 1;
+          wa.only = -1;
+          wa.poll_ns = 16;
+          wa.ci = 1;
+          wa.dbg = nullptr;
+          WaveRole& rc = wa.role[0];
+          rc.in = bwd ? wb.fb : wb.ff;
+          rc.ng = NG;
+          rc.D = Dc;
+          rc.out = bwd ? wb.fw : wb.fb;
+          rc.out2 = bwd ? wb.sw : nullptr;
+          rc.ngo = bwd ? 5 : NG;
+          rc.po = bwd ? 0 : 2 + 2 * NV + 8;
+          const long long hrows = (long long)sk.T + 2 * HPAD;
+          rc.hand = wb.hand + (bwd ? (long long)sk.nstrip * hrows * NV : 0);
+          rc.ticket = wb.prog;
+          wa.role[1] = rc;
+          const size_t smem = wave_role_smem(Dc, WK, NG, NV);
+          auto kfn = bwd ? k_wave2d<NSB, true, false> : k_wave2d<NSB, false, false>;
+          cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          cudaMemsetAsync(wb.prog, 0, sizeof(int) * 2, st);
+          kfn<<<sk.nstrip, 96, smem, st>>>(wa);
+          if (ev) cudaEventRecord(ev[2 + pass], st);
+        }
+        const int CE = 16;
+        const size_t esm = (size_t)(5 + ns) * CE * 32 * sizeof(double);
+        cudaFuncSetAttribute(k_epilogue2d<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
+        k_epilogue2d<NSB><<<sk.nstrip * (sk.T / CE), 256, esm, st>>>(mp, g, sk, scheme, q, wb.fw,
+                                                                     wb.sw, qn, dq_std, CE, flags);
+        if (ev) cudaEventRecord(ev[4], st);
+        return cudaGetLastError();
+      }
+    }
     const int nsI = per_species ? NSB : 1;
     const Skew& sk = wb.sk;
     const int NSF = nsI + NSB + 2;
@@ -826,10 +1083,11 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     };
     while (C > 1 && rsm_of(C) > 200 * 1024) C /= 2;
     const size_t rsm = rsm_of(C);
-    cudaFuncSetAttribute(k_records2d<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+    cudaFuncSetAttribute(k_records2d<NSB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)rsm);
     const int ncb = sk.T / C;
     if (ev) cudaEventRecord(ev[0], st);
-    k_records2d<NSB><<<sk.nstrip * ncb, 256, rsm, st>>>(mp, g, sk, q, R, cfl, lamS, domd,
+    k_records2d<NSB, false><<<sk.nstrip * ncb, 256, rsm, st>>>(mp, g, sk, q, R, cfl, lamS, domd,
                                                         dom_stride, per_species, sp_scale, wb, C,
                                                         flags);
     if (ev) cudaEventRecord(ev[1], st);
@@ -842,6 +1100,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       wa.nj = g.nj;
       wa.nsI = nsI;
       wa.only = -1;
+      wa.ci = 0;
       wa.poll_ns = 16;
       if (const char* ev_p = getenv("CSB_POLL_NS")) wa.poll_ns = atoi(ev_p);  // tuning probe
       if (const char* ev_o = getenv("CSB_WAVE_ONLY")) wa.only = atoi(ev_o);  // timing probe

@@ -182,7 +182,7 @@ def _wave_vs_generic(spec, scheme, tol=1e-10):
 
 
 @pytest.mark.parametrize("dims", [(64, 64, 1), (40, 45, 1), (3, 70, 1), (50, 7, 1), (33, 96, 1)])
-@pytest.mark.parametrize("scheme", ["CS1", "CS2"])
+@pytest.mark.parametrize("scheme", ["CS1", "CS2", "CI"])
 def test_wavefront_matches_generic_box(dims, scheme):
     from paper_2403_03440_b200 import configs as C
     _wave_vs_generic(C.config0(seed=7, dims=dims), scheme)
@@ -193,6 +193,9 @@ def test_wavefront_matches_generic_ogrid_and_chemistry():
     _wave_vs_generic(C.config2(seed=2, dims=(48, 40, 1)), "CS1")
     _wave_vs_generic(C.config3(20, dims=(24, 40, 1), chemistry=True), "CS1")
     _wave_vs_generic(C.config3(40, dims=(24, 36, 1)), "CS2")
+    # the coupled operator on the wavefront (frozen, ns <= 16)
+    _wave_vs_generic(C.config2(seed=2, dims=(48, 40, 1)), "CI")
+    _wave_vs_generic(C.config3(11, dims=(40, 70, 1)), "CI")
 
 
 # ---------------------------------------------------------------- fused iteration (bench path)
