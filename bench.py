@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--config", type=int, default=1)
     p.add_argument("--scheme", default="CS1", choices=["CS1", "CS2", "CI"])
     p.add_argument("--no-extras", action="store_true", help="skip coupled/e2e/cpu legs")
+    p.add_argument("--no-scan", action="store_true", help="skip the config-3 species scan")
     return p.parse_args()
 
 
@@ -327,6 +328,31 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- species scan
+def species_scan(flush, nss=(5, 11, 20, 40), dims=(1024, 1024, 1), K=3, W=2):
+    """Config 3 (BASELINE.json): split (CS1) vs coupled (CI) implicit
+    iterations per ns on a 1024^2 box, frozen chemistry, synthetic species
+    and states from seed.  Same per-step protocol as the headline (L2 flushed,
+    CUDA events)."""
+    import torch
+    from paper_2403_03440_b200 import configs as C
+    out = []
+    for ns in nss:
+        spec = C.config3(ns, dims=dims)
+        run = Runner(spec, "CS1")
+        cs_ms, _ = timed_steps(run, K, W, flush)
+        ci_ms, _ = timed_steps(run, K, W, flush, scheme=0)
+        run.eng.status()
+        N = run.eng.N
+        out.append({"ns": ns, "split_CS1": N * K / (cs_ms * 1e-3),
+                    "coupled_CI": N * K / (ci_ms * 1e-3),
+                    "coupled_path": "wavefront" if ns <= 16 else "hyperplane (ns > 16)"})
+        del run
+        torch.cuda.empty_cache()
+    return {"unit": UNIT, "grid": "x".join(map(str, dims)), "chemistry": "frozen",
+            "steps": K, "results": out}
+
+
 # ---------------------------------------------------------------- replicas
 def replica_aggregate(local_ms, cells_per_rank, steps, dist=None, device="cpu"):
     """Whole-job throughput of N independent replicas: the timed region's
@@ -389,6 +415,11 @@ def main():
         extras["coupled_CI"] = {"value": N * max(3, args.steps // 2) / (ci_ms * 1e-3), "unit": UNIT}
         run.eng.status()
         e2e_ms, h2d, d2h = e2e_steps(run, args.steps, max(1, args.warmup // 2))
+        if not args.no_scan:
+            try:
+                extras["species_scan"] = species_scan(flush)
+            except Exception as exc:  # the scan must not kill the headline line
+                extras["species_scan"] = {"error": repr(exc)}
         e2e = {"value": world * N * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
         run.eng.status()
