@@ -54,6 +54,6 @@ if __name__ == "__main__":
     shapes = list(zip(args[0::2], args[1::2])) if args else [
         (512, 32), (2048, 32), (512, 64), (512, 128), (512, 256), (512, 512), (1024, 1024)]
     for ni, nj in shapes:
-        probe(ni, nj)
+        probe(ni, nj, ns=int(os.environ.get("NS", 5)))
     if not args:
         probe(512, 512, ns=11)

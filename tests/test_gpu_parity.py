@@ -233,3 +233,36 @@ def test_fused_iteration_matches_stages_and_oracle(dims):
     th, og, obcs, omech = spec_oracle(spec)
     on = np.array(O.norms(O.residual(spec.q, og, obcs, omech, th)))
     assert np.max(np.abs(n_fused - on) / np.abs(on)) <= 1e-10
+
+
+# ---------------------------------------------------------------- steady march (driver)
+
+def _march_case(name):
+    from paper_2403_03440_b200.driver import Case
+    from paper_2403_03440_b200.mixture import make_primitive
+    grid, model, bcs, mech, q0, cfl = golden_product(name)
+    Y = np.full(2, 0.5)
+    chill = make_primitive(model, rho=1.0, T=250.0, Y=Y)
+    inf = make_primitive(model, rho=1.0, T=250.0, u=(2.0 * float(chill.c), 0.0, 0.0), Y=Y)
+    ramp = tuple(float(v) for v in get(name, "ramp"))
+    case = Case(grid=grid, model=model, bcs=bcs, freestream=inf, mech=mech, scheme=name[6:],
+                cfl=20.0, cfl_ramp=(ramp[0], ramp[1], int(ramp[2])), max_iters=60,
+                residual_drop_orders=np.inf, stop_on_absolute_floor=False)
+    return case, q0
+
+
+@pytest.mark.parametrize("name", ["march_CS1", "march_CI"])
+def test_steady_march_matches_reference_history(name):
+    """steady_solve (driver.py:266-317) over the reference's cylinder case
+    (test_driver.py:108-123, 60 iterations with the CFL ramp): residual
+    histories to plotting precision, CFL schedule exactly, final state."""
+    from paper_2403_03440_b200.driver import steady_solve
+    case, q0 = _march_case(name)
+    q, hist = steady_solve(case, q0)
+    assert hist.reason == "max_iters" and len(hist.iters) == 60
+    assert np.array_equal(np.asarray(hist.cfl), get(name, "cfl_used"))
+    for key in ("res_flow", "res_species", "res_density"):
+        got, ref = np.asarray(getattr(hist, key)), get(name, key)
+        assert got.shape == ref.shape
+        assert np.max(np.abs(np.log10(got) - np.log10(ref))) <= 1e-9, key
+    assert comp_relerr(q, get(name, "q_final")) <= 1e-9
