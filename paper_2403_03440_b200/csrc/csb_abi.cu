@@ -36,6 +36,8 @@ struct csb_ctx {
   double *dtau = nullptr, *R = nullptr, *dq = nullptr, *partial = nullptr, *norms = nullptr;
   double* dom_scratch = nullptr;
   double* norm_partial = nullptr;
+  double* fm_buf[2] = {nullptr, nullptr};  // static 2-D face metrics (workspace)
+  bool fm_dirty = true;
   unsigned int* norm_counter = nullptr;
   int npart_cap = 0;
   int assembled_scheme = -1;
@@ -174,6 +176,10 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
   c->npart_cap = (int)std::max<long long>(4096, N / 64 + 1);
   c->norm_partial = k.take<double>((size_t)3 * c->npart_cap);
   c->norm_counter = k.take<unsigned int>(64);
+  if (c->g.nk == 1) {
+    c->fm_buf[0] = k.take<double>((size_t)6 * c->g.NF[0]);
+    c->fm_buf[1] = k.take<double>((size_t)6 * c->g.NF[1]);
+  }
   c->norms = k.take<double>(4);
   // 2-D wavefront path buffers (csb_wave.cuh): strip-skewed planes
   c->wave_ok = false;
@@ -216,6 +222,21 @@ int zero_wave_records(csb_ctx* c, cudaStream_t st) {
         cudaSuccess)
       return 1;
   return 0;
+}
+
+// The K2D residual reads precomputed static face metrics (recomputed after a
+// grid change); without them it evaluates the metrics on the fly.
+int ensure_face_metrics(csb_ctx* c, cudaStream_t st) {
+  if (!c->fm_dirty) return CSB_OK;
+  c->g.fm[0] = c->g.fm[1] = nullptr;
+  if (c->g.nk == 1 && c->geom2d_ok && c->fm_buf[0]) {
+    cudaError_t e = launch_face_metrics2d(c->g, c->fm_buf[0], c->fm_buf[1], st);
+    if (e != cudaSuccess) return cuda_check(c, e, "face metrics");
+    c->g.fm[0] = c->fm_buf[0];
+    c->g.fm[1] = c->fm_buf[1];
+  }
+  c->fm_dirty = false;
+  return CSB_OK;
 }
 
 int reset_flags(csb_ctx* c, cudaStream_t st) {
@@ -353,6 +374,7 @@ int csb_set_grid(csb_ctx* c, int ni, int nj, int nk, const double* Si, const dou
   g.vol = vol;
   c->g = g;
   c->has_grid = true;
+  c->fm_dirty = true;
   if (changed) c->has_ws = false;
   c->geom2d_ok = 0;
   c->k2d_disabled = 0;
@@ -407,6 +429,7 @@ int csb_set_workspace(csb_ctx* c, void* dev, size_t bytes) {
   c->ws_bytes = bytes;
   c->has_ws = true;
   c->assembled_scheme = -1;
+  c->fm_dirty = true;
   if (cudaMemset(c->norm_counter, 0, 64 * sizeof(unsigned int)) != cudaSuccess)
     return fail(c, CSB_E_CUDA, "zero norm counter");
   if (c->wave_ok) {
@@ -448,6 +471,7 @@ int csb_residual(csb_ctx* c, const double* q, double* R, double* P, int first_or
   if ((r = check_bcs(c))) return r;
   if ((r = sync_fs(c))) return r;
   cudaStream_t st = S(stream);
+  if ((r = ensure_face_metrics(c, st))) return r;
   const bool k2d = use_k2d(c);
   cudaError_t e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
                                   k2d, c->flags, st);
@@ -729,6 +753,7 @@ int csb_iteration(csb_ctx* c, const double* q, double cfl, int scheme, int offdi
   if ((r = check_bcs(c))) return r;
   if ((r = sync_fs(c))) return r;
   cudaStream_t st = S(stream);
+  if ((r = ensure_face_metrics(c, st))) return r;
   double* R = R_out ? R_out : c->R;
   bool fused = false;
   cudaError_t e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,

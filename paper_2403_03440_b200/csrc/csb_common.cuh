@@ -69,6 +69,7 @@ struct GridDev {
   const double* S[3];   // SoA face vectors, S[d][x*NF_d + f]
   long long NF[3];
   const double* vol;
+  const double* fm[2];  // 2-D viscous face metrics [6][NF_d] (xn, xt), or null
 };
 
 enum BcKind : int { BC_FARFIELD = 0, BC_OUTFLOW = 1, BC_WALL = 2, BC_SYMMETRY = 3, BC_PERIODIC = 4 };
@@ -97,6 +98,44 @@ CSB_DEV void load_S(const GridDev& g, int d, long long f, double S[3]) {
   S[0] = __ldg(p + f);
   S[1] = __ldg(p + nf + f);
   S[2] = __ldg(p + 2 * nf + f);
+}
+
+// Metric terms of a 2-D face of direction D at global face (gi, gj):
+// xn = S / Vf, xt = face average of the tangential axis' cell-averaged
+// Sc * J (spatial.py:236-248).
+template <int D>
+CSB_DEV void face_metric2d(const GridDev& g, int gi, int gj, const double S[3], double xn[3],
+                           double xt[3], bool& hasm, bool& hasp, long long& cellm,
+                           long long& cellp) {
+  constexpr int A = 1 - D;  // tangential in-plane axis
+  const int nd = D == 0 ? g.ni : g.nj;
+  const int pos = D == 0 ? gi : gj;
+  const int mi = D == 0 ? gi - 1 : gi, mj = D == 0 ? gj : gj - 1;
+  hasm = pos > 0;
+  hasp = pos < nd;
+  cellm = hasm ? cell_index(g, mi, mj, 0) : -1;
+  cellp = hasp ? cell_index(g, gi, gj, 0) : -1;
+  const double Vm = hasm ? __ldg(g.vol + cellm) : 0.0;
+  const double Vp = hasp ? __ldg(g.vol + cellp) : 0.0;
+  const double Vf = (hasm && hasp) ? 0.5 * (Vp + Vm) : (hasm ? Vm : Vp);
+#pragma unroll
+  for (int x = 0; x < 3; ++x) xn[x] = S[x] / Vf;
+  double xc[2][3];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const bool has = side == 0 ? hasm : hasp;
+    if (!has) continue;
+    const int ci = side == 0 ? mi : gi, cj = side == 0 ? mj : gj;
+    double Slo[3], Shi[3];
+    load_S(g, A, face_index(g, A, ci, cj, 0), Slo);
+    load_S(g, A, face_index(g, A, ci + (A == 0), cj + (A == 1), 0), Shi);
+    const double J = 1.0 / (side == 0 ? Vm : Vp);
+#pragma unroll
+    for (int x = 0; x < 3; ++x) xc[side][x] = (0.5 * (Slo[x] + Shi[x])) * J;
+  }
+#pragma unroll
+  for (int x = 0; x < 3; ++x)
+    xt[x] = (hasm && hasp) ? 0.5 * (xc[1][x] + xc[0][x]) : (hasm ? xc[0][x] : xc[1][x]);
 }
 
 // numpy.maximum: NaN-propagating

@@ -186,4 +186,33 @@ cudaError_t launch_check_2d(const GridDev& g, int* ok, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Static 2-D viscous face metrics (spatial.py:236-248): xn = S / Vf and the
+// face-averaged tangential Sc * J, once per grid.
+template <int D>
+__global__ void k_face_metrics2d(GridDev g, double* fm) {
+  const int fx = g.ni + (D == 0), fy = g.nj + (D == 1);
+  const long long nf = g.NF[D];
+  for (long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x; f < (long long)fx * fy;
+       f += (long long)gridDim.x * blockDim.x) {
+    const int gi = (int)(f / fy), gj = (int)(f % fy);
+    double S[3], xn[3], xt[3];
+    const long long fidx = face_index(g, D, gi, gj, 0);
+    load_S(g, D, fidx, S);
+    bool hasm, hasp;
+    long long cm, cp;
+    face_metric2d<D>(g, gi, gj, S, xn, xt, hasm, hasp, cm, cp);
+    for (int x = 0; x < 3; ++x) {
+      fm[x * nf + fidx] = xn[x];
+      fm[(3 + x) * nf + fidx] = xt[x];
+    }
+  }
+}
+
+cudaError_t launch_face_metrics2d(const GridDev& g, double* fm0, double* fm1, cudaStream_t st) {
+  note_launches(2);
+  k_face_metrics2d<0><<<grid_for(g.NF[0], 256), 256, 0, st>>>(g, fm0);
+  k_face_metrics2d<1><<<grid_for(g.NF[1], 256), 256, 0, st>>>(g, fm1);
+  return cudaGetLastError();
+}
+
 }  // namespace csb

@@ -463,44 +463,6 @@ CSB_DEV bool face_visc2d(const Model& m, const double* sP, int ldP, int im, int 
   return ok;
 }
 
-// Metric terms of a 2-D face of direction D at global face (gi, gj):
-// xn = S / Vf, xt = face average of the tangential axis' cell-averaged
-// Sc * J (spatial.py:236-248).
-template <int D>
-CSB_DEV void face_metric2d(const GridDev& g, int gi, int gj, const double S[3], double xn[3],
-                           double xt[3], bool& hasm, bool& hasp, long long& cellm,
-                           long long& cellp) {
-  constexpr int A = 1 - D;  // tangential in-plane axis
-  const int nd = D == 0 ? g.ni : g.nj;
-  const int pos = D == 0 ? gi : gj;
-  const int mi = D == 0 ? gi - 1 : gi, mj = D == 0 ? gj : gj - 1;
-  hasm = pos > 0;
-  hasp = pos < nd;
-  cellm = hasm ? cell_index(g, mi, mj, 0) : -1;
-  cellp = hasp ? cell_index(g, gi, gj, 0) : -1;
-  const double Vm = hasm ? __ldg(g.vol + cellm) : 0.0;
-  const double Vp = hasp ? __ldg(g.vol + cellp) : 0.0;
-  const double Vf = (hasm && hasp) ? 0.5 * (Vp + Vm) : (hasm ? Vm : Vp);
-#pragma unroll
-  for (int x = 0; x < 3; ++x) xn[x] = S[x] / Vf;
-  double xc[2][3];
-#pragma unroll
-  for (int side = 0; side < 2; ++side) {
-    const bool has = side == 0 ? hasm : hasp;
-    if (!has) continue;
-    const int ci = side == 0 ? mi : gi, cj = side == 0 ? mj : gj;
-    double Slo[3], Shi[3];
-    load_S(g, A, face_index(g, A, ci, cj, 0), Slo);
-    load_S(g, A, face_index(g, A, ci + (A == 0), cj + (A == 1), 0), Shi);
-    const double J = 1.0 / (side == 0 ? Vm : Vp);
-#pragma unroll
-    for (int x = 0; x < 3; ++x) xc[side][x] = (0.5 * (Slo[x] + Shi[x])) * J;
-  }
-#pragma unroll
-  for (int x = 0; x < 3; ++x)
-    xt[x] = (hasm && hasp) ? 0.5 * (xc[1][x] + xc[0][x]) : (hasm ? xc[0][x] : xc[1][x]);
-}
-
 template <int NSB, int D>
 CSB_DEV void visc_pass2d(const Model& m, const GridDev& g, const double* sP, int ldP, double* sF,
                          int maxf, int i0, int j0, int ci, int cj, int BY,
@@ -514,10 +476,27 @@ CSB_DEV void visc_pass2d(const Model& m, const GridDev& g, const double* sP, int
     const int im = ip - sd;
     const int gi = i0 + fi, gj = j0 + fj;
     double S[3], xn[3], xt[3];
-    load_S(g, D, face_index(g, D, gi, gj, 0), S);
+    const long long fidx = face_index(g, D, gi, gj, 0);
+    load_S(g, D, fidx, S);
     bool hasm, hasp;
     long long cellm, cellp;
-    face_metric2d<D>(g, gi, gj, S, xn, xt, hasm, hasp, cellm, cellp);
+    if (g.fm[D]) {
+      // static metric terms, precomputed once per grid (k_face_metrics2d)
+      const double* fm = g.fm[D] + fidx;
+      const long long nf = g.NF[D];
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        xn[x] = __ldg(fm + x * nf);
+        xt[x] = __ldg(fm + (3 + x) * nf);
+      }
+      const int nd = D == 0 ? g.ni : g.nj, pos = D == 0 ? gi : gj;
+      hasm = pos > 0;
+      hasp = pos < nd;
+      cellm = hasm ? cell_index(g, D == 0 ? gi - 1 : gi, D == 0 ? gj : gj - 1, 0) : -1;
+      cellp = hasp ? cell_index(g, gi, gj, 0) : -1;
+    } else {
+      face_metric2d<D>(g, gi, gj, S, xn, xt, hasm, hasp, cellm, cellp);
+    }
     if (!face_visc2d<NSB, D>(m, sP, ldP, im, ip, st, S, xn, xt, sF + f, maxf))
       raise_flag(flags, EB_FACE_T, hasp ? cellp : cellm);
   }
