@@ -289,6 +289,7 @@ int csb_set_model(csb_ctx* c, int ns, const double* M, const double* cp, const d
     m.T_mu[s] = T_mu[s];
     m.S_mu[s] = S_mu[s];
     m.TS[s] = T_mu[s] + S_mu[s];
+    m.inv_T_mu[s] = 1.0 / T_mu[s];
   }
   if (!c->d_model && cudaMalloc(&c->d_model, sizeof(Model)) != cudaSuccess)
     return fail(c, CSB_E_CUDA, "cudaMalloc(model)");

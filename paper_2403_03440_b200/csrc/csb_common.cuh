@@ -42,7 +42,11 @@ struct Model {
   double Pr, Sc;
   double M[MAXNS], cp[MAXNS], Rs[MAXNS], bs[MAXNS];
   double mu_ref[MAXNS], T_mu[MAXNS], S_mu[MAXNS], TS[MAXNS];  // TS = T_mu + S_mu
+  double inv_T_mu[MAXNS];                                      // 1 / T_mu
 };
+// the per-species arrays of Model, contiguous from M (copied per block by
+// the residual kernel, first ns entries of each)
+constexpr int MODEL_NARR = 9;
 
 // Reactions in the reference's order; stoichiometry kept as (species, nu)
 // pairs in ascending species order (chemistry.py:56-62 iterates np.nonzero).
@@ -161,7 +165,7 @@ CSB_DEV void raise_flag(unsigned long long* fl, int bit, long long cell) {
 
 // Sutherland viscosity of species s (mixture.py:368); (T/T_mu)^1.5 as x*sqrt(x)
 CSB_DEV double mu_species(const Model& m, int s, double T) {
-  const double x = T / m.T_mu[s];
+  const double x = T * m.inv_T_mu[s];
   return m.mu_ref[s] * (x * sqrt(x)) * m.TS[s] / (T + m.S_mu[s]);
 }
 
@@ -178,15 +182,16 @@ CSB_DEV bool decode(const Model& m, const double* __restrict__ q, long long stri
   const int ns = m.ns;
   const double rho = q[0];
   bool ok = (rho > 0.0) && finite(rho);
-  const double ir = rho;
+  // reciprocal multiplies instead of divisions (last-ulp differences only)
+  const double ir = 1.0 / rho;
   o.rho = rho;
 #pragma unroll
-  for (int x = 0; x < 3; ++x) o.u[x] = q[(1 + x) * stride] / ir;
+  for (int x = 0; x < 3; ++x) o.u[x] = q[(1 + x) * stride] * ir;
   double sum = 0.0;
 #pragma unroll
   for (int s = 0; s < NSB; ++s) {
     if (s < ns) {
-      double y = q[(5 + s) * stride] / ir;
+      double y = q[(5 + s) * stride] * ir;
       if (y < -EPS_NEG) ok = false;
       if (y < 0.0) y = 0.0;
       o.Y[s] = y;
@@ -196,10 +201,11 @@ CSB_DEV bool decode(const Model& m, const double* __restrict__ q, long long stri
     }
   }
   double R = 0.0, cp = 0.0, yb = 0.0;
+  const double isum = 1.0 / sum;
 #pragma unroll
   for (int s = 0; s < NSB; ++s) {
     if (s < ns) {
-      const double y = o.Y[s] / sum;
+      const double y = o.Y[s] * isum;
       o.Y[s] = y;
       R += y * m.Rs[s];
       cp += y * m.cp[s];
@@ -208,13 +214,14 @@ CSB_DEV bool decode(const Model& m, const double* __restrict__ q, long long stri
   }
   o.Ek = 0.5 * ((o.u[0] * o.u[0] + o.u[1] * o.u[1]) + o.u[2] * o.u[2]);
   const double cv = cp - R;
-  const double e_int = q[4 * stride] / rho - o.Ek;
-  o.T = (e_int - yb) / cv;
+  const double icv = 1.0 / cv;
+  const double e_int = q[4 * stride] * ir - o.Ek;
+  o.T = (e_int - yb) * icv;
   if (!(o.T > 0.0) || !finite(o.T)) ok = false;
   o.R = R;
   o.cp = cp;
   o.p = rho * R * o.T;
-  o.gamma = cp / cv;
+  o.gamma = cp * icv;
   o.c = sqrt(o.gamma * R * o.T);
   o.h = yb + cp * o.T + o.Ek;
   return ok;

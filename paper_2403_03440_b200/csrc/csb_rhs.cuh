@@ -551,14 +551,23 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
                                                   Mech mech, const double* __restrict__ q,
                                                   double* __restrict__ R, int first_order, int TI,
                                                   int TJ, int TK, unsigned long long* flags,
-                                                  NormsOut nrm) {
+                                                  NormsOut nrm, int sr_on) {
   extern __shared__ double smem[];
   __shared__ Model sm;
   {
+    // header + the first ns entries of each per-species array (a full copy
+    // of the ~5 KB table per block cost ~12% of the kernel)
+    static_assert(offsetof(Model, M) % sizeof(double) == 0, "Model layout");
+    static_assert(offsetof(Model, inv_T_mu) == offsetof(Model, M) + 8 * MAXNS * sizeof(double),
+                  "Model arrays contiguous");
     const double* src = reinterpret_cast<const double*>(mp);
     double* dst = reinterpret_cast<double*>(&sm);
-    for (int i = threadIdx.x; i < (int)(sizeof(Model) / sizeof(double)); i += blockDim.x)
-      dst[i] = src[i];
+    const int h = (int)(offsetof(Model, M) / sizeof(double));
+    const int nsm = __ldg(&mp->ns);
+    for (int i = threadIdx.x; i < h + MODEL_NARR * nsm; i += blockDim.x) {
+      const int w = i < h ? i : h + ((i - h) / nsm) * MAXNS + (i - h) % nsm;
+      dst[w] = __ldg(src + w);
+    }
   }
   __syncthreads();
   const Model& m = sm;
@@ -578,6 +587,8 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
   double* sP = smem;
   const int maxf = max(max((TI + 1) * TJ * TK, TI * (TJ + 1) * TK), TI * TJ * (K2D ? 1 : TK + 1));
   double* sF = smem + (long long)nc * ldP;
+  // partial residual of the tile, sum over directions in order (0 + dR_0 + ...)
+  double* sR = sF + (long long)nv * maxf;
 
   // ---- stage decoded primitives + halo (padded coordinates = interior + NG)
   for (int l = threadIdx.x; l < ldP; l += blockDim.x) {
@@ -728,7 +739,7 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
       }
       for (int c = 0; c < nv; ++c) {
         const double dR = sF[c * maxf + fhi] - sF[c * maxf + flo];
-        double* r = R + (long long)c * g.N + cell;
+        double* r = sr_on ? sR + c * ncell + l : R + (long long)c * g.N + cell;
         if (d == 0) *r = dR;
         else *r = *r + dR;
       }
@@ -755,7 +766,7 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
 #pragma unroll
       for (int s = 0; s < NSB; ++s)
         if (s < ns) {
-          double* r = R + (long long)(5 + s) * g.N + cell;
+          double* r = sr_on ? sR + (5 + s) * ncell + l : R + (long long)(5 + s) * g.N + cell;
           *r = *r - om[s] * V;
         }
     }
@@ -764,7 +775,12 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
 #pragma unroll
     for (int c = 0; c < 5 + NSB; ++c)
       if (c < nv) {
-        rv[c] = R[(long long)c * g.N + cell];
+        if (sr_on) {
+          rv[c] = sR[c * ncell + l];
+          R[(long long)c * g.N + cell] = rv[c];
+        } else {
+          rv[c] = R[(long long)c * g.N + cell];
+        }
         fin &= finite(rv[c]);
       }
     if (!fin) raise_flag(flags, EB_RES_NONFINITE, cell);
@@ -884,12 +900,25 @@ static inline void pick_tile(int ns, bool k2d, int nk, int& TI, int& TJ, int& TK
   }
 }
 
+// Accumulate the tile's residual in shared memory (one global write per
+// component) when the extra TI*TJ*TK*nv doubles do not cost occupancy
+// (2 CTAs/SM under the 128-register bound up to ~104 KB of dynamic smem each).
+static inline bool residual_in_smem(size_t smem, int cells, int nv, size_t& total) {
+  total = smem + (size_t)cells * nv * sizeof(double);
+  // per-SM budget 228 KB including ~5 KB of static shared memory per CTA
+  const size_t two = 104 * 1024, one = 200 * 1024;
+  return smem <= two ? total <= two : total <= one;
+}
+
 cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                             const Mech& mech, const double* q, double* R, int first_order, bool k2d,
                             unsigned long long* flags, cudaStream_t st, NormsOut nrm, bool* fused) {
   int TI, TJ, TK;
   size_t smem;
   pick_tile(ns, k2d, g.nk, TI, TJ, TK, smem);
+  size_t smem_sr;
+  const int sr_on = residual_in_smem(smem, TI * TJ * TK, 5 + ns, smem_sr) ? 1 : 0;
+  if (sr_on) smem = smem_sr;
   const long long ntiles = (long long)((g.ni + TI - 1) / TI) * ((g.nj + TJ - 1) / TJ) *
                            (k2d ? 1 : (g.nk + TK - 1) / TK);
   if (!(nrm.out && ntiles <= nrm.cap)) nrm.out = nullptr;
@@ -900,12 +929,12 @@ cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, c
       auto kfn = k_residual<NSB, true>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       kfn<<<(unsigned)ntiles, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
-                                               nrm);
+                                               nrm, sr_on);
     } else {
       auto kfn = k_residual<NSB, false>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       kfn<<<(unsigned)ntiles, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
-                                               nrm);
+                                               nrm, sr_on);
     }
     err = cudaGetLastError();
   });
