@@ -991,6 +991,14 @@ __global__ void __launch_bounds__(256, 2) k_epilogue2d(const Model* __restrict__
 }
 
 // ============================================================== launcher
+// epilogue tile length: the dq tile of (5 + ns) planes stays <= 48 KB so that
+// large species counts keep 4 CTAs per SM
+inline int epilogue_steps(int ns) {
+  int ce = 16;
+  while (ce > 2 && (size_t)(5 + ns) * ce * 32 * sizeof(double) > 48 * 1024) ce /= 2;
+  return ce;
+}
+
 inline size_t wave_role_smem(int D, int WK, int NG, int nh) {
   return ((size_t)D * WK * NG * 32 + (size_t)(HRING + WK) * nh) * sizeof(double);
 }
@@ -1060,7 +1068,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
           kfn<<<sk.nstrip, 96, smem, st>>>(wa);
           if (ev) cudaEventRecord(ev[2 + pass], st);
         }
-        const int CE = 16;
+        const int CE = epilogue_steps(ns);
         const size_t esm = (size_t)(5 + ns) * CE * 32 * sizeof(double);
         cudaFuncSetAttribute(k_epilogue2d<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
         k_epilogue2d<NSB><<<sk.nstrip * (sk.T / CE), 256, esm, st>>>(mp, g, sk, scheme, q, wb.fw,
@@ -1163,7 +1171,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       if (ev) cudaEventRecord(ev[2 + pass], st);
     }
     // ---------------- epilogue
-    const int CE = 16;
+    const int CE = epilogue_steps(ns);
     const size_t esm = (size_t)(5 + ns) * CE * 32 * sizeof(double);
     cudaFuncSetAttribute(k_epilogue2d<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
     k_epilogue2d<NSB><<<sk.nstrip * (sk.T / CE), 256, esm, st>>>(mp, g, sk, scheme, q, wb.fw,
