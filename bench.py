@@ -346,7 +346,8 @@ def species_scan(flush, nss=(5, 11, 20, 40), dims=(1024, 1024, 1), K=3, W=2):
         N = run.eng.N
         out.append({"ns": ns, "split_CS1": N * K / (cs_ms * 1e-3),
                     "coupled_CI": N * K / (ci_ms * 1e-3),
-                    "coupled_path": "wavefront" if ns <= 16 else "hyperplane (ns > 16)"})
+                    "coupled_path": "wavefront (register chain)" if ns <= 16
+                    else "wavefront (smem-resident chain, ns > 16)"})
         del run
         torch.cuda.empty_cache()
     return {"unit": UNIT, "grid": "x".join(map(str, dims)), "chemistry": "frozen",

@@ -663,8 +663,8 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
   const bool chem = mech_of(c).nrx > 0;
   const bool full = chem && scheme == SCH_CI;
   if (full && !c->ws_block) return fail(c, CSB_E_STATE, "CI with chemistry needs block workspace");
-  // the coupled operator takes the wavefront path when frozen and ns <= 16
-  const bool ci_wave = scheme != SCH_CI || (!chem && bucket_of(c->ns) <= 16);
+  // the coupled operator takes the wavefront path when frozen
+  const bool ci_wave = scheme != SCH_CI || !chem;
   const bool wave = path != 1 && c->wave_ok && !c->wave_disabled && ci_wave && c->geom2d_ok;
   if (path == 2 && !wave) return fail(c, CSB_E_STATE, "2-D wavefront path not applicable");
   if (wave) {

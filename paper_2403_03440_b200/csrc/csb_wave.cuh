@@ -66,7 +66,7 @@ constexpr int ci_wk() {
   while (w > 1 && w * ci_planes<NSB>() * 256 > 64 * 1024) w /= 2;
   return w;
 }
-constexpr int CI_MAXNSB = 16;  // larger species counts use the generic CI path
+constexpr int CI_MAXNSB = 16;  // register-resident CI chain up to here; smem-resident above
 
 // species slot length: <= 64 KiB per slot at the widest layout (nsI = NSB)
 template <int NSB>
@@ -713,6 +713,93 @@ CSB_DEV void chain_ci(const ChainCtx& x, const WaveRole& ro) {
   }
 }
 
+// coupled chain for large species counts (NSB > CI_MAXNSB): the same
+// arithmetic as chain_ci with the per-row state in shared memory -- oi, the
+// double-buffered oj (read by the neighbouring row instead of a shuffle) and
+// dq -- laid out [component][lane].
+template <int NSB, bool BWD>
+CSB_DEV void chain_ci_big(const ChainCtx& x, const WaveRole& ro, double* st) {
+  constexpr int NV = 5 + NSB, NG = ci_planes<NSB>(), WK = ci_wk<NSB>();
+  constexpr int PV = BWD ? 2 + 2 * NV + 8 : 2 + 2 * NV;
+  constexpr int FQ = BWD ? 2 + 2 * NV : 2 + 3 * NV;
+  constexpr int NGO = BWD ? 5 : NG, PO = BWD ? 0 : 2 + 2 * NV + 8;
+  const int lane = threadIdx.x & 31;
+  const int nbr = BWD ? min(lane + 1, 31) : max(lane - 1, 0);  // j-neighbour row's lane
+  const WaveArgs& a = *x.a;
+  const long long slot = (long long)WK * NG * 32;
+  double* soi = st;                 // [NV][32]
+  double* soj = st + NV * 32;       // [2][NV][32]
+  double* sdq = st + 3 * NV * 32;   // [NV][32]
+  for (int c = 0; c < NV; ++c) soi[c * 32 + lane] = soj[c * 32 + lane] = soj[(NV + c) * 32 + lane] = 0.0;
+  __syncwarp();
+  int cur = 0;
+  int buf = 0, phase = 0;
+  for (int ks = 0; ks < x.nslots; ++ks) {
+    const int k = BWD ? x.nslots - 1 - ks : ks;
+    mbar_wait(&x.full_bar[buf], phase);
+    const double* base = x.ring + buf * slot + lane;
+    const long long st0 = (long long)x.s * a.sk.T + (long long)k * WK;
+    double* ob = ro.out + (st0 * NGO + PO) * 32 + lane;
+    double* ob2 = BWD ? ro.out2 + st0 * NSB * 32 + lane : nullptr;
+    const double* hb = x.recv ? x.hin + ((k * WK) % HRING) * NV : x.hin + HRING * NV;
+    double* ho = x.hand_out + (long long)k * WK * NV;
+    for (int m = 0; m < WK; ++m) {
+      const int kk = BWD ? WK - 1 - m : m;
+      const double* p = base + kk * NG * 32;
+      const double* hv = hb + kk * NV;
+      const double* ojp = soj + cur * NV * 32;      // previous step's products
+      double* ojn = soj + (cur ^ 1) * NV * 32;      // this step's
+      const double invd = p[0], hr2 = p[32];
+      double sb0 = 0.0, sb1 = 0.0, dq0 = 0.0, dq1 = 0.0, dq2 = 0.0;
+      for (int c = 0; c < NV; ++c) {
+        const double ij = fma(ojp[c * 32 + nbr], x.mul, hv[c]);
+        const double oic = soi[c * 32 + lane];
+        const double v = p[(PV + c) * 32];
+        const double dq = BWD ? v - (oic + ij) * invd : ((v + oic) + ij) * invd;
+        sdq[c * 32 + lane] = dq;
+        if (!BWD) ob[(kk * NGO + c) * 32] = dq;
+        else if (c < 5) ob[(kk * 5 + c) * 32] = dq;
+        else ob2[(kk * NSB + c - 5) * 32] = dq;
+        if (c & 1) sb1 = fma(p[(2 + NV + c) * 32], dq, sb1);
+        else sb0 = fma(p[(2 + NV + c) * 32], dq, sb0);
+        if (c == 0) dq0 = dq;
+        if (c == 1) dq1 = dq;
+        if (c == 2) dq2 = dq;
+      }
+      const double sb = sb0 + sb1;
+      double sa[2], e[2][3], sig[2];
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        const double* pf = p + (FQ + 4 * f) * 32;
+        e[f][0] = pf[0];
+        e[f][1] = pf[32];
+        e[f][2] = pf[64];
+        sig[f] = pf[96];
+        sa[f] = hr2 * ((e[f][0] * dq1 + e[f][1] * dq2) - e[f][2] * dq0);
+      }
+      for (int c = 0; c < NV; ++c) {
+        const double dq = sdq[c * 32 + lane];
+        const double wc = p[(2 + c) * 32];
+        const bool ev = c == 1 || c == 2 || c == 4;
+        const int ei = c == 1 ? 0 : c == 2 ? 1 : 2;
+        const double oi = ev ? wc * sa[0] + e[0][ei] * sb + sig[0] * dq : wc * sa[0] + sig[0] * dq;
+        const double oj = ev ? wc * sa[1] + e[1][ei] * sb + sig[1] * dq : wc * sa[1] + sig[1] * dq;
+        soi[c * 32 + lane] = oi;
+        ojn[c * 32 + lane] = oj;
+        st_pred_cg_f64(ho + kk * NV + c, oj, x.send);
+      }
+      __syncwarp();
+      cur ^= 1;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&x.empty_bar[buf]);
+    if (++buf == x.D) {
+      buf = 0;
+      phase ^= 1;
+    }
+  }
+}
+
 template <int NSB, bool BWD, bool PER>
 __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   extern __shared__ __align__(128) double wsm[];
@@ -863,7 +950,10 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   } else if (kind == 1) {
     chain_species<NSB, BWD, PER>(x, ro);
   } else {
-    if constexpr (NSB <= CI_MAXNSB && !PER) chain_ci<NSB, BWD>(x, ro);
+    if constexpr (!PER) {
+      if constexpr (NSB <= CI_MAXNSB) chain_ci<NSB, BWD>(x, ro);
+      else chain_ci_big<NSB, BWD>(x, ro, hin + (HRING + WK) * nh);
+    }
   }
   if (a.dbg && lane == 0) {
     unsigned long long t1;
@@ -1018,13 +1108,15 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
   CSB_NS_DISPATCH(ns, {
     if (scheme == SCH_CI) {
       // ---------------- coupled operator (frozen chemistry): one chain per strip
-      if constexpr (NSB > CI_MAXNSB) {
-        return cudaErrorInvalidConfiguration;
-      } else {
+      {
         if (per_species) return cudaErrorInvalidConfiguration;
         const Skew& sk = wb.sk;
         constexpr int NV = 5 + NSB, NG = ci_planes<NSB>(), WK = ci_wk<NSB>();
-        const int Dc = wave_depth(WK, NG, NV);
+        // large NSB: + the smem-resident chain state (4 x NV x 32 doubles)
+        const size_t extra = NSB > CI_MAXNSB ? (size_t)4 * NV * 32 * sizeof(double) : 0;
+        int Dc = 0;
+        for (int D = 4; D >= 2 && !Dc; --D)
+          if (wave_role_smem(D, WK, NG, NV) + extra <= 210 * 1024) Dc = D;
         if (!Dc) return cudaErrorInvalidConfiguration;
         int C = 4;
         auto rsm_of = [&](int c) {
@@ -1061,7 +1153,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
           rc.hand = wb.hand + (bwd ? (long long)sk.nstrip * hrows * NV : 0);
           rc.ticket = wb.prog;
           wa.role[1] = rc;
-          const size_t smem = wave_role_smem(Dc, WK, NG, NV);
+          const size_t smem = wave_role_smem(Dc, WK, NG, NV) + extra;
           auto kfn = bwd ? k_wave2d<NSB, true, false> : k_wave2d<NSB, false, false>;
           cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
           cudaMemsetAsync(wb.prog, 0, sizeof(int) * 2, st);

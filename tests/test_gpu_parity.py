@@ -196,6 +196,9 @@ def test_wavefront_matches_generic_ogrid_and_chemistry():
     # the coupled operator on the wavefront (frozen, ns <= 16)
     _wave_vs_generic(C.config2(seed=2, dims=(48, 40, 1)), "CI")
     _wave_vs_generic(C.config3(11, dims=(40, 70, 1)), "CI")
+    # large species counts: smem-resident coupled chain
+    _wave_vs_generic(C.config3(20, dims=(24, 40, 1)), "CI")
+    _wave_vs_generic(C.config3(40, dims=(30, 70, 1)), "CI")
 
 
 # ---------------------------------------------------------------- fused iteration (bench path)
