@@ -37,6 +37,7 @@ struct csb_ctx {
   double* dom_scratch = nullptr;
   double* norm_partial = nullptr;
   double* fm_buf[2] = {nullptr, nullptr};  // static 2-D face metrics (workspace)
+  double* cm_buf = nullptr;                // static cell metrics (workspace)
   bool fm_dirty = true;
   unsigned int* norm_counter = nullptr;
   int npart_cap = 0;
@@ -176,6 +177,7 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
   c->npart_cap = (int)std::max<long long>(4096, N / 64 + 1);
   c->norm_partial = k.take<double>((size_t)3 * c->npart_cap);
   c->norm_counter = k.take<unsigned int>(64);
+  c->cm_buf = k.take<double>((size_t)16 * N);
   if (c->g.nk == 1) {
     c->fm_buf[0] = k.take<double>((size_t)6 * c->g.NF[0]);
     c->fm_buf[1] = k.take<double>((size_t)6 * c->g.NF[1]);
@@ -229,6 +231,12 @@ int zero_wave_records(csb_ctx* c, cudaStream_t st) {
 int ensure_face_metrics(csb_ctx* c, cudaStream_t st) {
   if (!c->fm_dirty) return CSB_OK;
   c->g.fm[0] = c->g.fm[1] = nullptr;
+  c->g.cm = nullptr;
+  if (c->cm_buf) {
+    cudaError_t e = launch_cell_metrics(c->g, c->cm_buf, st);
+    if (e != cudaSuccess) return cuda_check(c, e, "cell metrics");
+    c->g.cm = c->cm_buf;
+  }
   if (c->g.nk == 1 && c->geom2d_ok && c->fm_buf[0]) {
     cudaError_t e = launch_face_metrics2d(c->g, c->fm_buf[0], c->fm_buf[1], st);
     if (e != cudaSuccess) return cuda_check(c, e, "face metrics");
@@ -660,6 +668,7 @@ int csb_residual_norms(csb_ctx* c, long long N, const double* R, double* out3, v
 static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cfl, int scheme,
                          int offdiag_paper, const double* dOm_in, double* q_new, cudaStream_t st,
                          int path = 0, double* dq_out = nullptr, cudaEvent_t* ev = nullptr) {
+  if (int r0 = ensure_face_metrics(c, st)) return r0;
   const bool chem = mech_of(c).nrx > 0;
   const bool full = chem && scheme == SCH_CI;
   if (full && !c->ws_block) return fail(c, CSB_E_STATE, "CI with chemistry needs block workspace");

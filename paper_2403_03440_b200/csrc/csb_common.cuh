@@ -74,6 +74,7 @@ struct GridDev {
   long long NF[3];
   const double* vol;
   const double* fm[2];  // 2-D viscous face metrics [6][NF_d] (xn, xt), or null
+  const double* cm;     // static cell metrics [16][N] (cell_metric), or null
 };
 
 enum BcKind : int { BC_FARFIELD = 0, BC_OUTFLOW = 1, BC_WALL = 2, BC_SYMMETRY = 3, BC_PERIODIC = 4 };
@@ -140,6 +141,32 @@ CSB_DEV void face_metric2d(const GridDev& g, int gi, int gj, const double S[3], 
 #pragma unroll
   for (int x = 0; x < 3; ++x)
     xt[x] = (hasm && hasp) ? 0.5 * (xc[1][x] + xc[0][x]) : (hasm ? xc[0][x] : xc[1][x]);
+}
+
+// Cell-averaged face vector of direction d (grid.py Sc_d), |Sc|^2 and |Sc|
+// (implicit.py:152-163), from the static table when present.  Table rows:
+// [5d + 0..2] Sc_d, [5d + 3] a2, [5d + 4] sqrt(a2), [15] 1 / V.
+CSB_DEV void cell_metric(const GridDev& g, long long c, int i, int j, int k, int d, double Sc[3],
+                         double& a2, double& sq) {
+  if (g.cm) {
+#pragma unroll
+    for (int x = 0; x < 3; ++x) Sc[x] = __ldg(g.cm + (5 * d + x) * g.N + c);
+    a2 = __ldg(g.cm + (5 * d + 3) * g.N + c);
+    sq = __ldg(g.cm + (5 * d + 4) * g.N + c);
+    return;
+  }
+  int hi[3] = {i, j, k};
+  hi[d] += 1;
+  double a[3], b[3];
+  load_S(g, d, face_index(g, d, i, j, k), a);
+  load_S(g, d, face_index(g, d, hi[0], hi[1], hi[2]), b);
+#pragma unroll
+  for (int x = 0; x < 3; ++x) Sc[x] = 0.5 * (a[x] + b[x]);
+  a2 = (Sc[0] * Sc[0] + Sc[1] * Sc[1]) + Sc[2] * Sc[2];
+  sq = sqrt(a2);
+}
+CSB_DEV double inv_volume(const GridDev& g, long long c) {
+  return g.cm ? __ldg(g.cm + 15 * g.N + c) : 1.0 / __ldg(g.vol + c);
 }
 
 // numpy.maximum: NaN-propagating

@@ -53,7 +53,7 @@ constexpr int HRING = 128;  // hand-off ring (steps)
 // signalling NaN marking a hand-off word not yet written (see the chains)
 constexpr unsigned long long HAND_SENTINEL = 0x7FF4DEADBEEF0001ull;
 constexpr int NFF = 30, NFB = 30, FB_DQ = 25;
-constexpr int WKF = 8;     // flow slot: 8 steps x 30 planes = 60 KiB
+constexpr int WKF = 8;     // flow slot: 8 steps x 30 planes = 60 KiB (measured: 4 is slower)
 
 // Coupled (CI, frozen chemistry) records, NV = 5 + NSB components:
 //   CF (forward)  invd, hr2, w[NV], b[NV], rhs[NV], upper faces (e[3], sig) x 2
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
     A[3 * NH + hl] = cs.c;
     A[4 * NH + hl] = nf;
     A[5 * NH + hl] = nsp;
-    A[6 * NH + hl] = V;
+    A[6 * NH + hl] = inv_volume(g, c);  // 1 / V (face radii multiply)
     A[7 * NH + hl] = 0.5 / cs.rho;
     const bool inner = tt >= 0 && tt < C && r >= 0 && r < 32;
     if (!inner) continue;
@@ -220,27 +220,20 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
     const int e = tt * 32 + r;  // tile element (tt, r)
     // cell radii at the cell-averaged metric, dtau (implicit.py:152-163, 33-44)
     double li[3], lv[3], rf = 0.0, rsp = 0.0;
+    const double iV = inv_volume(g, c);
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-      int hi[3] = {i, j, 0};
-      hi[d] += 1;
-      double a[3], b[3];
-      load_S(g, d, face_index(g, d, i, j, 0), a);
-      load_S(g, d, face_index(g, d, hi[0], hi[1], hi[2]), b);
-      double Sc[3];
-#pragma unroll
-      for (int x = 0; x < 3; ++x) Sc[x] = 0.5 * (a[x] + b[x]);
-      const double a2 = (Sc[0] * Sc[0] + Sc[1] * Sc[1]) + Sc[2] * Sc[2];
+      double Sc[3], a2, sq;
+      cell_metric(g, c, i, j, 0, d, Sc, a2, sq);
       const double U = fabs(cs.u[0] * Sc[0] + cs.u[1] * Sc[1] + cs.u[2] * Sc[2]);
-      const double sq = sqrt(a2);
       li[d] = U + cs.c * sq;
-      lv[d] = nu * a2 / V;
-      const double lf = (U + cs.c * sq) + 2.0 * nf * a2 / V;
-      const double ls = U + 2.0 * nsp * a2 / V;
+      lv[d] = nu * a2 * iV;
+      const double lf = (U + cs.c * sq) + 2.0 * nf * a2 * iV;
+      const double ls = U + 2.0 * nsp * a2 * iV;
       rf = d == 0 ? lf : rf + lf;
       rsp = d == 0 ? ls : rsp + ls;
     }
-    const double J = 1.0 / V;
+    const double J = iV;
     const double den = J * (((li[0] + li[1]) + li[2]) + ((lv[0] + lv[1]) + lv[2])) +
                        (lamS ? lamS[c] : 0.0);
     if (!(den > 0.0)) raise_flag(flags, EB_ZERO_WAVE, c);
@@ -251,17 +244,10 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
       double rci = 0.0;
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
-        int hi[3] = {i, j, 0};
-        hi[d] += 1;
-        double a[3], b[3];
-        load_S(g, d, face_index(g, d, i, j, 0), a);
-        load_S(g, d, face_index(g, d, hi[0], hi[1], hi[2]), b);
-        double Sc[3];
-#pragma unroll
-        for (int x = 0; x < 3; ++x) Sc[x] = 0.5 * (a[x] + b[x]);
-        const double a2 = (Sc[0] * Sc[0] + Sc[1] * Sc[1]) + Sc[2] * Sc[2];
+        double Sc[3], a2, sq;
+        cell_metric(g, c, i, j, 0, d, Sc, a2, sq);
         const double U = fabs(cs.u[0] * Sc[0] + cs.u[1] * Sc[1] + cs.u[2] * Sc[2]);
-        const double lu = (U + cs.c * sqrt(a2)) + 2.0 * nu * a2 / V;
+        const double lu = (U + cs.c * sq) + 2.0 * nu * a2 * iV;
         rci = d == 0 ? lu : rci + lu;
       }
       const double dci = base + rci;
@@ -368,7 +354,7 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
         auto lam = [&](int h) {
           const double Uh = fabs(A[0 * NH + h] * S[0] + A[1 * NH + h] * S[1] + A[2 * NH + h] * S[2]);
           const double nuh = npmax(A[4 * NH + h], A[5 * NH + h]);
-          return (Uh + A[3 * NH + h] * ar) + 2.0 * nuh * a2 / A[6 * NH + h];
+          return (Uh + A[3 * NH + h] * ar) + 2.0 * nuh * a2 * A[6 * NH + h];
         };
         const double lu = nb_in ? npmax(lam(lo), lam(hi)) : lam(hc);
         const double U = u * S[0] + v * S[1];
@@ -418,8 +404,8 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
       const int lo = upper ? hc : nb, hi = upper ? nb : hc;  // lower/upper cell of the face
       auto lam = [&](int h, bool sp) {
         const double U = fabs(A[0 * NH + h] * S[0] + A[1 * NH + h] * S[1] + A[2 * NH + h] * S[2]);
-        if (sp) return U + 2.0 * A[5 * NH + h] * a2 / A[6 * NH + h];
-        return (U + A[3 * NH + h] * ar) + 2.0 * A[4 * NH + h] * a2 / A[6 * NH + h];
+        if (sp) return U + 2.0 * A[5 * NH + h] * a2 * A[6 * NH + h];
+        return (U + A[3 * NH + h] * ar) + 2.0 * A[4 * NH + h] * a2 * A[6 * NH + h];
       };
       double lf, ls;
       if (nb_in) {
