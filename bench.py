@@ -146,13 +146,15 @@ class Runner:
         self.stream = ctypes.c_void_p(eng.stream)
         torch.cuda.synchronize()
 
-    def step(self, q=None, qn=None, scheme=None):
+    def step(self, q=None, qn=None, scheme=None, norms=None):
         e = self.eng
         rc = self.lib.csb_iteration(e.ctx, (q if q is not None else self.q).data_ptr(),
                                     float(self.spec.cfl),
                                     self.scheme if scheme is None else scheme, 0, 0,
                                     (qn if qn is not None else self.qn).data_ptr(),
-                                    self.R.data_ptr(), self.norms.data_ptr(), self.stream)
+                                    self.R.data_ptr(),
+                                    (norms if norms is not None else self.norms).data_ptr(),
+                                    ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream))
         if rc:
             raise RuntimeError(self.lib.csb_last_error(e.ctx))
 
@@ -213,35 +215,63 @@ def timed_steps(run, K, W, flush, sampler=None, scheme=None):
 def e2e_steps(run, K, W):
     """Same iteration through the C ABI with HOST (pinned) buffers in the
     reference layout (ni, nj, nk, nv): H2D copy, AoS->SoA, iteration,
-    SoA->AoS, D2H of Q^{m+1} and the norms, all inside the timed region."""
+    SoA->AoS, D2H of Q^{m+1} and the norms, all inside the timed region.
+    The steps are independent batches, pipelined over double buffers: the H2D
+    of step k+1 and the D2H of step k-1 overlap the compute of step k (copy
+    streams + events; the compute stream waits on both)."""
     torch, e, lib = run.torch, run.eng, run.lib
     nv, N = e.nv, e.N
     host_q = torch.from_numpy(np.ascontiguousarray(run.spec.q.reshape(N, nv))).pin_memory()
-    host_out = torch.empty((N, nv), dtype=torch.float64).pin_memory()
-    host_norms = torch.empty(4, dtype=torch.float64).pin_memory()
-    dev_aos = e.empty(N, nv)
-    q_soa = e.empty(nv, N)
-    out_aos = e.empty(N, nv)
-    st = run.stream
+    host_out = [torch.empty((N, nv), dtype=torch.float64).pin_memory() for _ in range(2)]
+    host_norms = [torch.empty(4, dtype=torch.float64).pin_memory() for _ in range(2)]
+    dev_aos = [e.empty(N, nv) for _ in range(2)]
+    q_soa = [e.empty(nv, N) for _ in range(2)]
+    qn = [e.empty(nv, N) for _ in range(2)]
+    norms = [e.empty(4) for _ in range(2)]
+    out_aos = [e.empty(N, nv) for _ in range(2)]
+    s_comp = torch.cuda.current_stream()
+    s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_h2d = [torch.cuda.Event() for _ in range(2)]
+    ev_in_free = [torch.cuda.Event() for _ in range(2)]
+    ev_comp = [torch.cuda.Event() for _ in range(2)]
+    ev_d2h = [torch.cuda.Event() for _ in range(2)]
+    st = ctypes.c_void_p(s_comp.cuda_stream)
+    issued = [False, False]
 
-    def one():
-        dev_aos.copy_(host_q, non_blocking=True)
-        lib.csb_transpose(N, nv, dev_aos.data_ptr(), q_soa.data_ptr(), 1, st)
-        run.step(q=q_soa)
-        lib.csb_transpose(N, nv, run.qn.data_ptr(), out_aos.data_ptr(), 0, st)
-        host_out.copy_(out_aos, non_blocking=True)
-        host_norms.copy_(run.norms, non_blocking=True)
+    def one(k):
+        b = k & 1
+        with torch.cuda.stream(s_h2d):
+            if issued[b]:
+                s_h2d.wait_event(ev_in_free[b])
+            dev_aos[b].copy_(host_q, non_blocking=True)
+            ev_h2d[b].record(s_h2d)
+        s_comp.wait_event(ev_h2d[b])
+        if issued[b]:
+            s_comp.wait_event(ev_d2h[b])
+        lib.csb_transpose(N, nv, dev_aos[b].data_ptr(), q_soa[b].data_ptr(), 1, st)
+        ev_in_free[b].record(s_comp)
+        run.step(q=q_soa[b], qn=qn[b], norms=norms[b])
+        lib.csb_transpose(N, nv, qn[b].data_ptr(), out_aos[b].data_ptr(), 0, st)
+        ev_comp[b].record(s_comp)
+        with torch.cuda.stream(s_d2h):
+            s_d2h.wait_event(ev_comp[b])
+            host_out[b].copy_(out_aos[b], non_blocking=True)
+            host_norms[b].copy_(norms[b], non_blocking=True)
+            ev_d2h[b].record(s_d2h)
+        issued[b] = True
 
-    for _ in range(W):
-        one()
+    for k in range(W):
+        one(k)
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(K):
-        one()
-    b.record()
+    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s_comp)
+    for k in range(K):
+        one(W + k)
+    for b in range(2):
+        s_comp.wait_event(ev_d2h[b])
+    z.record(s_comp)
     torch.cuda.synchronize()
-    return a.elapsed_time(b), N * nv * 8, N * nv * 8 + 3 * 8
+    return a.elapsed_time(z), N * nv * 8, N * nv * 8 + 3 * 8
 
 
 def ncu_traffic(path=os.path.join(ROOT, "profiles", "ncu_traffic.json")):
