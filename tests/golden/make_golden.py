@@ -325,6 +325,33 @@ def march_case():
         put(spec.name, "ramp", [5.0, 2.0, 10])
 
 
+def march_c4_case():
+    """Config 4 on a reduced grid (BASELINE.json config 4; the
+    history oracle is a reduced grid run through the identical code path):
+    48x32 O-grid (geometry as config 2), 11 species, freestream initial
+    field, CS1, CFL ramp 1 -> x2 every 8 iterations, 40 iterations."""
+    spec = C.config4(dims=(48, 32, 1))
+    model = ref_model(spec)
+    grid = compute_metrics(spec.nodes)
+    bcs = ref_bcs(spec, model)
+    rho, u, T, Y = spec.bcs["jmax"].fs
+    inf = make_primitive(model, rho=rho, u=u, T=T, Y=Y)
+    case = Case(grid=grid, model=model, bcs=bcs, freestream=inf, scheme="CS1", cfl=1000.0,
+                cfl_ramp=(1.0, 2.0, 8), max_iters=40, residual_drop_orders=np.inf,
+                stop_on_absolute_floor=False)
+    spec.q = case.initial_field()
+    name = "march_c4"
+    store_inputs(name, spec)
+    q, hist = steady_solve(case)
+    put(name, "res_flow", hist.res_flow)
+    put(name, "res_species", hist.res_species)
+    put(name, "res_density", hist.res_density)
+    put(name, "cfl_used", hist.cfl)
+    put(name, "q_final", q)
+    put(name, "ramp", [1.0, 2.0, 8])
+    put(name, "fs_prim", np.concatenate(([rho], u, [T], Y)))
+
+
 def main():
     spec = C.config0(seed=11, dims=(8, 6, 1))
     one_iteration("box_air5", spec, ("CI", "CS1", "CS2"))
@@ -336,6 +363,7 @@ def main():
     one_iteration("warped", case_warped(), ("CI", "CS1"))
     chem_rates_case()
     march_case()
+    march_c4_case()
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **OUT)
     print(f"wrote {path}: {len(OUT)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")

@@ -269,3 +269,26 @@ def test_steady_march_matches_reference_history(name):
         assert got.shape == ref.shape
         assert np.max(np.abs(np.log10(got) - np.log10(ref))) <= 1e-9, key
     assert comp_relerr(q, get(name, "q_final")) <= 1e-9
+
+
+def test_config4_reduced_march_matches_reference_history():
+    """Config 4 on a reduced 48x32 O-grid (11 species, freestream start, CFL
+    ramp, 40 iterations) against the reference's own steady_solve: the CFL
+    halvings/recoveries and the residual histories."""
+    from paper_2403_03440_b200.driver import Case, steady_solve
+    from paper_2403_03440_b200.mixture import make_primitive
+    name = "march_c4"
+    grid, model, bcs, mech, q0, cfl = golden_product(name)
+    f = get(name, "fs_prim")
+    inf = make_primitive(model, rho=f[0], u=f[1:4], T=f[4], Y=f[5:])
+    ramp = tuple(float(v) for v in get(name, "ramp"))
+    case = Case(grid=grid, model=model, bcs=bcs, freestream=inf, mech=mech, scheme="CS1",
+                cfl=1000.0, cfl_ramp=(ramp[0], ramp[1], int(ramp[2])), max_iters=40,
+                residual_drop_orders=np.inf, stop_on_absolute_floor=False)
+    q, hist = steady_solve(case, q0)
+    assert len(hist.iters) == 40
+    np.testing.assert_allclose(np.asarray(hist.cfl), get(name, "cfl_used"), rtol=1e-12)
+    for key in ("res_flow", "res_species", "res_density"):
+        got, ref = np.asarray(getattr(hist, key)), get(name, key)
+        assert np.max(np.abs(np.log10(got) - np.log10(ref))) <= 1e-8, key
+    assert comp_relerr(q, get(name, "q_final")) <= 1e-8
