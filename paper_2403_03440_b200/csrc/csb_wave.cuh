@@ -997,59 +997,66 @@ __global__ void __launch_bounds__(256, 2) k_epilogue2d(const Model* __restrict__
       if (k < nv) d[k] = es[k * CT + e];
     if (dq_std)
       for (int k = 0; k < nv; ++k) dq_std[(long long)k * N + c] = d[k];
+    // all q loads first (memory-level parallelism), closure in registers, the
+    // gate decodes the new state from registers (no read-back of q_new)
     const double* qc = q + c;
     double* qo = qn + c;
+    double qv[5 + NSB], o[5 + NSB];
 #pragma unroll
-    for (int k = 0; k < 5; ++k) qo[k * N] = qc[k * N] + d[k];
+    for (int k = 0; k < 5 + NSB; ++k) qv[k] = k < nv ? qc[k * N] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) o[k] = qv[k] + d[k];
     bool ok1 = true;
     if (scheme == SCH_CI) {
       double tail = 0.0;
-      for (int sp = 0; sp < ns - 1; ++sp) {
-        const double v = qc[(5 + sp) * N] + d[5 + sp];
-        qo[(5 + sp) * N] = v;
-        tail += v;
-      }
-      const double lastv = qo[0] - tail;
-      qo[(4 + ns) * N] = lastv;
-      ok1 = !(lastv < -1e-10 * qo[0]);
+#pragma unroll
+      for (int sp = 0; sp < NSB; ++sp)
+        if (sp < ns - 1) {
+          o[5 + sp] = qv[5 + sp] + d[5 + sp];
+          tail += o[5 + sp];
+        }
+      const double lastv = o[0] - tail;
+#pragma unroll
+      for (int sp = 0; sp < NSB; ++sp)
+        if (sp == ns - 1) o[5 + sp] = lastv;
+      ok1 = !(lastv < -1e-10 * o[0]);
     } else {
-      double rs[NSB], tot = 0.0, dsum = 0.0;
+      double tot = 0.0, dsum = 0.0;
 #pragma unroll
       for (int sp = 0; sp < NSB; ++sp)
         if (sp < ns) {
-          rs[sp] = qc[(5 + sp) * N];
-          tot += rs[sp];
+          tot += qv[5 + sp];
           dsum += d[5 + sp];
         }
-      double out[NSB], osum = 0.0;
+      double osum = 0.0;
       if (scheme == SCH_CS1) {
         const double defect = d[0] - dsum;
 #pragma unroll
         for (int sp = 0; sp < NSB; ++sp)
-          if (sp < ns) out[sp] = rs[sp] + d[5 + sp] + (rs[sp] / tot) * defect;
+          if (sp < ns) o[5 + sp] = qv[5 + sp] + d[5 + sp] + (qv[5 + sp] / tot) * defect;
       } else {
         const double rnew = tot + d[0];
         double rawsum = 0.0;
 #pragma unroll
         for (int sp = 0; sp < NSB; ++sp)
-          if (sp < ns) rawsum += rs[sp] + d[5 + sp];
+          if (sp < ns) rawsum += qv[5 + sp] + d[5 + sp];
 #pragma unroll
         for (int sp = 0; sp < NSB; ++sp)
-          if (sp < ns) out[sp] = rnew * (rs[sp] + d[5 + sp]) / rawsum;
+          if (sp < ns) o[5 + sp] = rnew * (qv[5 + sp] + d[5 + sp]) / rawsum;
       }
 #pragma unroll
       for (int sp = 0; sp < NSB; ++sp)
-        if (sp < ns) {
-          qo[(5 + sp) * N] = out[sp];
-          osum += out[sp];
-        }
+        if (sp < ns) osum += o[5 + sp];
       ok1 = !(osum <= 0.0);
 #pragma unroll
       for (int sp = 0; sp < NSB; ++sp)
-        if (sp < ns && out[sp] < -EPS_NEG * osum) ok1 = false;
+        if (sp < ns && o[5 + sp] < -EPS_NEG * osum) ok1 = false;
     }
+#pragma unroll
+    for (int k = 0; k < 5 + NSB; ++k)
+      if (k < nv) qo[k * N] = o[k];
     Cell<NSB> cs;
-    const bool ok2 = decode<NSB>(m, qn + c, N, cs);
+    const bool ok2 = decode<NSB>(m, o, 1, cs);
     if (!ok1 && first1 == ~0ull) first1 = (unsigned long long)c;
     if (!ok2 && first2 == ~0ull) first2 = (unsigned long long)c;
     if (!(ok1 && ok2)) ++bad_count;
