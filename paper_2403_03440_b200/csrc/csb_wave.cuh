@@ -558,54 +558,65 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
   }
 }
 
-// species chain: NSB independent scalar chains per row (padding species carry
+// species chains: NSB independent scalar chains per row (padding species carry
 // zero records, so they stay exactly zero).  PER: one diagonal per species
-// (chemistry) instead of one shared diagonal.
+// (chemistry) instead of one shared diagonal.  Large species counts split
+// over sp_warps<NSB>() chain warps of SG = NSB / sp_warps species each (all
+// in registers; measured: one warp with NSB = 48 register chains spills, and
+// an smem-resident state is MIO-bound).  All chain warps read the same ring.
+template <int NSB>
+constexpr int sp_warps() { return NSB <= 16 ? 1 : (NSB + 15) / 16; }
+
 template <int NSB, bool BWD, bool PER>
-CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro) {
+CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro, int grp) {
   constexpr int WK = wave_wks<NSB>();
+  constexpr int SG = NSB / sp_warps<NSB>();   // species of this warp
   constexpr int NI = PER ? NSB : 1, NG = NI + NSB + 2;
   constexpr int PC = BWD ? NI : NI + NSB;   // c_i, c_j planes
   constexpr int PV = BWD ? NI + 2 : NI;     // dq* (backward) | rhs (forward) planes
   constexpr int NGO = BWD ? NSB : NG, PO = BWD ? 0 : NI + 2;  // output: SW | SB dq* planes
+  static_assert(NSB % sp_warps<NSB>() == 0, "species groups");
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
+  const int c0 = grp * SG;
   const WaveArgs& a = *x.a;
   const long long slot = (long long)WK * NG * 32;
-  double oi[NSB], oj[NSB];
+  double oi[SG], oj[SG];
 #pragma unroll
-  for (int c = 0; c < NSB; ++c) oi[c] = oj[c] = 0.0;
+  for (int c = 0; c < SG; ++c) oi[c] = oj[c] = 0.0;
   int buf = 0, phase = 0;
   for (int ks = 0; ks < x.nslots; ++ks) {
     const int k = BWD ? x.nslots - 1 - ks : ks;
     mbar_wait(&x.full_bar[buf], phase);
     const double* base = x.ring + buf * slot + lane;
-    double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO) * 32 + lane;
-    const double* hb = x.recv ? x.hin + ((k * WK) % HRING) * NSB : x.hin + HRING * NSB;
-    double* ho = x.hand_out + (long long)k * WK * NSB;
+    double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO + c0) * 32 + lane;
+    const double* hb = (x.recv ? x.hin + ((k * WK) % HRING) * NSB : x.hin + HRING * NSB) + c0;
+    double* ho = x.hand_out + (long long)k * WK * NSB + c0;
 #pragma unroll
     for (int m = 0; m < WK; ++m) {
       const int kk = BWD ? WK - 1 - m : m;
       const double* p = base + kk * NG * 32;
       const double* hv = hb + kk * NSB;
-      double ij[NSB];
+      double ij[SG];
 #pragma unroll
-      for (int c = 0; c < NSB; ++c) {
+      for (int c = 0; c < SG; ++c) {
         const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
         ij[c] = fma(sh, x.mul, hv[c]);
       }
       const double ci = p[PC * 32], cj = p[(PC + 1) * 32];
+      const double* pi = p + (PER ? c0 : 0) * 32;
+      const double* pv = p + (PV + c0) * 32;
 #pragma unroll
-      for (int c = 0; c < NSB; ++c) {
-        const double inv = p[(PER ? c : 0) * 32];
-        const double v = p[(PV + c) * 32];
+      for (int c = 0; c < SG; ++c) {
+        const double inv = pi[(PER ? c : 0) * 32];
+        const double v = pv[c * 32];
         const double dq = BWD ? v - (oi[c] + ij[c]) * inv : ((v + oi[c]) + ij[c]) * inv;
         ob[(kk * NGO + c) * 32] = dq;
         oi[c] = ci * dq;
         oj[c] = cj * dq;
       }
 #pragma unroll
-      for (int c = 0; c < NSB; ++c) st_pred_cg_f64(ho + kk * NSB + c, oj[c], x.send);
+      for (int c = 0; c < SG; ++c) st_pred_cg_f64(ho + kk * NSB + c, oj[c], x.send);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&x.empty_bar[buf]);
@@ -786,8 +797,13 @@ CSB_DEV void chain_ci_big(const ChainCtx& x, const WaveRole& ro, double* st) {
   }
 }
 
+// threads per wavefront CTA: chain warps (up to sp_warps<NSB>()) + producer +
+// receiver
+template <int NSB>
+constexpr int wave_threads() { return 32 * (sp_warps<NSB>() + 2); }
+
 template <int NSB, bool BWD, bool PER>
-__global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
+__global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
   extern __shared__ __align__(128) double wsm[];
   __shared__ unsigned long long full_bar[8], empty_bar[8];
   __shared__ int s_strip;
@@ -804,6 +820,7 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   const WaveRole ro = kind == 1 ? a.role[1] : a.role[0];
   const int WK = kind == 2 ? ci_wk<NSB>() : kind ? wave_wks<NSB>() : WKF;
   const int nh = kind == 2 ? 5 + NSB : kind ? NSB : 5;
+  const int nchain = kind == 1 ? sp_warps<NSB>() : 1;  // chain warps of this role
   const int D = ro.D, NG = ro.ng;
   const long long slot = (long long)WK * NG * 32;
   double* ring = wsm;                     // [D][WK][NG][32]
@@ -838,7 +855,7 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   if (threadIdx.x == 0) {
     for (int b = 0; b < D; ++b) {
       mbar_init(&full_bar[b], x.has_up ? 2 : 1);  // TMA producer (+ hand-off receiver)
-      mbar_init(&empty_bar[b], 1);
+      mbar_init(&empty_bar[b], nchain);  // every chain warp releases the slot
     }
     for (int c = 0; c < WK * nh; ++c) hin[HRING * nh + c] = 0.0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -847,7 +864,7 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
   const int s = x.s;
   const int up = BWD ? s + 1 : s - 1;
 
-  if (warp == 1) {
+  if (warp == nchain) {
     // ---------------------------------------------------- producer (TMA)
     if (lane == 0) {
       int buf = 0, phase = 0;
@@ -870,53 +887,47 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
     return;
   }
 
-  if (warp == 2) {
+  if (warp == nchain + 1) {
     // ---------------------------------------------------- hand-off receiver
     // For each ring slot: the upstream columns its steps need (one per lane,
     // at most WK <= 32), polled until complete, copied into hin, then one
     // arrival on the slot's full barrier (release: the chain's wait acquires).
     if (!x.has_up) return;
-    constexpr int CAP = (NSB > 5 ? NSB : 5) < 16 ? (NSB > 5 ? NSB : 5) : 16;
     // upstream row u of the hand-off buffer holds what the upstream strip's
-    // sending row produced at its step u; this strip's first row needs, at
-    // its step t, the upstream step t + 31 (forward: upstream row 31 -> our
-    // row 0) or t - 31 (backward: upstream row 0 -> our row 31)
+    // sending row produced at its step u; our receiving row needs, at our step
+    // t, the upstream step t + 31 (forward: upstream row 31 -> our row 0) or
+    // t - 31 (backward: upstream row 0 -> our row 31).  A slot needs WK rows
+    // of nh words: the words are spread over the lanes (up to 8 per lane),
+    // all loaded at once, and the slot is released when none is the sentinel.
     const double* src = ro.hand + ((long long)up * (T + 2 * HPAD) + HPAD) * nh;
+    const int nw = WK * nh;  // words per slot (<= 256)
     int buf = 0, phase = 0;
     for (int ks = 0; ks < x.nslots; ++ks) {
       const int k = BWD ? x.nslots - 1 - ks : ks;
       if (ks >= D) mbar_wait(&empty_bar[buf], phase ^ 1);  // slot free: hin rows too
-      const int t = k * WK + lane;                          // our step
-      const long long u = BWD ? t - 31 : t + 31;            // upstream step
-      const bool in = lane < WK;
-      unsigned long long w[CAP];
-      bool done = !in;
+      const long long u0 = (long long)k * WK + (BWD ? -31 : 31);  // upstream step of kk = 0
+      const long long* sw = reinterpret_cast<const long long*>(src) + u0 * nh;
+      double* dst = hin + ((k * WK) % HRING) * nh;
+      unsigned long long w[8];
+      unsigned have = 0u;  // bit r: word lane + 32 r loaded and final
+      const int cnt = nw > lane ? (nw - lane + 31) / 32 : 0;
+      const unsigned need = (1u << cnt) - 1u;
       while (true) {
-        bool ok = true;
-        if (!done) {
 #pragma unroll
-          for (int c = 0; c < CAP; ++c) {
-            if (c < nh) {
-              w[c] = (unsigned long long)__ldcg(reinterpret_cast<const long long*>(src) +
-                                                u * nh + c);
-              ok &= w[c] != HAND_SENTINEL;
-            }
-          }
-          for (int c = CAP; c < nh; ++c)
-            ok &= (unsigned long long)__ldcg(reinterpret_cast<const long long*>(src) + u * nh +
-                                             c) != HAND_SENTINEL;
-          if (ok) {
-#pragma unroll
-            for (int c = 0; c < CAP; ++c)
-              if (c < nh) hin[(t % HRING) * nh + c] = __longlong_as_double((long long)w[c]);
-            for (int c = CAP; c < nh; ++c)
-              hin[(t % HRING) * nh + c] = __longlong_as_double(
-                  __ldcg(reinterpret_cast<const long long*>(src) + u * nh + c));
-            done = true;
+        for (int r = 0; r < 8; ++r) {
+          const int e = lane + 32 * r;
+          if (e < nw && !(have >> r & 1u)) {
+            w[r] = (unsigned long long)__ldcg(sw + e);
+            if (w[r] != HAND_SENTINEL) have |= 1u << r;
           }
         }
-        if (__all_sync(0xffffffffu, done)) break;
+        if (__all_sync(0xffffffffu, (have & need) == need)) break;
         __nanosleep(a.poll_ns);
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int e = lane + 32 * r;
+        if (e < nw) dst[e] = __longlong_as_double((long long)w[r]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_bar[buf]);
@@ -928,13 +939,14 @@ __global__ void __launch_bounds__(96, 1) k_wave2d(WaveArgs a) {
     return;
   }
 
-  // -------------------------------------------------------- chain (warp 0)
+  // -------------------------------------------------------- chain warps
+  if (warp >= nchain) return;  // surplus warps of a role with fewer chains
   unsigned long long t0 = 0;
   if (a.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   if (kind == 0) {
     chain_flow<BWD>(x, ro);
   } else if (kind == 1) {
-    chain_species<NSB, BWD, PER>(x, ro);
+    chain_species<NSB, BWD, PER>(x, ro, warp);
   } else {
     if constexpr (!PER) {
       if constexpr (NSB <= CI_MAXNSB) chain_ci<NSB, BWD>(x, ro);
@@ -1150,7 +1162,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
           auto kfn = bwd ? k_wave2d<NSB, true, false> : k_wave2d<NSB, false, false>;
           cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
           cudaMemsetAsync(wb.prog, 0, sizeof(int) * 2, st);
-          kfn<<<sk.nstrip, 96, smem, st>>>(wa);
+          kfn<<<sk.nstrip, wave_threads<NSB>(), smem, st>>>(wa);
           if (ev) cudaEventRecord(ev[2 + pass], st);
         }
         const int CE = epilogue_steps(ns);
@@ -1166,7 +1178,11 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     const Skew& sk = wb.sk;
     const int NSF = nsI + NSB + 2;
     constexpr int WKS = wave_wks<NSB>();
-    const int Df = wave_depth(WKF, NFF, 5), Ds = wave_depth(WKS, NSF, NSB);
+    const size_t sp_extra = 0;
+    const int Df = wave_depth(WKF, NFF, 5);
+    int Ds = 0;
+    for (int D = 4; D >= 2 && !Ds; --D)
+      if (wave_role_smem(D, WKS, NSF, NSB) + sp_extra <= 210 * 1024) Ds = D;
     if (!Df || !Ds) return cudaErrorInvalidConfiguration;
     // ---------------- records
     int C = 4;  // measured: 4 steps per tile with 4 CTAs/SM beats 8 (1 CTA/SM less)
@@ -1224,7 +1240,8 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       rs.po = bwd ? 0 : nsI + 2;
       rs.hand = wb.hand + (bwd ? hsz : 0) + (long long)sk.nstrip * hrows * 5;
       rs.ticket = wb.prog + 1;
-      const size_t smem = std::max(wave_role_smem(Df, WKF, NFF, 5), wave_role_smem(Ds, WKS, NSF, NSB));
+      const size_t smem =
+          std::max(wave_role_smem(Df, WKF, NFF, 5), wave_role_smem(Ds, WKS, NSF, NSB) + sp_extra);
       auto kfn = bwd ? (per_species ? k_wave2d<NSB, true, true> : k_wave2d<NSB, true, false>)
                      : (per_species ? k_wave2d<NSB, false, true> : k_wave2d<NSB, false, false>);
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1232,7 +1249,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       const int nblk = wa.only == 0 || wa.only == 1 ? sk.nstrip
                        : wa.only == 4               ? 4 * sk.nstrip
                                                     : (2 * sk.nstrip + 3) / 4 * 4;
-      kfn<<<nblk, 96, smem, st>>>(wa);
+      kfn<<<nblk, wave_threads<NSB>(), smem, st>>>(wa);
       if (wa.dbg) {
         std::vector<unsigned long long> h(16 * 2 * sk.nstrip);
         cudaMemcpyAsync(h.data(), wa.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
