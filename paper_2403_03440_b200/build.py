@@ -21,7 +21,7 @@ LIB = os.path.join(LIBDIR, "libcsflow_b200.so")
 OBJDIR = os.path.join(ROOT, "build", "obj")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-BUCKETS = (2, 4, 6, 8, 12, 16, 24, 32, 48, 64)  # csb_common.cuh CSB_BUCKET_LIST
+BUCKETS = (2, 4, 5, 6, 8, 12, 16, 20, 24, 32, 40, 48, 64)  # csb_common.cuh CSB_BUCKET_LIST
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
 

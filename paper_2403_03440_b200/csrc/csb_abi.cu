@@ -299,6 +299,9 @@ int csb_set_model(csb_ctx* c, int ns, const double* M, const double* cp, const d
     m.TS[s] = T_mu[s] + S_mu[s];
     m.inv_T_mu[s] = 1.0 / T_mu[s];
   }
+  m.suth_shared = 1;
+  for (int s = 1; s < ns; ++s)
+    if (T_mu[s] != T_mu[0] || S_mu[s] != S_mu[0]) m.suth_shared = 0;
   if (!c->d_model && cudaMalloc(&c->d_model, sizeof(Model)) != cudaSuccess)
     return fail(c, CSB_E_CUDA, "cudaMalloc(model)");
   cudaError_t e = cudaMemcpy(c->d_model, &m, sizeof(Model), cudaMemcpyHostToDevice);

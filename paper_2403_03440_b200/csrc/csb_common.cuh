@@ -39,6 +39,7 @@ constexpr int FLAG_GATE_COUNT = 15;
 
 struct Model {
   int ns;
+  int suth_shared;  // every species has the same (T_mu, S_mu): one Sutherland factor per state
   double Pr, Sc;
   double M[MAXNS], cp[MAXNS], Rs[MAXNS], bs[MAXNS];
   double mu_ref[MAXNS], T_mu[MAXNS], S_mu[MAXNS], TS[MAXNS];  // TS = T_mu + S_mu
@@ -259,11 +260,25 @@ template <int NSB>
 CSB_DEV void transport(const Model& m, double T, const double* Y, double rho, double& mu, double& k,
                        double& D) {
   double acc = 0.0, cp = 0.0;
+  if (m.suth_shared) {
+    // mu_s = mu_ref_s * F(T) with F shared by all species: one sqrt and one
+    // division per state instead of ns (reassociated: last-ulp differences)
+    const double x = T * m.inv_T_mu[0];
+    const double F = (x * sqrt(x)) * m.TS[0] / (T + m.S_mu[0]);
 #pragma unroll
-  for (int s = 0; s < NSB; ++s) {
-    if (s < m.ns) {
-      acc += Y[s] * mu_species(m, s, T);
-      cp += Y[s] * m.cp[s];
+    for (int s = 0; s < NSB; ++s) {
+      if (s < m.ns) {
+        acc += Y[s] * (m.mu_ref[s] * F);
+        cp += Y[s] * m.cp[s];
+      }
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < NSB; ++s) {
+      if (s < m.ns) {
+        acc += Y[s] * mu_species(m, s, T);
+        cp += Y[s] * m.cp[s];
+      }
     }
   }
   mu = acc;
@@ -298,7 +313,7 @@ CSB_DEV double block_sum(double v, double* sh) {
 // templated kernels are instantiated once per bucket in separate translation
 // units (csb_bucket.cu compiled with -DCSB_BUCKET=<b>); their launchers are
 // named <name>_b<b> there (CSB_BK) and routed by csb_dispatch.cu.
-#define CSB_BUCKET_LIST(X) X(2) X(4) X(6) X(8) X(12) X(16) X(24) X(32) X(48) X(64)
+#define CSB_BUCKET_LIST(X) X(2) X(4) X(5) X(6) X(8) X(12) X(16) X(20) X(24) X(32) X(40) X(48) X(64)
 #define CSB_CAT2(a, b) a##_b##b
 #define CSB_CAT(a, b) CSB_CAT2(a, b)
 #ifdef CSB_BUCKET
@@ -312,8 +327,9 @@ CSB_DEV double block_sum(double v, double* sh) {
 #endif
 
 static inline int bucket_of(int ns) {
-  return ns <= 2 ? 2 : ns <= 4 ? 4 : ns <= 6 ? 6 : ns <= 8 ? 8 : ns <= 12 ? 12 : ns <= 16 ? 16
-       : ns <= 24 ? 24 : ns <= 32 ? 32 : ns <= 48 ? 48 : 64;
+  return ns <= 2 ? 2 : ns <= 4 ? 4 : ns <= 5 ? 5 : ns <= 6 ? 6 : ns <= 8 ? 8 : ns <= 12 ? 12
+       : ns <= 16 ? 16 : ns <= 20 ? 20 : ns <= 24 ? 24 : ns <= 32 ? 32 : ns <= 40 ? 40
+       : ns <= 48 ? 48 : 64;
 }
 
 static inline int grid_for(long long n, int bs) {

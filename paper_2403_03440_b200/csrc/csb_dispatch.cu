@@ -46,12 +46,15 @@ CSB_BUCKET_LIST(CSB_DECL)
   switch (bucket_of(ns)) {                                  \
     case 2: return NAME##_b2(__VA_ARGS__);                  \
     case 4: return NAME##_b4(__VA_ARGS__);                  \
+    case 5: return NAME##_b5(__VA_ARGS__);                  \
     case 6: return NAME##_b6(__VA_ARGS__);                  \
     case 8: return NAME##_b8(__VA_ARGS__);                  \
     case 12: return NAME##_b12(__VA_ARGS__);                \
     case 16: return NAME##_b16(__VA_ARGS__);                \
+    case 20: return NAME##_b20(__VA_ARGS__);                \
     case 24: return NAME##_b24(__VA_ARGS__);                \
     case 32: return NAME##_b32(__VA_ARGS__);                \
+    case 40: return NAME##_b40(__VA_ARGS__);                \
     case 48: return NAME##_b48(__VA_ARGS__);                \
     default: return NAME##_b64(__VA_ARGS__);                \
   }

@@ -565,7 +565,13 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
 // in registers; measured: one warp with NSB = 48 register chains spills, and
 // an smem-resident state is MIO-bound).  All chain warps read the same ring.
 template <int NSB>
-constexpr int sp_warps() { return NSB <= 16 ? 1 : (NSB + 15) / 16; }
+constexpr int sp_warps() {
+  // fewest warps with <= 8 register chains each (NSB divisible): the species
+  // chain then issues no more per step than the flow chain
+  int w = 1;
+  while (NSB / w > 8 || NSB % w != 0) ++w;
+  return w;
+}
 
 template <int NSB, bool BWD, bool PER>
 CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro, int grp) {
