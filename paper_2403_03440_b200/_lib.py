@@ -11,7 +11,7 @@ import os
 
 from .errors import ExtensionMissing
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libcsflow_b200.so")
+LIB_PATH = os.environ.get("CSB_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libcsflow_b200.so")
 
 _p = ctypes.c_void_p
 _d = ctypes.c_double

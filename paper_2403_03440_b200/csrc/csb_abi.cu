@@ -203,6 +203,7 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
     c->wb.sw = k.take<double>((size_t)nsb * sk.Np);
     c->wb.hand = k.take<double>((size_t)2 * sk.nstrip * (sk.T + 2 * HPAD) * (5 + nsb));
     c->wb.prog = k.take<int>(2);
+    c->wb.rdy = k.take<int>((size_t)sk.nstrip * sk.T);
     c->wb.nsI = 0;
     c->wave_ok = true;
   }
@@ -223,6 +224,8 @@ int zero_wave_records(csb_ctx* c, cudaStream_t st) {
     if (cudaMemsetAsync(gp.first, 0, (size_t)gp.second * w.sk.Np * sizeof(double), st) !=
         cudaSuccess)
       return 1;
+  if (cudaMemsetAsync(w.rdy, 0, (size_t)w.sk.nstrip * w.sk.T * sizeof(int), st) != cudaSuccess)
+    return 1;
   return 0;
 }
 
@@ -274,6 +277,9 @@ void csb_destroy(csb_ctx* c) {
   if (c->d_model) cudaFree(c->d_model);
   if (c->d_rx) cudaFree(c->d_rx);
   if (c->d_fs) cudaFree(c->d_fs);
+  if (c->wb.s2) cudaStreamDestroy(c->wb.s2);
+  if (c->wb.e1) cudaEventDestroy(c->wb.e1);
+  if (c->wb.e2) cudaEventDestroy(c->wb.e2);
   delete c;
 }
 
@@ -699,6 +705,16 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
       e = zero_wave_records(c, st) ? cudaErrorUnknown : cudaSuccess;
       c->wb.nsI = nsI;
     }
+    if (e == cudaSuccess && !c->wb.s2) {
+      // high-priority side stream of the overlapped forward sweep
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if (cudaStreamCreateWithPriority(&c->wb.s2, cudaStreamNonBlocking, hi) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c->wb.e1, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c->wb.e2, cudaEventDisableTiming) != cudaSuccess)
+        e = cudaErrorUnknown;
+    }
+    c->wb.epoch += 1;
     if (e == cudaSuccess)
       e = launch_wave_step(c->d_model, c->ns, c->g, c->wb, q, R, cfl, lamS, domd, dstride,
                            chem ? 1 : 0, scheme, offdiag_paper ? 1.0 : 0.5, q_new, dq_out, c->flags,

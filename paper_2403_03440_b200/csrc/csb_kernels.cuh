@@ -58,6 +58,14 @@ struct WaveBufs {
   double* hand;   // strip hand-off rows [2 sweeps][flow nstrip*(T+2*HPAD)*5 | species ..*NSB]
   int* prog;      // [2]: flow and species CTA tickets
   int nsI;        // species-diagonal planes of the current layout (0 = unset)
+  // records -> forward sweep overlap: the records kernel publishes epoch in
+  // rdy[strip][records tile] once a tile is stored; the forward sweep runs
+  // concurrently on the high-priority stream s2 and its TMA producer waits
+  // for the tiles of each ring slot (csb_wave.cuh)
+  int* rdy;       // [nstrip][T] (tiles of >= 1 step)
+  int epoch;      // this launch's tag (incremented per implicit step)
+  cudaStream_t s2;
+  cudaEvent_t e1, e2;
 };
 
 cudaError_t launch_wave_step(const Model* mp, int ns, const GridDev& g, const WaveBufs& wb,

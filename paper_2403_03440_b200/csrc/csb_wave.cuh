@@ -124,6 +124,40 @@ CSB_DEV long long gaddr(const Skew& k, int NG, int s, int t, int p, int r) {
   return (((long long)s * k.T + t) * NG + p) * 32 + r;
 }
 
+// ============================================================== hand-off reset
+// Both sweeps' strip hand-off rows: signalling-NaN sentinel in the data rows,
+// zero in the HPAD pad rows (one thread per row).
+static __global__ void k_hand_reset(double* __restrict__ hand, int nstrip, int T, int nhf, int nhs) {
+  const int rows = T + 2 * HPAD;
+  const long long nrow = 2LL * 2 * nstrip * rows;  // [sweep][role][strip][row]
+  const double sent = __longlong_as_double((long long)HAND_SENTINEL);
+  for (long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x; l < nrow;
+       l += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(l % rows);
+    const long long sr = l / rows;                 // [sweep][role][strip]
+    const int strip = (int)(sr % nstrip);
+    const int role = (int)((sr / nstrip) % 2);
+    const int sweep = (int)(sr / (2LL * nstrip));
+    const long long per_sweep = (long long)nstrip * rows * (nhf + nhs);
+    const int nh = role ? nhs : nhf;
+    double* p = hand + sweep * per_sweep + (role ? (long long)nstrip * rows * nhf : 0) +
+                ((long long)strip * rows + r) * nh;
+    const double v = (r < HPAD || r >= rows - HPAD) ? 0.0 : sent;
+    for (int c = 0; c < nh; ++c) p[c] = v;
+  }
+}
+
+// records tile (strip s, step block ib) stored: publish the launch epoch
+CSB_DEV void publish_tile(const WaveBufs& wb, int s, int ib) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(wb.rdy + (long long)s * wb.sk.T + ib),
+                 "r"(wb.epoch)
+                 : "memory");
+  }
+}
+
 // ============================================================== records
 // Tile = one strip (32 rows) x C wavefront steps, i.e. a parallelogram in
 // (i, j): element (tt, r) is cell (i = t0 + tt - r, j = j0 + r).  In these
@@ -137,7 +171,9 @@ CSB_DEV long long gaddr(const Skew& k, int NG, int s, int t, int p, int r) {
 // -R.  Phase B: per interior cell, face radii (max of the two adjacent cells
 // at the face metric), face coefficients, and all record stores.
 template <int NSB, bool CI>
-__global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ mp, GridDev g, Skew sk,
+// (measured: 4 CTAs/SM for small species counts; above, 3 CTAs/SM with 80
+// registers removes the spills: ns = 11 records 493 -> 400 us at 1024^2)
+__global__ void __launch_bounds__(256, NSB <= 8 ? 4 : 3) k_records2d(const Model* __restrict__ mp, GridDev g, Skew sk,
                                                    const double* __restrict__ q,
                                                    const double* __restrict__ R, double cfl,
                                                    const double* __restrict__ lamS,
@@ -149,7 +185,9 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
   const int ns = m.ns, nsI = per_species ? NSB : 1;  // species-diagonal planes
   const int NSF = nsI + NSB + 2;  // = SB group planes
   const int ncb = sk.T / C;
-  const int s = blockIdx.x / ncb, ib = blockIdx.x % ncb;
+  // tiles in step-block-major order: the concurrently running forward sweep
+  // consumes every strip's first columns first
+  const int s = blockIdx.x % sk.nstrip, ib = blockIdx.x / sk.nstrip;
   const int t0 = ib * C, j0 = s * 32;
   const int HX = C + 2, HY = 34, NH = HX * HY;
   const int CT = C * 32;
@@ -160,20 +198,6 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
                                                //   lower-i face Sx Sy, lower-j face Sx Sy
   double* TC = sm + 12 * NH;                   // [NCP][CT]
   const long long N = g.N;
-  {
-    // reset both sweeps' hand-off buffers: sentinel, zero in the pad rows
-    const long long rows = (long long)sk.T + 2 * HPAD;
-    const long long per_sweep = (long long)sk.nstrip * rows * (5 + NSB);
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < 2 * per_sweep;
-         e += (long long)gridDim.x * blockDim.x) {
-      const long long w = e % per_sweep;
-      const long long flow_words = CI ? per_sweep : (long long)sk.nstrip * rows * 5;
-      const int nh = CI ? 5 + NSB : w < flow_words ? 5 : NSB;
-      const long long r = (w < flow_words ? w : w - flow_words) / nh % rows;
-      wb.hand[e] = (r < HPAD || r >= rows - HPAD) ? 0.0
-                                                  : __longlong_as_double((long long)HAND_SENTINEL);
-    }
-  }
   // ---------------- phase A: halo-extended per-cell quantities.  Enumerated
   // column by column (fixed i, consecutive j) so that the loads of a warp are
   // contiguous runs of up to C + 2 cells: i' = tt - r in [-33, C + 1],
@@ -430,6 +454,7 @@ __global__ void __launch_bounds__(256, 4) k_records2d(const Model* __restrict__ 
       else sb[(nsI + d) * 32] = csp;
     }
   }
+  publish_tile(wb, s, ib);
 }
 
 // ============================================================== wavefront
@@ -450,6 +475,8 @@ struct WaveArgs {
   int only;          // -1: both roles (production); 0/1: one role (timing probe)
   int ci;            // coupled operator: one CI chain per strip (role[0])
   int poll_ns;       // receiver back-off between empty polls
+  const int* rdy;    // forward sweep overlapped with the records kernel: tile flags (or null)
+  int epoch, rC;     // their launch tag and the records tile length (steps)
   unsigned long long* dbg;  // timing probe: [CTA][4] globaltimer stamps (or null)
   WaveRole role[2];  // 0 flow, 1 species
 };
@@ -877,6 +904,15 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
       for (int ks = 0; ks < x.nslots; ++ks) {
         const int k = BWD ? x.nslots - 1 - ks : ks;
         if (ks >= D) mbar_wait(&empty_bar[buf], phase ^ 1);
+        if (a.rdy) {
+          // records tiles of this slot's steps stored (records kernel running
+          // concurrently): acquire their flags, then order the bulk copy
+          // (async proxy) after the acquire
+          const int* f = a.rdy + (long long)s * T;
+          for (int b = (k * WK) / a.rC; b <= (k * WK + WK - 1) / a.rC; ++b)
+            while (ld_acquire(f + b) != a.epoch) __nanosleep(64);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         const unsigned bytes = (unsigned)(slot * 8);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                          smem_u32(&full_bar[buf])),
@@ -1110,6 +1146,15 @@ inline int wave_depth(int WK, int NG, int nh) {
   return 0;
 }
 
+// One implicit step on the 2-D wavefront path.  Stream order: hand-off reset,
+// records, forward sweep, backward sweep, epilogue -- except that (outside
+// the per-stage timing probe, ev == nullptr) the forward sweep runs on the
+// high-priority side stream wb.s2 CONCURRENTLY with the records kernel (when
+// the sweeps use at most 48 SMs): the
+// sweep's 2 x nstrip CTAs take their SMs first, the records tiles fill the
+// remaining ones in step-block-major order, and each sweep ring slot waits
+// only for its own records tiles (WaveBufs::rdy).  CSB_NO_OVERLAP=1 restores
+// the serial order.
 cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, const WaveBufs& wb,
                                      const double* q, const double* R, double cfl,
                                      const double* lamS, const double* domd, int dom_stride,
@@ -1117,167 +1162,159 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
                                      double* dq_std, unsigned long long* flags, cudaStream_t st,
                                      cudaEvent_t* ev) {
   CSB_NS_DISPATCH(ns, {
-    if (scheme == SCH_CI) {
-      // ---------------- coupled operator (frozen chemistry): one chain per strip
-      {
-        if (per_species) return cudaErrorInvalidConfiguration;
-        const Skew& sk = wb.sk;
-        constexpr int NV = 5 + NSB, NG = ci_planes<NSB>(), WK = ci_wk<NSB>();
-        // large NSB: + the smem-resident chain state (4 x NV x 32 doubles)
-        const size_t extra = NSB > CI_MAXNSB ? (size_t)4 * NV * 32 * sizeof(double) : 0;
-        int Dc = 0;
-        for (int D = 4; D >= 2 && !Dc; --D)
-          if (wave_role_smem(D, WK, NG, NV) + extra <= 210 * 1024) Dc = D;
-        if (!Dc) return cudaErrorInvalidConfiguration;
-        int C = 4;
-        auto rsm_of = [&](int c) {
-          return ((size_t)(2 + 3 * NV) * c * 32 + 12 * (size_t)(c + 2) * 34) * sizeof(double);
-        };
-        while (C > 1 && rsm_of(C) > 200 * 1024) C /= 2;
-        const size_t rsm = rsm_of(C);
-        cudaFuncSetAttribute(k_records2d<NSB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)rsm);
-        if (ev) cudaEventRecord(ev[0], st);
-        k_records2d<NSB, true><<<sk.nstrip * (sk.T / C), 256, rsm, st>>>(
-            mp, g, sk, q, R, cfl, lamS, domd, dom_stride, 0, sp_scale, wb, C, flags);
-        if (ev) cudaEventRecord(ev[1], st);
-        for (int pass = 0; pass < 2; ++pass) {
-          const bool bwd = pass == 1;
-          WaveArgs wa{};
-          wa.sk = sk;
-          wa.ni = g.ni;
-          wa.nj = g.nj;
-          wa.nsI = 1;
-          wa.only = -1;
-          wa.poll_ns = 16;
-          wa.ci = 1;
-          wa.dbg = nullptr;
-          WaveRole& rc = wa.role[0];
-          rc.in = bwd ? wb.fb : wb.ff;
-          rc.ng = NG;
-          rc.D = Dc;
-          rc.out = bwd ? wb.fw : wb.fb;
-          rc.out2 = bwd ? wb.sw : nullptr;
-          rc.ngo = bwd ? 5 : NG;
-          rc.po = bwd ? 0 : 2 + 2 * NV + 8;
-          const long long hrows = (long long)sk.T + 2 * HPAD;
-          rc.hand = wb.hand + (bwd ? (long long)sk.nstrip * hrows * NV : 0);
-          rc.ticket = wb.prog;
-          wa.role[1] = rc;
-          const size_t smem = wave_role_smem(Dc, WK, NG, NV) + extra;
-          auto kfn = bwd ? k_wave2d<NSB, true, false> : k_wave2d<NSB, false, false>;
-          cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          cudaMemsetAsync(wb.prog, 0, sizeof(int) * 2, st);
-          kfn<<<sk.nstrip, wave_threads<NSB>(), smem, st>>>(wa);
-          if (ev) cudaEventRecord(ev[2 + pass], st);
-        }
-        const int CE = epilogue_steps(ns);
-        const size_t esm = (size_t)(5 + ns) * CE * 32 * sizeof(double);
-        cudaFuncSetAttribute(k_epilogue2d<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
-        k_epilogue2d<NSB><<<sk.nstrip * (sk.T / CE), 256, esm, st>>>(mp, g, sk, scheme, q, wb.fw,
-                                                                     wb.sw, qn, dq_std, CE, flags);
-        if (ev) cudaEventRecord(ev[4], st);
-        return cudaGetLastError();
-      }
-    }
-    const int nsI = per_species ? NSB : 1;
     const Skew& sk = wb.sk;
+    const bool ci = scheme == SCH_CI;
+    if (ci && per_species) return cudaErrorInvalidConfiguration;
+    constexpr int NV = 5 + NSB;
+    const int nsI = per_species ? NSB : 1;
     const int NSF = nsI + NSB + 2;
     constexpr int WKS = wave_wks<NSB>();
-    const size_t sp_extra = 0;
-    const int Df = wave_depth(WKF, NFF, 5);
-    int Ds = 0;
-    for (int D = 4; D >= 2 && !Ds; --D)
-      if (wave_role_smem(D, WKS, NSF, NSB) + sp_extra <= 210 * 1024) Ds = D;
-    if (!Df || !Ds) return cudaErrorInvalidConfiguration;
-    // ---------------- records
+    constexpr int NGC = ci_planes<NSB>(), WKC = ci_wk<NSB>();
+    // large NSB (CI): + the smem-resident chain state (4 x NV x 32 doubles)
+    const size_t ci_extra = NSB > CI_MAXNSB ? (size_t)4 * NV * 32 * sizeof(double) : 0;
+    int Df = 0, Ds = 0, Dc = 0;
+    if (ci) {
+      for (int D = 4; D >= 2 && !Dc; --D)
+        if (wave_role_smem(D, WKC, NGC, NV) + ci_extra <= 210 * 1024) Dc = D;
+      if (!Dc) return cudaErrorInvalidConfiguration;
+    } else {
+      Df = wave_depth(WKF, NFF, 5);
+      for (int D = 4; D >= 2 && !Ds; --D)
+        if (wave_role_smem(D, WKS, NSF, NSB) <= 210 * 1024) Ds = D;
+      if (!Df || !Ds) return cudaErrorInvalidConfiguration;
+    }
+    // ---------------- records tile length C (steps) and shared memory
     int C = 4;  // measured: 4 steps per tile with 4 CTAs/SM beats 8 (1 CTA/SM less)
     if (const char* ev_c = getenv("CSB_REC_C")) C = atoi(ev_c);  // tuning probe
     auto rsm_of = [&](int c) {
-      return ((size_t)(16 + nsI + NSB) * c * 32 + 12 * (size_t)(c + 2) * 34) * sizeof(double);
+      const int ncp = ci ? 2 + 3 * NV : 16 + nsI + NSB;
+      return ((size_t)ncp * c * 32 + 12 * (size_t)(c + 2) * 34) * sizeof(double);
     };
     while (C > 1 && rsm_of(C) > 200 * 1024) C /= 2;
     const size_t rsm = rsm_of(C);
-    cudaFuncSetAttribute(k_records2d<NSB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)rsm);
-    const int ncb = sk.T / C;
-    if (ev) cudaEventRecord(ev[0], st);
-    k_records2d<NSB, false><<<sk.nstrip * ncb, 256, rsm, st>>>(mp, g, sk, q, R, cfl, lamS, domd,
-                                                        dom_stride, per_species, sp_scale, wb, C,
-                                                        flags);
-    if (ev) cudaEventRecord(ev[1], st);
-    // ---------------- sweeps: one flow and one species CTA per strip
-    for (int pass = 0; pass < 2; ++pass) {
-      const bool bwd = pass == 1;
-      WaveArgs wa;
+    auto krec = ci ? k_records2d<NSB, true> : k_records2d<NSB, false>;
+    cudaFuncSetAttribute(krec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+    const int nrec = sk.nstrip * (sk.T / C);
+    auto launch_records = [&](cudaStream_t s) {
+      krec<<<nrec, 256, rsm, s>>>(mp, g, sk, q, R, cfl, lamS, domd, dom_stride, ci ? 0 : per_species,
+                                  sp_scale, wb, C, flags);
+    };
+    // ---------------- one sweep
+    int only = -1;
+    if (const char* ev_o = getenv("CSB_WAVE_ONLY")) only = atoi(ev_o);  // timing probe
+    const long long hrows = (long long)sk.T + 2 * HPAD;
+    auto launch_pass = [&](bool bwd, cudaStream_t s, const int* rdy) -> cudaError_t {
+      WaveArgs wa{};
       wa.sk = sk;
       wa.ni = g.ni;
       wa.nj = g.nj;
-      wa.nsI = nsI;
-      wa.only = -1;
-      wa.ci = 0;
+      wa.nsI = ci ? 1 : nsI;
+      wa.ci = ci ? 1 : 0;
+      wa.only = ci ? -1 : only;
       wa.poll_ns = 16;
       if (const char* ev_p = getenv("CSB_POLL_NS")) wa.poll_ns = atoi(ev_p);  // tuning probe
-      if (const char* ev_o = getenv("CSB_WAVE_ONLY")) wa.only = atoi(ev_o);  // timing probe
-      static unsigned long long* dbg = nullptr;
+      wa.rdy = rdy;
+      wa.epoch = wb.epoch;
+      wa.rC = C;
       wa.dbg = nullptr;
+      static unsigned long long* dbg = nullptr;
       if (getenv("CSB_WAVE_DBG")) {
         if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 16 * 2 * 4096);
-        cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 16 * 2 * sk.nstrip, st);
+        cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 16 * 2 * sk.nstrip, s);
         wa.dbg = dbg;
       }
-      WaveRole& rf = wa.role[0];
-      WaveRole& rs = wa.role[1];
-      rf.in = bwd ? wb.fb : wb.ff;
-      rf.ng = bwd ? NFB : NFF;
-      rf.D = Df;
-      rf.out = bwd ? wb.fw : wb.fb;
-      rf.ngo = bwd ? 5 : NFB;
-      rf.po = bwd ? 0 : FB_DQ;
-      const long long hrows = (long long)sk.T + 2 * HPAD;
-      const long long hsz = (long long)sk.nstrip * hrows * (5 + NSB);  // one sweep
-      rf.hand = wb.hand + (bwd ? hsz : 0);
-      rf.ticket = wb.prog;
-      rs.in = bwd ? wb.sb : wb.sf;
-      rs.ng = NSF;
-      rs.D = Ds;
-      rs.out = bwd ? wb.sw : wb.sb;
-      rs.ngo = bwd ? NSB : NSF;
-      rs.po = bwd ? 0 : nsI + 2;
-      rs.hand = wb.hand + (bwd ? hsz : 0) + (long long)sk.nstrip * hrows * 5;
-      rs.ticket = wb.prog + 1;
-      const size_t smem =
-          std::max(wave_role_smem(Df, WKF, NFF, 5), wave_role_smem(Ds, WKS, NSF, NSB) + sp_extra);
+      size_t smem;
+      int nblk;
+      if (ci) {
+        WaveRole& rc = wa.role[0];
+        rc.in = bwd ? wb.fb : wb.ff;
+        rc.ng = NGC;
+        rc.D = Dc;
+        rc.out = bwd ? wb.fw : wb.fb;
+        rc.out2 = bwd ? wb.sw : nullptr;
+        rc.ngo = bwd ? 5 : NGC;
+        rc.po = bwd ? 0 : 2 + 2 * NV + 8;
+        rc.hand = wb.hand + (bwd ? (long long)sk.nstrip * hrows * NV : 0);
+        rc.ticket = wb.prog;
+        wa.role[1] = rc;
+        smem = wave_role_smem(Dc, WKC, NGC, NV) + ci_extra;
+        nblk = sk.nstrip;
+      } else {
+        WaveRole& rf = wa.role[0];
+        WaveRole& rs = wa.role[1];
+        rf.in = bwd ? wb.fb : wb.ff;
+        rf.ng = bwd ? NFB : NFF;
+        rf.D = Df;
+        rf.out = bwd ? wb.fw : wb.fb;
+        rf.out2 = nullptr;
+        rf.ngo = bwd ? 5 : NFB;
+        rf.po = bwd ? 0 : FB_DQ;
+        const long long hsz = (long long)sk.nstrip * hrows * (5 + NSB);  // one sweep
+        rf.hand = wb.hand + (bwd ? hsz : 0);
+        rf.ticket = wb.prog;
+        rs.in = bwd ? wb.sb : wb.sf;
+        rs.ng = NSF;
+        rs.D = Ds;
+        rs.out = bwd ? wb.sw : wb.sb;
+        rs.out2 = nullptr;
+        rs.ngo = bwd ? NSB : NSF;
+        rs.po = bwd ? 0 : nsI + 2;
+        rs.hand = wb.hand + (bwd ? hsz : 0) + (long long)sk.nstrip * hrows * 5;
+        rs.ticket = wb.prog + 1;
+        smem = std::max(wave_role_smem(Df, WKF, NFF, 5), wave_role_smem(Ds, WKS, NSF, NSB));
+        nblk = only == 0 || only == 1 ? sk.nstrip
+               : only == 4            ? 4 * sk.nstrip
+                                      : (2 * sk.nstrip + 3) / 4 * 4;
+      }
       auto kfn = bwd ? (per_species ? k_wave2d<NSB, true, true> : k_wave2d<NSB, true, false>)
                      : (per_species ? k_wave2d<NSB, false, true> : k_wave2d<NSB, false, false>);
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      cudaMemsetAsync(wb.prog, 0, sizeof(int) * 2, st);
-      const int nblk = wa.only == 0 || wa.only == 1 ? sk.nstrip
-                       : wa.only == 4               ? 4 * sk.nstrip
-                                                    : (2 * sk.nstrip + 3) / 4 * 4;
-      kfn<<<nblk, wave_threads<NSB>(), smem, st>>>(wa);
+      cudaMemsetAsync(wb.prog, 0, sizeof(int) * 2, s);
+      kfn<<<nblk, wave_threads<NSB>(), smem, s>>>(wa);
       if (wa.dbg) {
         std::vector<unsigned long long> h(16 * 2 * sk.nstrip);
-        cudaMemcpyAsync(h.data(), wa.dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
+        cudaMemcpyAsync(h.data(), wa.dbg, h.size() * 8, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
         unsigned long long tmin = ~0ull;
         for (int e = 0; e < 2 * sk.nstrip; ++e)
           if (h[16 * e]) tmin = std::min(tmin, h[16 * e]);
         for (int e = 0; e < 2 * sk.nstrip; ++e)
-          if (h[16 * e]) {
-            fprintf(stderr, "wave%s strip %d kind %d: start %.2f first %.2f end %.2f | stamps:",
-                    bwd ? "B" : "F", e / 2, e % 2, (h[16 * e] - tmin) * 1e-3,
-                    h[16 * e + 2] ? (h[16 * e + 2] - tmin) * 1e-3 : -1.0,
-                    (h[16 * e + 1] - tmin) * 1e-3);
-            for (int k = 3; k < 13; ++k)
-              if (h[16 * e + k]) fprintf(stderr, " %.1f", (h[16 * e + k] - tmin) * 1e-3);
-            fprintf(stderr, " | reloads %llu waited %llu polls %llu", h[16 * e + 13], h[16 * e + 14],
-                    h[16 * e + 15]);
-            fprintf(stderr, "\n");
-          }
+          if (h[16 * e])
+            fprintf(stderr, "wave%s strip %d kind %d: start %.2f end %.2f\n", bwd ? "B" : "F",
+                    e / 2, e % 2, (h[16 * e] - tmin) * 1e-3, (h[16 * e + 1] - tmin) * 1e-3);
       }
-      if (ev) cudaEventRecord(ev[2 + pass], st);
+      return cudaGetLastError();
+    };
+    // ---------------- the step
+    note_launches(1);
+    k_hand_reset<<<grid_for(4LL * sk.nstrip * hrows, 256), 256, 0, st>>>(
+        wb.hand, sk.nstrip, sk.T, ci ? NV : 5, ci ? 0 : NSB);
+    // measured: the overlap pays while the sweeps hold a small share of the
+    // SMs (512^2: 32 of 148 SMs, 0.649 -> 0.587 ms per iteration); at 1024^2
+    // (64 SMs) the concurrent records tiles slow the chains more than they hide
+    // (2.23 -> 2.35 ms at ns = 11)
+    const bool overlap = !ev && wb.s2 && only == -1 && 2 * sk.nstrip <= 48 &&
+                         !getenv("CSB_NO_OVERLAP");
+    cudaError_t e;
+    if (overlap) {
+      cudaEventRecord(wb.e1, st);
+      cudaStreamWaitEvent(wb.s2, wb.e1, 0);
+      e = launch_pass(false, wb.s2, wb.rdy);  // first: its CTAs take their SMs
+      if (e != cudaSuccess) return e;
+      launch_records(st);
+      cudaEventRecord(wb.e2, wb.s2);
+      cudaStreamWaitEvent(st, wb.e2, 0);
+    } else {
+      if (ev) cudaEventRecord(ev[0], st);
+      launch_records(st);
+      if (ev) cudaEventRecord(ev[1], st);
+      e = launch_pass(false, st, nullptr);
+      if (e != cudaSuccess) return e;
+      if (ev) cudaEventRecord(ev[2], st);
     }
+    e = launch_pass(true, st, nullptr);
+    if (e != cudaSuccess) return e;
+    if (ev) cudaEventRecord(ev[3], st);
     // ---------------- epilogue
     const int CE = epilogue_steps(ns);
     const size_t esm = (size_t)(5 + ns) * CE * 32 * sizeof(double);

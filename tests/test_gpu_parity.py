@@ -181,7 +181,7 @@ def _wave_vs_generic(spec, scheme, tol=1e-10):
     assert (fw, cw) == (fg, cg)
 
 
-@pytest.mark.parametrize("dims", [(64, 64, 1), (40, 45, 1), (3, 70, 1), (50, 7, 1), (33, 96, 1)])
+@pytest.mark.parametrize("dims", [(64, 64, 1), (40, 45, 1), (3, 70, 1), (50, 7, 1), (33, 96, 1), (24, 330, 1)])
 @pytest.mark.parametrize("scheme", ["CS1", "CS2", "CI"])
 def test_wavefront_matches_generic_box(dims, scheme):
     from paper_2403_03440_b200 import configs as C
