@@ -384,6 +384,104 @@ def species_scan(flush, nss=(5, 11, 20, 40), dims=(1024, 1024, 1), K=3, W=2):
             "steps": K, "results": out}
 
 
+# ---------------------------------------------------------------- FP64 block LU
+def fp64_peak_tflops(lib, torch):
+    """Measured FP64 pipe peak (csb_fp64_peak: independent DFMA chains on
+    every SM), the denominator of the block-inverse roofline."""
+    scratch = torch.zeros(1, dtype=torch.float64, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    iters = 4000
+    lib.csb_fp64_peak(50, scratch.data_ptr(), st)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    lib.csb_fp64_peak(iters, scratch.data_ptr(), st)
+    b.record()
+    torch.cuda.synchronize()
+    flops = sms * 4 * 256 * iters * 16 * 8 * 2.0
+    return flops / (a.elapsed_time(b) * 1e-3) / 1e12
+
+
+def block_lu(hbm_peak, nss=(5, 11, 20), N=1 << 20, reps=5):
+    """Batched species block inverse inv(d I - V dOmega) of the coupled
+    operator with chemistry (reference implicit.py:362-368) on N = 2^20 cells
+    (config-3 cell count) per ns: achieved FP64 TFLOP/s (2 n^3 flops per
+    cell, Gauss-Jordan = LAPACK getrf + getri count) against the measured
+    FP64 peak, and algorithmic bytes (2 n^2 + 2 doubles per cell) against
+    HBM."""
+    import torch
+    from paper_2403_03440_b200 import _lib
+    lib = _lib.load()
+    peak = fp64_peak_tflops(lib, torch)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    out = []
+    for ns in nss:
+        dom = torch.randn((ns * ns, N), generator=g, device="cuda", dtype=torch.float64)
+        d = torch.rand(N, generator=g, device="cuda", dtype=torch.float64) * ns + ns
+        V = torch.ones(N, device="cuda", dtype=torch.float64)
+        dinv = torch.empty_like(dom)
+        fl = torch.zeros(16, dtype=torch.int64, device="cuda")
+        lib.csb_batched_inverse(ns, N, dom.data_ptr(), d.data_ptr(), V.data_ptr(), dinv.data_ptr(),
+                                fl.data_ptr(), st)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            lib.csb_batched_inverse(ns, N, dom.data_ptr(), d.data_ptr(), V.data_ptr(),
+                                    dinv.data_ptr(), fl.data_ptr(), st)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        tf = 2.0 * ns ** 3 * N / (ms * 1e-3) / 1e12
+        gbs = (2 * ns * ns + 2) * 8.0 * N / (ms * 1e-3) / 1e9
+        out.append({"ns": ns, "ms": ms, "tflops": tf, "fp64_frac": tf / peak, "gbs": gbs,
+                    "hbm_frac": gbs / hbm_peak,
+                    "bound": "fp64" if tf / peak >= gbs / hbm_peak else "hbm"})
+        del dom, dinv
+    return {"cells": N, "fp64_peak_tflops": peak,
+            "fp64_peak_source": "measured live (csb_fp64_peak DFMA chains, all SMs)",
+            "flops_per_cell": "2 ns^3", "bytes_per_cell": "(2 ns^2 + 2) x 8", "results": out}
+
+
+# ---------------------------------------------------------------- config 4 stages
+def config4_stages(hbm_peak, dims=(4096, 2048, 1)):
+    """Config 4 (BASELINE.json): 4096 x 2048 O-grid, 11 species, CS1.  Stage
+    times of one implicit iteration on the freestream start state (CUDA
+    events, serialized stages) and each stage's algorithmic bytes (SURVEY
+    §8(d)) against the HBM peak -- the size where the sweeps are meant to
+    approach the bandwidth roofline."""
+    import torch
+    from paper_2403_03440_b200 import configs as C
+    spec = C.config4(dims=dims)
+    run = Runner(spec, "CS1")
+    for _ in range(2):
+        run.step()
+    torch.cuda.synchronize()
+    K = 5
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(K):
+        run.step()
+    b.record()
+    torch.cuda.synchronize()
+    it_ms = a.elapsed_time(b) / K
+    st = run.stages(reps=2)
+    run.eng.status()
+    N, nv = run.eng.N, run.eng.nv
+    ab = algorithmic_bytes(nv)
+    per = {}
+    for k, nb in (("rhs", ab["rhs"]), ("assemble", ab["assemble"]), ("sweeps", ab["sweeps"])):
+        gbs = N * nb * 8 / (st[k] * 1e-3) / 1e9
+        per[k] = {"ms": st[k], "gbs": gbs, "frac": gbs / hbm_peak}
+    out = {"grid": "x".join(map(str, dims)), "ns": spec.ns, "cells": N,
+           "ms_per_iteration": it_ms, "cell_it_per_s": N / (it_ms * 1e-3),
+           "iteration_roofline_frac": (N * ab["total"] * 8 / (it_ms * 1e-3) / 1e9) / hbm_peak,
+           "stages_ms": st, "stage_roofline": per}
+    del run
+    torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------- replicas
 def replica_aggregate(local_ms, cells_per_rank, steps, dist=None, device="cpu"):
     """Whole-job throughput of N independent replicas: the timed region's
@@ -451,6 +549,12 @@ def main():
                 extras["species_scan"] = species_scan(flush)
             except Exception as exc:  # the scan must not kill the headline line
                 extras["species_scan"] = {"error": repr(exc)}
+            for key, fn in (("block_lu", lambda: block_lu(peaks()[0])),
+                            ("config4", lambda: config4_stages(peaks()[0]))):
+                try:
+                    extras[key] = fn()
+                except Exception as exc:  # extras must not kill the headline line
+                    extras[key] = {"error": repr(exc)}
         e2e = {"value": world * N * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
         run.eng.status()

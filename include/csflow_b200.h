@@ -201,6 +201,20 @@ int csb_iteration(csb_ctx* ctx, const double* q, double cfl, int scheme, int off
 /* AoS [N][nv] <-> SoA [nv][N] (device). */
 int csb_transpose(long long N, int nv, const double* src, double* dst, int to_soa, void* stream);
 
+/* Batched species block inverse of the coupled operator with chemistry:
+ * dinv_c = inv(d_c I - V_c dOmega_c) for N cells (implicit.py:362-368,
+ * numpy.linalg.inv per cell).  dOm, dinv: [n*n][N] (block row-major, cell
+ * minor); d, V: [N] (V may be NULL: 1).  n <= 23.  One thread per cell,
+ * in-place Gauss-Jordan with partial pivoting.  flags (device, may be NULL):
+ * the context flag-word layout; singular / non-finite blocks set EB_BLOCK. */
+int csb_batched_inverse(int n, long long N, const double* dOm, const double* d, const double* V,
+                        double* dinv, unsigned long long* flags, void* stream);
+
+/* FP64 pipe probe: 4 CTAs x 256 threads per SM, 8 independent DFMA chains
+ * per thread, iters x 128 DFMA each (2 flops per DFMA).  scratch: 1 double
+ * (device).  Used by bench.py as the measured FP64 peak of the roofline. */
+int csb_fp64_peak(int iters, double* scratch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

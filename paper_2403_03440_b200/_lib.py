@@ -54,6 +54,8 @@ SIGNATURES = {
     "csb_implicit_step_ex": (_i, [_p, _dp, _dp, _d, _i, _i, _dp, _dp, _dp, _i, _p]),
     "csb_iteration": (_i, [_p, _dp, _d, _i, _i, _i, _dp, _dp, _dp, _p]),
     "csb_transpose": (_i, [_ll, _i, _dp, _dp, _i, _p]),
+    "csb_batched_inverse": (_i, [_i, _ll, _dp, _dp, _dp, _dp, _dp, _p]),
+    "csb_fp64_peak": (_i, [_i, _dp, _p]),
 }
 
 _LIB = None

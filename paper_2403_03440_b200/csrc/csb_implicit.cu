@@ -1,5 +1,7 @@
 // csflow-b200: non-templated assembly kernels (reference implicit.py:176-197,
 // 362-368) and the bucket-independent launchers.
+#include <algorithm>
+
 #include "csb_common.cuh"
 #include "csb_kernels.cuh"
 
@@ -130,6 +132,161 @@ __global__ void k_block_inverse(int ns, GridDev g, OpDev op, unsigned long long*
   }
 }
 
+// ------------------------------------------ batched block inverse (thread/cell)
+// dinv = inv(d I - V dOmega) (implicit.py:362-368), one THREAD per cell: the
+// block lives in shared memory interleaved over the CTA's cells
+// (element e of cell l at sh[e * blk + l]: every access of a warp is one
+// contiguous 256-byte row, bank-conflict free), the pivot row in registers.
+// In-place Gauss-Jordan with partial pivoting (row swaps recorded, undone as
+// column swaps at the end): n^3 multiply-adds per cell, ~2 n^3 flops like
+// LAPACK getrf + getri behind numpy.linalg.inv.  Each multiply-add reads and
+// writes shared memory once, so the kernel runs at ~1/2 of the FP64 pipe rate
+// when it is not HBM-bound (2 n^2 doubles of traffic per cell).
+// dom: [n*n][N] (row-major block, cell-minor), d, V: [N] (V null: 1),
+// dinv: [n*n][N].  Singular / non-finite blocks raise EB_BLOCK.
+template <int NMAX>
+__global__ void k_block_inv_t(int n, long long N, const double* __restrict__ dom,
+                              const double* __restrict__ dd, const double* __restrict__ V,
+                              double* __restrict__ dinv, unsigned long long* flags) {
+  extern __shared__ double sh[];
+  const int blk = blockDim.x, l = threadIdx.x;
+  const int nn = n * n;
+  double* A = sh + l;                                       // element e at A[e * blk]
+  int* perm = reinterpret_cast<int*>(sh + (size_t)nn * blk) + l;  // pivot row of step k at perm[k * blk]
+  for (long long base = (long long)blockIdx.x * blk; base < N; base += (long long)gridDim.x * blk) {
+    const long long c = base + l;
+    if (c >= N) continue;
+    {
+      const double v = V ? __ldg(V + c) : 1.0;
+      const double d = __ldg(dd + c);
+      int e = 0;
+      for (int r = 0; r < n; ++r)
+        for (int cc = 0; cc < n; ++cc, ++e) {
+          const double vd = __ldg(dom + (long long)e * N + c) * v;
+          A[e * blk] = (r == cc ? d : 0.0) - vd;
+        }
+    }
+    bool singular = false;
+    for (int k = 0; k < n; ++k) {
+      // partial pivot: first row of largest |A[r][k]|, r >= k (LAPACK idamax)
+      int p = k;
+      double best = fabs(A[(k * n + k) * blk]);
+      for (int r = k + 1; r < n; ++r) {
+        const double a = fabs(A[(r * n + k) * blk]);
+        if (a > best) {
+          best = a;
+          p = r;
+        }
+      }
+      perm[k * blk] = p;
+      if (!(best > 0.0) || !isfinite(best)) singular = true;
+      // pivot row -> registers (swapped into row k), scaled by 1 / pivot
+      const double ip = 1.0 / A[(p * n + k) * blk];
+      double rowk[NMAX], rowo[NMAX];
+#pragma unroll
+      for (int cc = 0; cc < NMAX; ++cc) {
+        rowo[cc] = cc < n ? A[(k * n + cc) * blk] : 0.0;
+        rowk[cc] = cc < n ? A[(p * n + cc) * blk] : 0.0;
+      }
+#pragma unroll
+      for (int cc = 0; cc < NMAX; ++cc) {
+        if (cc < n) {
+          rowk[cc] = (cc == k ? 1.0 : rowk[cc]) * ip;
+          A[(p * n + cc) * blk] = rowo[cc];  // (p == k: rewritten below)
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < NMAX; ++cc)
+        if (cc < n) A[(k * n + cc) * blk] = rowk[cc];
+      // elimination: every row's loads are issued before its stores (the
+      // compiler cannot prove the strided smem accesses disjoint, so
+      // interleaved load / store would serialise on the smem latency)
+      for (int r = 0; r < n; ++r) {
+        if (r == k) continue;
+        double* Ar = A + (long long)r * n * blk;
+        double x[NMAX];
+#pragma unroll
+        for (int cc = 0; cc < NMAX; ++cc) x[cc] = cc < n ? Ar[cc * blk] : 0.0;
+        const double f = Ar[k * blk];
+#pragma unroll
+        for (int cc = 0; cc < NMAX; ++cc)
+          if (cc < n) Ar[cc * blk] = cc == k ? -f * rowk[cc] : fma(-f, rowk[cc], x[cc]);
+      }
+    }
+    // undo the row interchanges as column interchanges, last first
+    for (int k = n - 1; k >= 0; --k) {
+      const int p = perm[k * blk];
+      if (p != k)
+        for (int r = 0; r < n; ++r) {
+          const double t = A[(r * n + k) * blk];
+          A[(r * n + k) * blk] = A[(r * n + p) * blk];
+          A[(r * n + p) * blk] = t;
+        }
+    }
+    for (int e = 0; e < nn; ++e) {
+      const double x = A[e * blk];
+      if (!isfinite(x)) singular = true;
+      dinv[(long long)e * N + c] = x;
+    }
+    if (singular && flags) raise_flag(flags, EB_BLOCK, c);
+  }
+}
+
+// threads per CTA for the thread-per-cell inverse: the interleaved blocks
+// (+ pivot indices) of one CTA within ~220 KB of shared memory, 32 .. 256
+// cells; 0 when not even 32 cells fit (n > 23: warp-per-cell kernel)
+static int block_inv_threads(int n) {
+  const size_t per = (size_t)n * n * sizeof(double) + (size_t)n * sizeof(int);
+  int t = (int)std::min<size_t>(256, (220 * 1024) / per);
+  return t >= 32 ? (t / 32) * 32 : 0;
+}
+
+cudaError_t launch_block_inverse(int n, long long N, const double* dom, const double* d,
+                                 const double* V, double* dinv, unsigned long long* flags,
+                                 cudaStream_t st) {
+  const int bt = block_inv_threads(n);
+  if (bt == 0 || n > 32) return cudaErrorInvalidValue;
+  const size_t smem = ((size_t)n * n * sizeof(double) + (size_t)n * sizeof(int)) * bt;
+  const int blocks = (int)std::min<long long>((N + bt - 1) / bt, 148LL * 8);
+  note_launches(1);
+  if (n <= 8) {
+    cudaFuncSetAttribute(k_block_inv_t<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_block_inv_t<8><<<blocks, bt, smem, st>>>(n, N, dom, d, V, dinv, flags);
+  } else if (n <= 16) {
+    cudaFuncSetAttribute(k_block_inv_t<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_block_inv_t<16><<<blocks, bt, smem, st>>>(n, N, dom, d, V, dinv, flags);
+  } else {
+    cudaFuncSetAttribute(k_block_inv_t<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_block_inv_t<32><<<blocks, bt, smem, st>>>(n, N, dom, d, V, dinv, flags);
+  }
+  return cudaGetLastError();
+}
+
+// FP64 pipe peak probe: independent DFMA chains per thread, all SMs.
+__global__ void k_fp64_peak(int iters, double* out) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+  double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+  const double b = 0.9999999, cc = 1e-12;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, b, cc); a1 = fma(a1, b, cc); a2 = fma(a2, b, cc); a3 = fma(a3, b, cc);
+      a4 = fma(a4, b, cc); a5 = fma(a5, b, cc); a6 = fma(a6, b, cc); a7 = fma(a7, b, cc);
+    }
+  }
+  const double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+  if (r == 1234.5) out[0] = r;  // keeps the chains live
+}
+
+cudaError_t launch_fp64_peak(int iters, double* out, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  note_launches(1);
+  k_fp64_peak<<<sms * 4, 256, 0, st>>>(iters, out);
+  return cudaGetLastError();
+}
+
 // 2-D fast-path geometric precondition: i/j faces have zero
 // z-component, k faces are pure z and identical on both k planes.
 __global__ void k_check_2d(GridDev g, int* ok) {
@@ -169,7 +326,10 @@ cudaError_t launch_assemble(const Model* mp, int ns, const GridDev& g, const dou
   for (int d = 0; d < 3; ++d) k_assemble_face<<<grid_for(g.NF[d], 256), 256, 0, st>>>(g, op, d);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (op.mode == SCH_CI && op.chem) {
+  if (op.mode == SCH_CI && op.chem && ns <= 23) {
+    // dom_full layout [ns*ns][N]: the block of cell c, row-major (csb_implicit.cuh)
+    e = launch_block_inverse(ns, g.N, op.dom, op.d, g.vol, op.dinv, flags, st);
+  } else if (op.mode == SCH_CI && op.chem) {
     const int wpb = 4;
     const size_t smem = (size_t)wpb * ns * (2 * ns + 1) * sizeof(double);
     cudaFuncSetAttribute(k_block_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -108,6 +108,10 @@ cudaError_t launch_time_step(const Model* mp, int ns, const GridDev& g, const do
 cudaError_t launch_assemble(const Model* mp, int ns, const GridDev& g, const double* q,
                             const double* dtau, double theta, double dt, OpDev& op,
                             unsigned long long* flags, cudaStream_t st);
+cudaError_t launch_block_inverse(int n, long long N, const double* dom, const double* d,
+                                 const double* V, double* dinv, unsigned long long* flags,
+                                 cudaStream_t st);
+cudaError_t launch_fp64_peak(int iters, double* out, cudaStream_t st);
 cudaError_t launch_assemble_cell(const Model* mp, int ns, const GridDev& g, const double* q,
                                  const double* dtau, double theta, double dt, OpDev& op,
                                  unsigned long long* flags, cudaStream_t st);

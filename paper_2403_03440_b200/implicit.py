@@ -403,6 +403,36 @@ def _correct(mode, rho_s, d_rho_s, d_rho, eps_neg):
     return _out(eng, out, rho_s if is_torch(rho_s) else None, tuple(rs.shape))
 
 
+def species_block_inverse(d, V, dOmega):
+    """dinv = inv(d I - V dOmega) per cell: the coupled operator's species
+    block with chemistry (reference implicit.py:362-368, numpy.linalg.inv),
+    on the device as one batched call (csb_batched_inverse: one thread per
+    cell, in-place Gauss-Jordan with partial pivoting).  d, V: (N,);
+    dOmega: (N, ns, ns) with ns <= 23.  Raises SingularDiagonal like the
+    reference."""
+    eng = util_engine()
+    torch = eng.torch
+    dO = _dev(eng, dOmega)
+    if dO.dim() != 3 or dO.shape[1] != dO.shape[2]:
+        raise ValueError("dOmega must be (N, ns, ns)")
+    N, ns = int(dO.shape[0]), int(dO.shape[1])
+    if ns > 23:
+        raise ValueError("csb_batched_inverse handles ns <= 23 (one cell per thread in shared memory)")
+    blocks = dO.reshape(N, ns * ns).t().contiguous()
+    dd = _dev(eng, d).reshape(N).contiguous()
+    vv = _dev(eng, V).reshape(N).contiguous()
+    out = torch.empty((ns * ns, N), dtype=torch.float64, device=eng.device)
+    fl = torch.zeros(16, dtype=torch.int64, device=eng.device)
+    eng._chk(eng.lib.csb_batched_inverse(ns, N, blocks.data_ptr(), dd.data_ptr(), vv.data_ptr(),
+                                         out.data_ptr(), fl.data_ptr(), ctypes.c_void_p(eng.stream)),
+             "batched_inverse")
+    torch.cuda.synchronize()
+    if int(fl[0].item()) & (1 << 7):
+        raise SingularDiagonal("species diagonal block not invertible")
+    res = out.t().reshape(N, ns, ns).contiguous()
+    return _out(eng, res, dOmega if is_torch(dOmega) else None, (N, ns, ns))
+
+
 def correct_increment_cs1(rho_s, d_rho_s, d_rho, eps_neg: float = EPS_NEG):
     """First consistency correction (implicit.py:113-125)."""
     return _correct(1, rho_s, d_rho_s, d_rho, eps_neg)
@@ -414,4 +444,5 @@ def correct_normalize_cs2(rho_s, d_rho_s, d_rho, eps_neg: float = EPS_NEG):
 
 
 __all__ = ["MODES", "ImplicitOperator", "assemble_lhs", "cell_spectral_radii",
-           "correct_increment_cs1", "correct_normalize_cs2", "local_time_step", "SingularDiagonal"]
+           "correct_increment_cs1", "correct_normalize_cs2", "local_time_step", "SingularDiagonal",
+           "species_block_inverse"]

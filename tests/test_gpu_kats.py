@@ -289,3 +289,34 @@ def test_nonphysical_state_raises():
         spatial.assemble_residual(q, grid, all_faces(BC("farfield", freestream=inf)), None, model)
     with pytest.raises(P.NonPhysicalState):
         P.cons_to_prim(q, model)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ns", [2, 5, 11, 16, 20, 23])
+def test_species_block_inverse_matches_numpy_inv(ns):
+    """csb_batched_inverse against the reference's numpy.linalg.inv of
+    d I - V dOmega (implicit.py:362-368) on seeded blocks, including blocks
+    that need row pivoting."""
+    from paper_2403_03440_b200.implicit import species_block_inverse
+    rng = np.random.default_rng(100 + ns)
+    N = 1000
+    dOm = rng.normal(size=(N, ns, ns))
+    V = rng.uniform(0.5, 2.0, N)
+    d = rng.uniform(0.1, 3.0, N) * ns
+    d[:50] = 0.0  # zero diagonal: pivoting required
+    blk = d[:, None, None] * np.eye(ns) - V[:, None, None] * dOm
+    ref = np.linalg.inv(blk)
+    got = species_block_inverse(d, V, dOm)
+    cond = np.linalg.cond(blk)
+    err = np.max(np.abs(got - ref), axis=(1, 2)) / np.max(np.abs(ref), axis=(1, 2))
+    assert np.all(err <= 1e-13 * np.maximum(cond, 1.0)), float(np.max(err / np.maximum(cond, 1.0)))
+
+
+@pytest.mark.gpu
+def test_species_block_inverse_singular_raises():
+    from paper_2403_03440_b200.errors import SingularDiagonal
+    from paper_2403_03440_b200.implicit import species_block_inverse
+    ns = 4
+    dOm = np.zeros((3, ns, ns))
+    with pytest.raises(SingularDiagonal):
+        species_block_inverse(np.array([1.0, 0.0, 1.0]), np.ones(3), dOm)
