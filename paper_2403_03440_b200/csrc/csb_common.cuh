@@ -205,21 +205,23 @@ struct Cell {
 
 // Decode conservative vector q[c*stride] into primitives.  Returns false on
 // the reference's NonPhysicalState conditions (rho, Y < -eps, T).
-template <int NSB>
-CSB_DEV bool decode(const Model& m, const double* __restrict__ q, long long stride, Cell<NSB>& o) {
+// QK(k) returns component k (a pointer read or a register array element:
+// the register form keeps the caller's array out of local memory).
+template <int NSB, class QK>
+CSB_DEV bool decode_from(const Model& m, QK qk, Cell<NSB>& o) {
   const int ns = m.ns;
-  const double rho = q[0];
+  const double rho = qk(0);
   bool ok = (rho > 0.0) && finite(rho);
   // reciprocal multiplies instead of divisions (last-ulp differences only)
   const double ir = 1.0 / rho;
   o.rho = rho;
 #pragma unroll
-  for (int x = 0; x < 3; ++x) o.u[x] = q[(1 + x) * stride] * ir;
+  for (int x = 0; x < 3; ++x) o.u[x] = qk(1 + x) * ir;
   double sum = 0.0;
 #pragma unroll
   for (int s = 0; s < NSB; ++s) {
     if (s < ns) {
-      double y = q[(5 + s) * stride] * ir;
+      double y = qk(5 + s) * ir;
       if (y < -EPS_NEG) ok = false;
       if (y < 0.0) y = 0.0;
       o.Y[s] = y;
@@ -243,7 +245,7 @@ CSB_DEV bool decode(const Model& m, const double* __restrict__ q, long long stri
   o.Ek = 0.5 * ((o.u[0] * o.u[0] + o.u[1] * o.u[1]) + o.u[2] * o.u[2]);
   const double cv = cp - R;
   const double icv = 1.0 / cv;
-  const double e_int = q[4 * stride] * ir - o.Ek;
+  const double e_int = qk(4) * ir - o.Ek;
   o.T = (e_int - yb) * icv;
   if (!(o.T > 0.0) || !finite(o.T)) ok = false;
   o.R = R;
@@ -253,6 +255,11 @@ CSB_DEV bool decode(const Model& m, const double* __restrict__ q, long long stri
   o.c = sqrt(o.gamma * R * o.T);
   o.h = yb + cp * o.T + o.Ek;
   return ok;
+}
+
+template <int NSB>
+CSB_DEV bool decode(const Model& m, const double* __restrict__ q, long long stride, Cell<NSB>& o) {
+  return decode_from<NSB>(m, [&](int k) { return q[k * stride]; }, o);
 }
 
 // Transport (mixture.py:354-372): mu, k, D (D identical for all species).

@@ -1010,7 +1010,7 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
 // phase B: closure + gate column by column, so the q / q_new accesses of a
 // warp are contiguous runs of up to C cells.
 template <int NSB>
-__global__ void __launch_bounds__(256, 2) k_epilogue2d(const Model* __restrict__ mp, GridDev g, Skew sk,
+__global__ void __launch_bounds__(256, NSB <= 8 ? 3 : 2) k_epilogue2d(const Model* __restrict__ mp, GridDev g, Skew sk,
                                                     int scheme, const double* __restrict__ q,
                                                     const double* __restrict__ fw,
                                                     const double* __restrict__ sw,
@@ -1049,8 +1049,11 @@ __global__ void __launch_bounds__(256, 2) k_epilogue2d(const Model* __restrict__
 #pragma unroll
     for (int k = 0; k < 5 + NSB; ++k)
       if (k < nv) d[k] = es[k * CT + e];
-    if (dq_std)
-      for (int k = 0; k < nv; ++k) dq_std[(long long)k * N + c] = d[k];
+    if (dq_std) {
+#pragma unroll
+      for (int k = 0; k < 5 + NSB; ++k)
+        if (k < nv) dq_std[(long long)k * N + c] = d[k];
+    }
     // all q loads first (memory-level parallelism), closure in registers, the
     // gate decodes the new state from registers (no read-back of q_new)
     const double* qc = q + c;
@@ -1070,9 +1073,14 @@ __global__ void __launch_bounds__(256, 2) k_epilogue2d(const Model* __restrict__
           tail += o[5 + sp];
         }
       const double lastv = o[0] - tail;
+      // bitwise select (a guarded store here becomes one dynamically indexed
+      // store, which moves o[] to local memory)
 #pragma unroll
-      for (int sp = 0; sp < NSB; ++sp)
-        if (sp == ns - 1) o[5 + sp] = lastv;
+      for (int sp = 0; sp < NSB; ++sp) {
+        const unsigned long long msk = 0ull - (unsigned long long)(sp == ns - 1);
+        o[5 + sp] = __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(o[5 + sp]) & ~msk) |
+                                                     ((unsigned long long)__double_as_longlong(lastv) & msk)));
+      }
       ok1 = !(lastv < -1e-10 * o[0]);
     } else {
       double tot = 0.0, dsum = 0.0;
@@ -1110,7 +1118,7 @@ __global__ void __launch_bounds__(256, 2) k_epilogue2d(const Model* __restrict__
     for (int k = 0; k < 5 + NSB; ++k)
       if (k < nv) qo[k * N] = o[k];
     Cell<NSB> cs;
-    const bool ok2 = decode<NSB>(m, o, 1, cs);
+    const bool ok2 = decode_from<NSB>(m, [&](int k) { return o[k]; }, cs);
     if (!ok1 && first1 == ~0ull) first1 = (unsigned long long)c;
     if (!ok2 && first2 == ~0ull) first2 = (unsigned long long)c;
     if (!(ok1 && ok2)) ++bad_count;
