@@ -465,13 +465,17 @@ CSB_DEV bool face_visc2d(const Model& m, const double* sP, int ldP, int im, int 
 
 template <int NSB, int D>
 CSB_DEV void visc_pass2d(const Model& m, const GridDev& g, const double* sP, int ldP, double* sF,
-                         int maxf, int i0, int j0, int ci, int cj, int BY,
+                         int maxf, int i0, int j0, int ci, int cj, int BY, int TIc, int TJc,
                          unsigned long long* flags) {
+  // faces enumerated over the full tile shape (compile-time divisor when the
+  // tile is fixed), faces beyond a partial edge tile skipped
+  const int FX = TIc + (D == 0), FY = TJc + (D == 1);
   const int fx = ci + (D == 0), fy = cj + (D == 1);
-  const int nf = fx * fy;
+  const int nf = FX * FY;
   const int sd = D == 0 ? BY : 1, st = D == 0 ? 1 : BY;
   for (int f = threadIdx.x; f < nf; f += blockDim.x) {
-    const int fj = f % fy, fi = f / fy;
+    const int fj = f % FY, fi = f / FY;
+    if (fi >= fx || fj >= fy) continue;
     const int ip = (fi + NG) * BY + (fj + NG);
     const int im = ip - sd;
     const int gi = i0 + fi, gj = j0 + fj;
@@ -546,12 +550,16 @@ CSB_DEV void omega_cell(const Model& m, const Mech& mech, double T, const double
 // residual kernel
 // ----------------------------------------------------------------------------
 
-template <int NSB, bool K2D>
+// FTI, FTJ: compile-time 2-D tile (0: runtime TI_, TJ_).  With a fixed tile
+// every shared-memory plane stride and face / cell index divisor is a
+// constant, which removes most of the integer address arithmetic.
+template <int NSB, bool K2D, int FTI = 0, int FTJ = 0>
 __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ mp, GridDev g, BCDev bc,
                                                   Mech mech, const double* __restrict__ q,
-                                                  double* __restrict__ R, int first_order, int TI,
-                                                  int TJ, int TK, unsigned long long* flags,
+                                                  double* __restrict__ R, int first_order, int TI_,
+                                                  int TJ_, int TK, unsigned long long* flags,
                                                   NormsOut nrm, int sr_on) {
+  const int TI = FTI ? FTI : TI_, TJ = FTJ ? FTJ : TJ_;
   extern __shared__ double smem[];
   __shared__ Model sm;
   {
@@ -633,14 +641,21 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
   const int strideX = K2D ? BY : BY * BZ, strideY = K2D ? 1 : BZ, strideZ = 1;
   const int ndir = K2D ? 2 : 3;
 
+#pragma unroll 1
   for (int d = 0; d < ndir; ++d) {
-    // faces of direction d inside the tile: dims (ci+1, cj, ck) etc.
+    // faces of direction d inside the tile: dims (ci+1, cj, ck) etc.  2-D:
+    // enumerated over the full tile (FY columns; constant with a fixed tile),
+    // faces beyond a partial edge tile skipped; the flux buffer uses the
+    // same full-tile face index
     const int fx = ci + (d == 0), fy = cj + (d == 1), fz = ck + (d == 2);
-    const int nf = fx * fy * fz;
+    const int FY = K2D ? TJ + (d == 1) : fy;
+    const int nf = K2D ? (TI + (d == 0)) * FY : fx * fy * fz;
     for (int f = threadIdx.x; f < nf; f += blockDim.x) {
-      const int fk = f % fz;
-      const int fj = (f / fz) % fy;
-      const int fi = f / (fz * fy);
+      // (d == 1 ? ... : ...) keeps both divisors compile-time with a fixed tile
+      const int fk = K2D ? 0 : f % fz;
+      const int fj = K2D ? (d == 1 ? f % (TJ + 1) : f % TJ) : (f / fz) % fy;
+      const int fi = K2D ? (d == 1 ? f / (TJ + 1) : f / TJ) : f / (fz * fy);
+      if (K2D && (fi >= fx || fj >= fy)) continue;
       // local (staged) coordinates of the "p" cell (upper side of the face)
       int lx = fi + NG, ly = fj + NG, lz = K2D ? 0 : fk + NG;
       const int sd = d == 0 ? strideX : (d == 1 ? strideY : strideZ);
@@ -661,8 +676,8 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
     }
     // viscous pass over the same faces (same thread -> face map: no barrier)
     if (K2D) {
-      if (d == 0) visc_pass2d<NSB, 0>(m, g, sP, ldP, sF, maxf, i0, j0, ci, cj, BY, flags);
-      else visc_pass2d<NSB, 1>(m, g, sP, ldP, sF, maxf, i0, j0, ci, cj, BY, flags);
+      if (d == 0) visc_pass2d<NSB, 0>(m, g, sP, ldP, sF, maxf, i0, j0, ci, cj, BY, TI, TJ, flags);
+      else visc_pass2d<NSB, 1>(m, g, sP, ldP, sF, maxf, i0, j0, ci, cj, BY, TI, TJ, flags);
     } else {
     for (int f = threadIdx.x; f < nf; f += blockDim.x) {
       const int fk = f % fz;
@@ -721,20 +736,24 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
     }
     }
     __syncthreads();
-    // difference into R (R = 0 + dR_0 + dR_1 + dR_2, spatial.py:258-259)
-    const int ncell = ci * cj * ck;
+    // difference into R (R = 0 + dR_0 + dR_1 + dR_2, spatial.py:258-259);
+    // 2-D: cells over the full tile (index ii * TJ + jj, also the sR index)
+    const int ncell = K2D ? TI * TJ : ci * cj * ck;
     for (int l = threadIdx.x; l < ncell; l += blockDim.x) {
-      const int kk = l % ck, jj = (l / ck) % cj, ii = l / (ck * cj);
+      const int kk = K2D ? 0 : l % ck;
+      const int jj = K2D ? l % TJ : (l / ck) % cj;
+      const int ii = K2D ? l / TJ : l / (ck * cj);
+      if (K2D && (ii >= ci || jj >= cj)) continue;
       const long long cell = cell_index(g, i0 + ii, j0 + jj, k0 + kk);
       int flo, fhi;
       if (d == 0) {
-        flo = (ii * fy + jj) * fz + kk;
-        fhi = ((ii + 1) * fy + jj) * fz + kk;
+        flo = (ii * FY + jj) * fz + kk;
+        fhi = ((ii + 1) * FY + jj) * fz + kk;
       } else if (d == 1) {
-        flo = (ii * fy + jj) * fz + kk;
-        fhi = (ii * fy + jj + 1) * fz + kk;
+        flo = (ii * FY + jj) * fz + kk;
+        fhi = (ii * FY + jj + 1) * fz + kk;
       } else {
-        flo = (ii * fy + jj) * fz + kk;
+        flo = (ii * FY + jj) * fz + kk;
         fhi = flo + 1;
       }
       for (int c = 0; c < nv; ++c) {
@@ -750,9 +769,12 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
   // chemistry source (spatial.py:261-267), the finite check (269-271) and,
   // when requested, the residual norms (driver.py:85-90)
   double n_flow = 0.0, n_sp = 0.0, n_rho = 0.0;
-  const int ncell = ci * cj * ck;
+  const int ncell = K2D ? TI * TJ : ci * cj * ck;
   for (int l = threadIdx.x; l < ncell; l += blockDim.x) {
-    const int kk = l % ck, jj = (l / ck) % cj, ii = l / (ck * cj);
+    const int kk = K2D ? 0 : l % ck;
+    const int jj = K2D ? l % TJ : (l / ck) % cj;
+    const int ii = K2D ? l / TJ : l / (ck * cj);
+    if (K2D && (ii >= ci || jj >= cj)) continue;
     const long long cell = cell_index(g, i0 + ii, j0 + jj, k0 + kk);
     if (mech.nrx > 0) {
       const int ls = lidx(ii + NG, jj + NG, K2D ? 0 : kk + NG);
@@ -874,17 +896,25 @@ static inline void pick_tile(int ns, bool k2d, int nk, int& TI, int& TJ, int& TK
   const int nc = 6 + ns, nv = 5 + ns;
   const size_t budget = 200 * 1024;
   if (k2d) {
-    int cand[][2] = {{15, 16}, {7, 16}, {7, 8}, {3, 8}, {3, 4}, {1, 4}};
+    // the largest tile that keeps 2 CTAs per SM (<= 104 KB), else the largest
+    // that fits (measured: ns = 20 on a 15 x 16 tile at 1 CTA/SM is 3x slower
+    // per cell than ns = 11)
+    // (tiles below 7 x 16 cells lose more to the halo than they gain:
+    // ns = 40 on 7 x 8 at 2 CTAs/SM is 20% slower than 7 x 16 at one)
+    int cand[][2] = {{15, 16}, {11, 16}, {7, 16}, {7, 8}, {3, 8}, {3, 4}, {1, 4}};
     if (const char* e = getenv("CSB_RHS_TILE")) sscanf(e, "%d,%d", &cand[0][0], &cand[0][1]);
-    for (auto& c : cand) {
-      TI = c[0];
-      TJ = c[1];
-      TK = 1;
-      const size_t ldP = (size_t)(TI + 4) * (TJ + 4);
-      const size_t maxf = std::max((size_t)(TI + 1) * TJ, (size_t)TI * (TJ + 1));
-      smem = (ldP * nc + maxf * nv) * sizeof(double);
-      if (smem <= budget) return;
-    }
+    for (int pass = 0; pass < 2; ++pass)
+      for (auto& c : cand) {
+        TI = c[0];
+        TJ = c[1];
+        TK = 1;
+        if (pass == 0 && TI * TJ < 112) break;
+        if (pass == 1 && TI == 11) continue;
+        const size_t ldP = (size_t)(TI + 4) * (TJ + 4);
+        const size_t maxf = std::max((size_t)(TI + 1) * TJ, (size_t)TI * (TJ + 1));
+        smem = (ldP * nc + maxf * nv) * sizeof(double);
+        if (smem <= (pass == 0 ? (size_t)104 * 1024 : budget)) return;
+      }
   } else {
     const int cand[][3] = {{6, 8, 4}, {4, 4, 4}, {4, 4, 2}, {2, 4, 2}, {2, 2, 2}, {1, 2, 1}};
     for (auto& c : cand) {
@@ -926,7 +956,7 @@ cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, c
   cudaError_t err = cudaSuccess;
   CSB_NS_DISPATCH(ns, {
     if (k2d) {
-      auto kfn = k_residual<NSB, true>;
+      auto kfn = TI == 15 && TJ == 16 ? k_residual<NSB, true, 15, 16> : k_residual<NSB, true>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       kfn<<<(unsigned)ntiles, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
                                                nrm, sr_on);
