@@ -1305,11 +1305,15 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
                          !getenv("CSB_NO_OVERLAP");
     cudaError_t e;
     if (overlap) {
+      // the records kernel is submitted FIRST: the sweep only ever waits for
+      // a kernel that is already running or queued ahead of it, so the step
+      // cannot deadlock even where kernels are serialised (ncu replay,
+      // CUDA_LAUNCH_BLOCKING) -- it then simply runs in the serial order
       cudaEventRecord(wb.e1, st);
-      cudaStreamWaitEvent(wb.s2, wb.e1, 0);
-      e = launch_pass(false, wb.s2, wb.rdy);  // first: its CTAs take their SMs
-      if (e != cudaSuccess) return e;
       launch_records(st);
+      cudaStreamWaitEvent(wb.s2, wb.e1, 0);
+      e = launch_pass(false, wb.s2, wb.rdy);
+      if (e != cudaSuccess) return e;
       cudaEventRecord(wb.e2, wb.s2);
       cudaStreamWaitEvent(st, wb.e2, 0);
     } else {
