@@ -204,6 +204,7 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
     c->wb.hand = k.take<double>((size_t)2 * sk.nstrip * (sk.T + 2 * HPAD) * (5 + nsb));
     c->wb.prog = k.take<int>(2);
     c->wb.rdy = k.take<int>((size_t)sk.nstrip * sk.T);
+    c->wb.nonplanar = k.take<int>(1);
     c->wb.nsI = 0;
     c->wave_ok = true;
   }
@@ -226,6 +227,7 @@ int zero_wave_records(csb_ctx* c, cudaStream_t st) {
       return 1;
   if (cudaMemsetAsync(w.rdy, 0, (size_t)w.sk.nstrip * w.sk.T * sizeof(int), st) != cudaSuccess)
     return 1;
+  if (cudaMemsetAsync(w.nonplanar, 0, sizeof(int), st) != cudaSuccess) return 1;
   return 0;
 }
 

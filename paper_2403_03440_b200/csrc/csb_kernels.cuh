@@ -63,6 +63,7 @@ struct WaveBufs {
   // concurrently on the high-priority stream s2 and its TMA producer waits
   // for the tiles of each ring slot (csb_wave.cuh)
   int* rdy;       // [nstrip][T] (tiles of >= 1 step)
+  int* nonplanar; // == epoch when the step is not planar (csb_wave.cuh k_hand_reset)
   int epoch;      // this launch's tag (incremented per implicit step)
   cudaStream_t s2;
   cudaEvent_t e1, e2;

@@ -127,7 +127,18 @@ CSB_DEV long long gaddr(const Skew& k, int NG, int s, int t, int p, int r) {
 // ============================================================== hand-off reset
 // Both sweeps' strip hand-off rows: signalling-NaN sentinel in the data rows,
 // zero in the HPAD pad rows (one thread per row).
-static __global__ void k_hand_reset(double* __restrict__ hand, int nstrip, int T, int nhf, int nhs) {
+static __global__ void k_hand_reset(double* __restrict__ hand, int nstrip, int T, int nhf, int nhs,
+                                    long long N, const double* __restrict__ q3,
+                                    const double* __restrict__ R3, int* flag, int epoch) {
+  // planarity of the step (chain_flow PL): epoch stored when any cell has a
+  // nonzero (or non-finite) z-momentum q3 or z-momentum residual R3
+  {
+    bool bad = false;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < N;
+         c += (long long)gridDim.x * blockDim.x)
+      bad |= !(q3[c] == 0.0) || !(R3[c] == 0.0);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = epoch;
+  }
   const int rows = T + 2 * HPAD;
   const long long nrow = 2LL * 2 * nstrip * rows;  // [sweep][role][strip][row]
   const double sent = __longlong_as_double((long long)HAND_SENTINEL);
@@ -476,6 +487,7 @@ struct WaveArgs {
   int ci;            // coupled operator: one CI chain per strip (role[0])
   int poll_ns;       // receiver back-off between empty polls
   const int* rdy;    // forward sweep overlapped with the records kernel: tile flags (or null)
+  const int* nonplanar;  // == epoch: some cell has z-momentum or its residual != 0 (or null)
   int epoch, rC;     // their launch tag and the records tile length (steps)
   unsigned long long* dbg;  // timing probe: [CTA][4] globaltimer stamps (or null)
   WaveRole role[2];  // 0 flow, 1 species
@@ -517,7 +529,11 @@ CSB_DEV void st_pred_cg_f64(double* p, double v, bool pred) {
 }
 
 // flow chain: 5 coupled components per row (rank-2 half blocks)
-template <bool BWD>
+// PL (planar): every cell has z-momentum 0 and z-momentum residual 0 this
+// step (checked by k_hand_reset), so the component-3 records (w3, b3, rhs3) are zero
+// and dq3, oi3, oj3 stay exactly zero: the chain skips component 3 (8 fewer
+// FP64 operations, a shuffle and 4 shared-memory loads per step).
+template <bool BWD, bool PL>
 CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
   constexpr int WK = WKF, NG = 30;
   constexpr int FQ = BWD ? 11 : 16;                         // first face plane
@@ -546,6 +562,10 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
       double ij[5];
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
+        if (PL && c == 3) {
+          ij[c] = 0.0;
+          continue;
+        }
         const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
         ij[c] = fma(sh, x.mul, hv[c]);
       }
@@ -553,14 +573,23 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
       double dq[5];
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
+        if (PL && c == 3) {
+          dq[c] = 0.0;
+          if (BWD) ob[(kk * NGO + c) * 32] = 0.0;  // the epilogue reads dq3
+          continue;
+        }
         if (BWD) dq[c] = p[(FB_DQ + c) * 32] - (oi[c] + ij[c]) * invd;
         else dq[c] = ((p[(11 + c) * 32] + oi[c]) + ij[c]) * invd;
         ob[(kk * NGO + c) * 32] = dq[c];
       }
-      const double w0 = p[1 * 32], w1 = p[2 * 32], w2 = p[3 * 32], w3 = p[4 * 32], w4 = p[5 * 32];
+      const double w0 = p[1 * 32], w1 = p[2 * 32], w2 = p[3 * 32], w3 = PL ? 0.0 : p[4 * 32],
+                   w4 = p[5 * 32];
       // balanced sums: short dependency chains behind dq
-      const double sb = ((p[6 * 32] * dq[0] + p[7 * 32] * dq[1]) +
-                         (p[8 * 32] * dq[2] + p[9 * 32] * dq[3])) + p[10 * 32] * dq[4];
+      const double sb = PL ? ((p[6 * 32] * dq[0] + p[7 * 32] * dq[1]) + p[8 * 32] * dq[2]) +
+                                 p[10 * 32] * dq[4]
+                           : ((p[6 * 32] * dq[0] + p[7 * 32] * dq[1]) +
+                              (p[8 * 32] * dq[2] + p[9 * 32] * dq[3])) +
+                                 p[10 * 32] * dq[4];
 #pragma unroll
       for (int f = 0; f < 2; ++f) {
         const double* pf = p + (FQ + 7 * f) * 32;
@@ -570,11 +599,12 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
         o[0] = w0 * sa + sig * dq[0];
         o[1] = w1 * sa + pf[3 * 32] * sb + sig * dq[1];
         o[2] = w2 * sa + pf[4 * 32] * sb + sig * dq[2];
-        o[3] = w3 * sa + sig * dq[3];
+        o[3] = PL ? 0.0 : w3 * sa + sig * dq[3];
         o[4] = w4 * sa + pf[5 * 32] * sb + sig * dq[4];
       }
 #pragma unroll
-      for (int c = 0; c < 5; ++c) st_pred_cg_f64(ho + kk * 5 + c, oj[c], x.send);
+      for (int c = 0; c < 5; ++c)
+        if (!(PL && c == 3)) st_pred_cg_f64(ho + kk * 5 + c, oj[c], x.send);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&x.empty_bar[buf]);
@@ -943,6 +973,8 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
     // all loaded at once, and the slot is released when none is the sentinel.
     const double* src = ro.hand + ((long long)up * (T + 2 * HPAD) + HPAD) * nh;
     const int nw = WK * nh;  // words per slot (<= 256)
+    // planar step: the flow chains neither send nor read hand-off word 3
+    const bool skip3 = BWD && kind == 0 && a.nonplanar && ld_relaxed(a.nonplanar) != a.epoch;
     int buf = 0, phase = 0;
     for (int ks = 0; ks < x.nslots; ++ks) {
       const int k = BWD ? x.nslots - 1 - ks : ks;
@@ -959,8 +991,13 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
         for (int r = 0; r < 8; ++r) {
           const int e = lane + 32 * r;
           if (e < nw && !(have >> r & 1u)) {
-            w[r] = (unsigned long long)__ldcg(sw + e);
-            if (w[r] != HAND_SENTINEL) have |= 1u << r;
+            if (skip3 && e % nh == 3) {
+              w[r] = 0ull;
+              have |= 1u << r;
+            } else {
+              w[r] = (unsigned long long)__ldcg(sw + e);
+              if (w[r] != HAND_SENTINEL) have |= 1u << r;
+            }
           }
         }
         if (__all_sync(0xffffffffu, (have & need) == need)) break;
@@ -986,7 +1023,13 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
   unsigned long long t0 = 0;
   if (a.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   if (kind == 0) {
-    chain_flow<BWD>(x, ro);
+    // planarity of this step: k_hand_reset stores the launch epoch on
+    // any nonzero z-momentum or z-momentum residual
+    // (backward sweep only -- measured: the planar forward chain is faster on
+    // one strip, 147 -> 130 ns per step, but its multi-strip pipeline is
+    // slower, 512^2 199 -> 216 us; the planar backward sweep gains 207 -> 200)
+    if (BWD && a.nonplanar && ld_relaxed(a.nonplanar) != a.epoch) chain_flow<BWD, true>(x, ro);
+    else chain_flow<BWD, false>(x, ro);
   } else if (kind == 1) {
     chain_species<NSB, BWD, PER>(x, ro, warp);
   } else {
@@ -1222,6 +1265,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       wa.poll_ns = 16;
       if (const char* ev_p = getenv("CSB_POLL_NS")) wa.poll_ns = atoi(ev_p);  // tuning probe
       wa.rdy = rdy;
+      wa.nonplanar = getenv("CSB_NO_PLANAR") ? nullptr : wb.nonplanar;  // (tuning probe)
       wa.epoch = wb.epoch;
       wa.rC = C;
       wa.dbg = nullptr;
@@ -1295,8 +1339,9 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     };
     // ---------------- the step
     note_launches(1);
-    k_hand_reset<<<grid_for(4LL * sk.nstrip * hrows, 256), 256, 0, st>>>(
-        wb.hand, sk.nstrip, sk.T, ci ? NV : 5, ci ? 0 : NSB);
+    k_hand_reset<<<grid_for(std::max(4LL * sk.nstrip * hrows, g.N), 256), 256, 0, st>>>(
+        wb.hand, sk.nstrip, sk.T, ci ? NV : 5, ci ? 0 : NSB, g.N, q + 3 * g.N, R + 3 * g.N,
+        wb.nonplanar, wb.epoch);
     // measured: the overlap pays while the sweeps hold a small share of the
     // SMs (512^2: 32 of 148 SMs, 0.649 -> 0.587 ms per iteration); at 1024^2
     // (64 SMs) the concurrent records tiles slow the chains more than they hide

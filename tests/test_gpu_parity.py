@@ -201,6 +201,23 @@ def test_wavefront_matches_generic_ogrid_and_chemistry():
     _wave_vs_generic(C.config3(40, dims=(30, 70, 1)), "CI")
 
 
+def test_wavefront_nonplanar_matches_generic():
+    """w != 0 on a 2-D grid (outflow k boundaries): the flow chains take the
+    full 5-component path (the planar path is skipped when any z-momentum or
+    its residual is nonzero)."""
+    from paper_2403_03440_b200 import configs as C
+    spec = C.config0(seed=11, dims=(40, 70, 1))
+    spec.bcs["kmin"] = C.BCSpec("supersonic_outflow")
+    spec.bcs["kmax"] = C.BCSpec("supersonic_outflow")
+    rng = np.random.default_rng(5)
+    rho = spec.q[..., 0]
+    w = rng.uniform(-300.0, 300.0, rho.shape)
+    spec.q[..., 3] = rho * w
+    spec.q[..., 4] += 0.5 * rho * w * w
+    for scheme in ("CS1", "CI"):
+        _wave_vs_generic(spec, scheme)
+
+
 # ---------------------------------------------------------------- fused iteration (bench path)
 
 @pytest.mark.parametrize("dims", [(96, 80, 1), (33, 70, 1)])
