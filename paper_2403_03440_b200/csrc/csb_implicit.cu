@@ -144,89 +144,108 @@ __global__ void k_block_inverse(int ns, GridDev g, OpDev op, unsigned long long*
 // when it is not HBM-bound (2 n^2 doubles of traffic per cell).
 // dom: [n*n][N] (row-major block, cell-minor), d, V: [N] (V null: 1),
 // dinv: [n*n][N].  Singular / non-finite blocks raise EB_BLOCK.
-template <int NMAX>
-__global__ void k_block_inv_t(int n, long long N, const double* __restrict__ dom,
+template <int NS>
+__global__ void k_block_inv_t(long long N, const double* __restrict__ dom,
                               const double* __restrict__ dd, const double* __restrict__ V,
                               double* __restrict__ dinv, unsigned long long* flags) {
+  // NS = block size, compile-time: every column loop is straight-line code
+  // (with a runtime n the guarded loops cost ~25 instructions per element)
+  constexpr int n = NS, nn = NS * NS;
   extern __shared__ double sh[];
   const int blk = blockDim.x, l = threadIdx.x;
-  const int nn = n * n;
   double* A = sh + l;                                       // element e at A[e * blk]
   int* perm = reinterpret_cast<int*>(sh + (size_t)nn * blk) + l;  // pivot row of step k at perm[k * blk]
   for (long long base = (long long)blockIdx.x * blk; base < N; base += (long long)gridDim.x * blk) {
     const long long c = base + l;
     if (c >= N) continue;
     {
+      // 8 independent global loads in flight per thread (a load -> store
+      // loop would serialise on the DRAM latency, one element at a time)
       const double v = V ? __ldg(V + c) : 1.0;
       const double d = __ldg(dd + c);
-      int e = 0;
-      for (int r = 0; r < n; ++r)
-        for (int cc = 0; cc < n; ++cc, ++e) {
-          const double vd = __ldg(dom + (long long)e * N + c) * v;
-          A[e * blk] = (r == cc ? d : 0.0) - vd;
+#pragma unroll 1
+      for (int e0 = 0; e0 < nn; e0 += 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e0 + u < nn) x[u] = __ldg(dom + (long long)(e0 + u) * N + c);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u;
+          if (e < nn) A[e * blk] = (e % (n + 1) == 0 ? d : 0.0) - x[u] * v;
         }
+      }
     }
     bool singular = false;
     for (int k = 0; k < n; ++k) {
       // partial pivot: first row of largest |A[r][k]|, r >= k (LAPACK idamax)
       int p = k;
-      double best = fabs(A[(k * n + k) * blk]);
-      for (int r = k + 1; r < n; ++r) {
-        const double a = fabs(A[(r * n + k) * blk]);
-        if (a > best) {
-          best = a;
-          p = r;
-        }
+      double best = -1.0;
+      {
+        double col[NS];
+#pragma unroll
+        for (int r = 0; r < NS; ++r) col[r] = fabs(A[(r * n + k) * blk]);
+#pragma unroll
+        for (int r = 0; r < NS; ++r)
+          if (r >= k && col[r] > best) {
+            best = col[r];
+            p = r;
+          }
       }
       perm[k * blk] = p;
       if (!(best > 0.0) || !isfinite(best)) singular = true;
       // pivot row -> registers (swapped into row k), scaled by 1 / pivot
       const double ip = 1.0 / A[(p * n + k) * blk];
-      double rowk[NMAX], rowo[NMAX];
+      double rowk[NS], rowo[NS];
 #pragma unroll
-      for (int cc = 0; cc < NMAX; ++cc) {
-        rowo[cc] = cc < n ? A[(k * n + cc) * blk] : 0.0;
-        rowk[cc] = cc < n ? A[(p * n + cc) * blk] : 0.0;
+      for (int cc = 0; cc < NS; ++cc) {
+        rowo[cc] = A[(k * n + cc) * blk];
+        rowk[cc] = A[(p * n + cc) * blk];
       }
 #pragma unroll
-      for (int cc = 0; cc < NMAX; ++cc) {
-        if (cc < n) {
-          rowk[cc] = (cc == k ? 1.0 : rowk[cc]) * ip;
-          A[(p * n + cc) * blk] = rowo[cc];  // (p == k: rewritten below)
-        }
+      for (int cc = 0; cc < NS; ++cc) {
+        rowk[cc] = (cc == k ? 1.0 : rowk[cc]) * ip;
+        A[(p * n + cc) * blk] = rowo[cc];  // (p == k: rewritten below)
       }
 #pragma unroll
-      for (int cc = 0; cc < NMAX; ++cc)
-        if (cc < n) A[(k * n + cc) * blk] = rowk[cc];
+      for (int cc = 0; cc < NS; ++cc) A[(k * n + cc) * blk] = rowk[cc];
       // elimination: every row's loads are issued before its stores (the
       // compiler cannot prove the strided smem accesses disjoint, so
       // interleaved load / store would serialise on the smem latency)
       for (int r = 0; r < n; ++r) {
         if (r == k) continue;
         double* Ar = A + (long long)r * n * blk;
-        double x[NMAX];
+        double x[NS];
 #pragma unroll
-        for (int cc = 0; cc < NMAX; ++cc) x[cc] = cc < n ? Ar[cc * blk] : 0.0;
-        const double f = Ar[k * blk];
+        for (int cc = 0; cc < NS; ++cc) x[cc] = Ar[cc * blk];
+        const double f = Ar[k * blk];  // (x[k] would be a dynamic register index)
 #pragma unroll
-        for (int cc = 0; cc < NMAX; ++cc)
-          if (cc < n) Ar[cc * blk] = cc == k ? -f * rowk[cc] : fma(-f, rowk[cc], x[cc]);
+        for (int cc = 0; cc < NS; ++cc) Ar[cc * blk] = cc == k ? -f * rowk[cc] : fma(-f, rowk[cc], x[cc]);
       }
     }
     // undo the row interchanges as column interchanges, last first
     for (int k = n - 1; k >= 0; --k) {
       const int p = perm[k * blk];
       if (p != k)
-        for (int r = 0; r < n; ++r) {
+#pragma unroll
+        for (int r = 0; r < NS; ++r) {
           const double t = A[(r * n + k) * blk];
           A[(r * n + k) * blk] = A[(r * n + p) * blk];
           A[(r * n + p) * blk] = t;
         }
     }
-    for (int e = 0; e < nn; ++e) {
-      const double x = A[e * blk];
-      if (!isfinite(x)) singular = true;
-      dinv[(long long)e * N + c] = x;
+#pragma unroll 1
+    for (int e0 = 0; e0 < nn; e0 += 8) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e0 + u < nn) x[u] = A[(e0 + u) * blk];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (e0 + u < nn) {
+          if (!isfinite(x[u])) singular = true;
+          dinv[(long long)(e0 + u) * N + c] = x[u];
+        }
     }
     if (singular && flags) raise_flag(flags, EB_BLOCK, c);
   }
@@ -245,19 +264,24 @@ cudaError_t launch_block_inverse(int n, long long N, const double* dom, const do
                                  const double* V, double* dinv, unsigned long long* flags,
                                  cudaStream_t st) {
   const int bt = block_inv_threads(n);
-  if (bt == 0 || n > 32) return cudaErrorInvalidValue;
+  if (bt == 0 || n > 23) return cudaErrorInvalidValue;
   const size_t smem = ((size_t)n * n * sizeof(double) + (size_t)n * sizeof(int)) * bt;
   const int blocks = (int)std::min<long long>((N + bt - 1) / bt, 148LL * 8);
   note_launches(1);
-  if (n <= 8) {
-    cudaFuncSetAttribute(k_block_inv_t<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_block_inv_t<8><<<blocks, bt, smem, st>>>(n, N, dom, d, V, dinv, flags);
-  } else if (n <= 16) {
-    cudaFuncSetAttribute(k_block_inv_t<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_block_inv_t<16><<<blocks, bt, smem, st>>>(n, N, dom, d, V, dinv, flags);
-  } else {
-    cudaFuncSetAttribute(k_block_inv_t<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_block_inv_t<32><<<blocks, bt, smem, st>>>(n, N, dom, d, V, dinv, flags);
+  switch (n) {
+#define CSB_BLKINV(NS)                                                                       \
+  case NS:                                                                                   \
+    cudaFuncSetAttribute(k_block_inv_t<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                         (int)smem);                                                         \
+    k_block_inv_t<NS><<<blocks, bt, smem, st>>>(N, dom, d, V, dinv, flags);                  \
+    break;
+    CSB_BLKINV(1) CSB_BLKINV(2) CSB_BLKINV(3) CSB_BLKINV(4) CSB_BLKINV(5) CSB_BLKINV(6)
+    CSB_BLKINV(7) CSB_BLKINV(8) CSB_BLKINV(9) CSB_BLKINV(10) CSB_BLKINV(11) CSB_BLKINV(12)
+    CSB_BLKINV(13) CSB_BLKINV(14) CSB_BLKINV(15) CSB_BLKINV(16) CSB_BLKINV(17) CSB_BLKINV(18)
+    CSB_BLKINV(19) CSB_BLKINV(20) CSB_BLKINV(21) CSB_BLKINV(22) CSB_BLKINV(23)
+#undef CSB_BLKINV
+    default:
+      return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
