@@ -50,6 +50,10 @@
 namespace csb {
 
 constexpr int HRING = 128;  // hand-off ring (steps)
+#ifndef CSB_CHAIN_UNROLL
+#define CSB_CHAIN_UNROLL 8
+#endif
+constexpr int CHAIN_UNROLL = CSB_CHAIN_UNROLL;  // steps of a ring slot unrolled in the chains
 // signalling NaN marking a hand-off word not yet written (see the chains)
 constexpr unsigned long long HAND_SENTINEL = 0x7FF4DEADBEEF0001ull;
 constexpr int NFF = 30, NFB = 30, FB_DQ = 25;
@@ -524,11 +528,38 @@ struct ChainCtx {
 // predicated store without a branch (a branch would end the scheduling region
 // of the unrolled step loop)
 CSB_DEV void st_pred_cg_f64(double* p, double v, bool pred) {
-  asm("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.cg.f64 [%0], %1;\n}" ::"l"(p), "d"(v),
-      "r"((int)pred));
+  asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.cg.f64 [%0], %1;\n}" ::"l"(p),
+               "d"(v), "r"((int)pred));
 }
 
 // flow chain: 5 coupled components per row (rank-2 half blocks)
+// Lane shuffles of the chains as volatile asm: volatile asm statements keep
+// their order, so the hand-off stores of step m (st_pred_cg_f64, also
+// volatile) stay ahead of the shuffles of step m + 1 instead of being sunk to
+// the end of the unrolled slot (measured in SASS: ~5 steps late, which adds
+// directly to the strip-to-strip lag).  No memory clobber: the records loads
+// and dq stores still schedule freely around them.
+template <bool DOWN>
+CSB_DEV double shfl1_f64(double v) {
+  double r;
+  if constexpr (DOWN) {
+    asm volatile(
+        "{\n.reg .b32 lo, hi;\nmov.b64 {lo, hi}, %1;\n"
+        "shfl.sync.down.b32 lo, lo, 1, 0x1f, 0xffffffff;\n"
+        "shfl.sync.down.b32 hi, hi, 1, 0x1f, 0xffffffff;\nmov.b64 %0, {lo, hi};\n}"
+        : "=d"(r)
+        : "d"(v));
+  } else {
+    asm volatile(
+        "{\n.reg .b32 lo, hi;\nmov.b64 {lo, hi}, %1;\n"
+        "shfl.sync.up.b32 lo, lo, 1, 0x0, 0xffffffff;\n"
+        "shfl.sync.up.b32 hi, hi, 1, 0x0, 0xffffffff;\nmov.b64 %0, {lo, hi};\n}"
+        : "=d"(r)
+        : "d"(v));
+  }
+  return r;
+}
+
 // PL (planar): every cell has z-momentum 0 and z-momentum residual 0 this
 // step (checked by k_hand_reset), so the component-3 records (w3, b3, rhs3) are zero
 // and dq3, oi3, oj3 stay exactly zero: the chain skips component 3 (8 fewer
@@ -551,7 +582,7 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
     double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO) * 32 + lane;
     const double* hb = x.recv ? x.hin + ((k * WK) % HRING) * 5 : x.hin + HRING * 5;
     double* ho = x.hand_out + (long long)k * WK * 5;
-#pragma unroll
+#pragma unroll (CHAIN_UNROLL)
     for (int m = 0; m < WK; ++m) {
       const int kk = BWD ? WK - 1 - m : m;
       const double* p = base + kk * NG * 32;
@@ -566,7 +597,7 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
           ij[c] = 0.0;
           continue;
         }
-        const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
+        const double sh = shfl1_f64<BWD>(oj[c]);
         ij[c] = fma(sh, x.mul, hv[c]);
       }
       const double invd = p[0];
@@ -655,7 +686,7 @@ CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro, int grp) {
     double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO + c0) * 32 + lane;
     const double* hb = (x.recv ? x.hin + ((k * WK) % HRING) * NSB : x.hin + HRING * NSB) + c0;
     double* ho = x.hand_out + (long long)k * WK * NSB + c0;
-#pragma unroll
+#pragma unroll (CHAIN_UNROLL)
     for (int m = 0; m < WK; ++m) {
       const int kk = BWD ? WK - 1 - m : m;
       const double* p = base + kk * NG * 32;
@@ -663,7 +694,7 @@ CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro, int grp) {
       double ij[SG];
 #pragma unroll
       for (int c = 0; c < SG; ++c) {
-        const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
+        const double sh = shfl1_f64<BWD>(oj[c]);
         ij[c] = fma(sh, x.mul, hv[c]);
       }
       const double ci = p[PC * 32], cj = p[(PC + 1) * 32];
@@ -724,7 +755,7 @@ CSB_DEV void chain_ci(const ChainCtx& x, const WaveRole& ro) {
       double ij[NV];
 #pragma unroll
       for (int c = 0; c < NV; ++c) {
-        const double sh = BWD ? __shfl_down_sync(FULL, oj[c], 1) : __shfl_up_sync(FULL, oj[c], 1);
+        const double sh = shfl1_f64<BWD>(oj[c]);
         ij[c] = fma(sh, x.mul, hv[c]);
       }
       const double invd = p[0], hr2 = p[32];
