@@ -195,6 +195,44 @@ CSB_DEV bool face_state(const Model& m, const double* W, double& T, double& c, d
   return ok;
 }
 
+// face_state with the species sums R = sum Y_s R_s, cp = sum Y_s cp_s,
+// yb = sum Y_s b_s supplied by the caller (accumulated in species order from
+// 0, i.e. bit-identical to face_state's own loop)
+CSB_DEV bool face_state_sums(double W0, double W1, double W2, double W3, double W4, double R,
+                             double cp, double yb, double& T, double& c, double& et) {
+  T = W4 / (W0 * R);
+  const bool ok = (T > 0.0) && finite(T);
+  const double gamma = cp / (cp - R);
+  c = sqrt(gamma * R * T);
+  const double Ek = 0.5 * ((W1 * W1 + W2 * W2) + W3 * W3);
+  et = yb + (cp - R) * T + Ek;
+  return ok;
+}
+
+// MUSCL-minmod face values of staged component c (spatial.py:217-226)
+CSB_DEV void muscl_pair(const double* sP, int ldP, int imm, int im, int ip, int ipp, int c,
+                        bool first_order, double& l, double& r) {
+  const double vm = sP[c * ldP + im];
+  const double vp = sP[c * ldP + ip];
+  if (first_order) {
+    l = vm;
+    r = vp;
+  } else {
+    const double vmm = sP[c * ldP + imm];
+    const double vpp = sP[c * ldP + ipp];
+    const double dc = vp - vm;
+    l = vm + 0.5 * minmod(vm - vmm, dc);
+    r = vp - 0.5 * minmod(dc, vpp - vp);
+  }
+}
+
+// Large species counts (NSB > 12): the face passes stream the species
+// instead of holding 2 x (5 + NSB) face values in registers (which spilled:
+// ns = 40 residual 6.7 ms per 10^6 cells); species values are recomputed per
+// pass from shared memory with the same arithmetic, so results are identical.
+template <int NSB>
+constexpr bool stream_species() { return NSB > 12; }
+
 // Face flux = convective part (face_conv, writes F) + viscous part
 // (face_visc, adds to F), evaluated in two passes so that their register
 // footprints do not add up.  sP: staged padded primitives, component plane
@@ -209,6 +247,54 @@ CSB_DEV bool face_conv(const Model& m, const double* sP, int ldP, int imm, int i
   const int ns = m.ns;
   const int nv = 5 + ns;
   bool ok = true;
+  if constexpr (stream_species<NSB>()) {
+    double WL[5], WR[5];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) muscl_pair(sP, ldP, imm, im, ip, ipp, c, first_order, WL[c], WR[c]);
+    double RL = 0.0, cpL = 0.0, ybL = 0.0, RR = 0.0, cpR = 0.0, ybR = 0.0;
+    for (int sp = 0; sp < ns; ++sp) {
+      double yl, yr;
+      muscl_pair(sP, ldP, imm, im, ip, ipp, 5 + sp, first_order, yl, yr);
+      RL += yl * m.Rs[sp];
+      cpL += yl * m.cp[sp];
+      ybL += yl * m.bs[sp];
+      RR += yr * m.Rs[sp];
+      cpR += yr * m.cp[sp];
+      ybR += yr * m.bs[sp];
+    }
+    double TL, cL, eL, TR, cR, eR;
+    ok &= face_state_sums(WL[0], WL[1], WL[2], WL[3], WL[4], RL, cpL, ybL, TL, cL, eL);
+    ok &= face_state_sums(WR[0], WR[1], WR[2], WR[3], WR[4], RR, cpR, ybR, TR, cR, eR);
+    const double UL = WL[1] * S[0] + WL[2] * S[1] + WL[3] * S[2];
+    const double UR = WR[1] * S[0] + WR[2] * S[1] + WR[3] * S[2];
+    const double area = sqrt((S[0] * S[0] + S[1] * S[1]) + S[2] * S[2]);
+    const double lam = npmax(fabs(UL) + cL * area, fabs(UR) + cR * area);
+    const double hl = 0.5 * lam;
+    {
+      const double qL = WL[0], qR = WR[0];
+      F[0] = 0.5 * (UL * qL + UR * qR) - hl * (qR - qL);
+    }
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      const double qL = WL[0] * WL[1 + x], qR = WR[0] * WR[1 + x];
+      const double fl = UL * qL + WL[4] * S[x];
+      const double fr = UR * qR + WR[4] * S[x];
+      F[(1 + x) * ldF] = 0.5 * (fl + fr) - hl * (qR - qL);
+    }
+    {
+      const double qL = WL[0] * eL, qR = WR[0] * eR;
+      const double fl = UL * qL + WL[4] * UL;
+      const double fr = UR * qR + WR[4] * UR;
+      F[4 * ldF] = 0.5 * (fl + fr) - hl * (qR - qL);
+    }
+    for (int sp = 0; sp < ns; ++sp) {
+      double yl, yr;
+      muscl_pair(sP, ldP, imm, im, ip, ipp, 5 + sp, first_order, yl, yr);
+      const double qL = WL[0] * yl, qR = WR[0] * yr;
+      F[(5 + sp) * ldF] = 0.5 * (UL * qL + UR * qR) - hl * (qR - qL);
+    }
+    return ok;
+  }
   double WL[5 + NSB], WR[5 + NSB];
 #pragma unroll
   for (int c = 0; c < 5 + NSB; ++c) {
@@ -396,6 +482,83 @@ CSB_DEV bool face_visc2d(const Model& m, const double* sP, int ldP, int im, int 
                          int ldF) {
   const int ns = m.ns;
   const int nv = 5 + ns;
+  if constexpr (stream_species<NSB>()) {
+    auto wf = [&](int c) { return 0.5 * (sP[c * ldP + im] + sP[c * ldP + ip]); };
+    const double W0 = wf(0), W1 = wf(1), W2 = wf(2), W3 = wf(3), W4 = wf(4);
+    double R = 0.0, cpf = 0.0, yb = 0.0;
+    for (int sp = 0; sp < ns; ++sp) {
+      const double y = wf(5 + sp);
+      R += y * m.Rs[sp];
+      cpf += y * m.cp[sp];
+      yb += y * m.bs[sp];
+    }
+    double Tf, cf, ef;
+    const bool ok = face_state_sums(W0, W1, W2, W3, W4, R, cpf, yb, Tf, cf, ef);
+    const double rho = W0;
+    // transport (mixture.py:354-372) with the species streamed; cp is the
+    // same species sum as the face state's
+    double acc = 0.0;
+    if (m.suth_shared) {
+      const double xx = Tf * m.inv_T_mu[0];
+      const double Fs = (xx * sqrt(xx)) * m.TS[0] / (Tf + m.S_mu[0]);
+      for (int sp = 0; sp < ns; ++sp) acc += wf(5 + sp) * (m.mu_ref[sp] * Fs);
+    } else {
+      for (int sp = 0; sp < ns; ++sp) acc += wf(5 + sp) * mu_species(m, sp, Tf);
+    }
+    const double mu = acc, kc = mu * cpf / m.Pr, Dm = mu / (rho * m.Sc);
+    double tS[3];
+    {
+      double gu[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) face_grad2d<D>(sP, ldP, im, ip, st, xn, xt, 1 + i, gu[i]);
+      const double div = (gu[0][0] + gu[1][1]) + gu[2][2];
+      const double tdiv = 2.0 / 3.0 * mu * div;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+          double tau = mu * (gu[i][x] + gu[x][i]);
+          if (x == i) tau -= tdiv;
+          a = (x == 0) ? tau * S[0] : a + tau * S[x];
+        }
+        tS[i] = a;
+      }
+    }
+    const double nrd = -(rho * Dm);
+    double jsum[3] = {0.0, 0.0, 0.0};
+    for (int sp = 0; sp < ns; ++sp) {
+      double gy[3];
+      face_grad2d<D>(sP, ldP, im, ip, st, xn, xt, 5 + sp, gy);
+#pragma unroll
+      for (int x = 0; x < 3; ++x) jsum[x] += nrd * gy[x];
+    }
+    double hsj[3] = {0.0, 0.0, 0.0};
+    for (int sp = 0; sp < ns; ++sp) {
+      double gy[3], js[3];
+      face_grad2d<D>(sP, ldP, im, ip, st, xn, xt, 5 + sp, gy);
+      const double hs = m.bs[sp] + m.cp[sp] * Tf;
+      const double y = wf(5 + sp);
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        js[x] = nrd * gy[x] - y * jsum[x];
+        hsj[x] += hs * js[x];
+      }
+      F[(5 + sp) * ldF] += (js[0] * S[0] + js[1] * S[1]) + js[2] * S[2];
+    }
+    double gT[3];
+    face_grad2d<D>(sP, ldP, im, ip, st, xn, xt, 5 + ns, gT);
+    double qv[3];
+#pragma unroll
+    for (int x = 0; x < 3; ++x) qv[x] = -kc * gT[x] + hsj[x];
+    F[1 * ldF] += -tS[0];
+    F[2 * ldF] += -tS[1];
+    F[3 * ldF] += -tS[2];
+    const double utS = (W1 * tS[0] + W2 * tS[1]) + W3 * tS[2];
+    const double qS = (qv[0] * S[0] + qv[1] * S[1]) + qv[2] * S[2];
+    F[4 * ldF] += -utS + qS;
+    return ok;
+  }
   double Wf[5 + NSB];
 #pragma unroll
   for (int c = 0; c < 5 + NSB; ++c) Wf[c] = c < nv ? 0.5 * (sP[c * ldP + im] + sP[c * ldP + ip]) : 0.0;
