@@ -770,7 +770,49 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
     const bool inside_pad = pi < g.ni + 2 * NG && pj < g.nj + 2 * NG && pk < g.nk + 2 * NG;
     const bool interior = inside_pad && pi >= NG && pi < g.ni + NG && pj >= NG &&
                           pj < g.nj + NG && pk >= NG && pk < g.nk + NG;
-    if (interior) {
+    if (interior && stream_species<NSB>()) {
+      // large species counts: decode_from's arithmetic with the mass
+      // fractions written straight to (and renormalised in) shared memory
+      const long long cell = cell_index(g, pi - NG, pj - NG, pk - NG);
+      const double* qc = q + cell;
+      const long long N = g.N;
+      const double rho = qc[0];
+      bool ok = (rho > 0.0) && finite(rho);
+      const double ir = 1.0 / rho;
+      double u[3];
+#pragma unroll
+      for (int x = 0; x < 3; ++x) u[x] = qc[(1 + x) * N] * ir;
+      double sum = 0.0;
+      for (int sp = 0; sp < ns; ++sp) {
+        double y = qc[(5 + sp) * N] * ir;
+        if (y < -EPS_NEG) ok = false;
+        if (y < 0.0) y = 0.0;
+        sP[(5 + sp) * ldP + l] = y;
+        sum += y;
+      }
+      double R = 0.0, cp = 0.0, yb = 0.0;
+      const double isum = 1.0 / sum;
+      for (int sp = 0; sp < ns; ++sp) {
+        const double y = sP[(5 + sp) * ldP + l] * isum;
+        sP[(5 + sp) * ldP + l] = y;
+        R += y * m.Rs[sp];
+        cp += y * m.cp[sp];
+        yb += y * m.bs[sp];
+      }
+      const double Ek = 0.5 * ((u[0] * u[0] + u[1] * u[1]) + u[2] * u[2]);
+      const double icv = 1.0 / (cp - R);
+      const double e_int = qc[4 * N] * ir - Ek;
+      const double T = (e_int - yb) * icv;
+      if (!(T > 0.0) || !finite(T)) ok = false;
+      if (!ok) raise_flag(flags, EB_DECODE, cell);
+      if (K2D && bc.kind[4] == BC_SYMMETRY && qc[3 * N] != 0.0) raise_flag(flags, EB_KSKIP, cell);
+      sP[0 * ldP + l] = rho;
+      sP[1 * ldP + l] = u[0];
+      sP[2 * ldP + l] = u[1];
+      sP[3 * ldP + l] = u[2];
+      sP[4 * ldP + l] = rho * R * T;
+      sP[(5 + ns) * ldP + l] = T;
+    } else if (interior) {
       const long long cell = cell_index(g, pi - NG, pj - NG, pk - NG);
       Cell<NSB> cs;
       if (!decode<NSB>(m, q + cell, g.N, cs)) raise_flag(flags, EB_DECODE, cell);

@@ -1214,6 +1214,7 @@ __global__ void __launch_bounds__(256, NSB <= 8 ? 3 : 2) k_epilogue2d(const Mode
 // large species counts keep 4 CTAs per SM
 inline int epilogue_steps(int ns) {
   int ce = 16;
+  if (const char* e = getenv("CSB_EPI_C")) ce = atoi(e);  // tuning probe
   while (ce > 2 && (size_t)(5 + ns) * ce * 32 * sizeof(double) > 48 * 1024) ce /= 2;
   return ce;
 }
