@@ -998,6 +998,35 @@ __global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ m
         }
     }
     bool fin = true;
+    if constexpr (stream_species<NSB>()) {
+      // large species counts: one component at a time (same sums, same order)
+      double f = 0.0, sp = 0.0, r0 = 0.0;
+      for (int c = 0; c < nv; ++c) {
+        double v;
+        if (sr_on) {
+          v = sR[c * ncell + l];
+          R[(long long)c * g.N + cell] = v;
+        } else {
+          v = R[(long long)c * g.N + cell];
+        }
+        fin &= finite(v);
+        if (c == 0) {
+          r0 = v;
+          f = v * v;
+        } else if (c < 5) {
+          f += v * v;
+        } else {
+          sp += v;
+        }
+      }
+      if (!fin) raise_flag(flags, EB_RES_NONFINITE, cell);
+      if (nrm.out) {
+        n_flow += f;
+        n_sp += sp * sp;
+        n_rho += r0 * r0;
+      }
+      continue;
+    }
     double rv[5 + NSB];
 #pragma unroll
     for (int c = 0; c < 5 + NSB; ++c)
