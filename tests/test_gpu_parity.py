@@ -220,8 +220,8 @@ def test_wavefront_nonplanar_matches_generic():
 
 # ---------------------------------------------------------------- fused iteration (bench path)
 
-@pytest.mark.parametrize("dims", [(96, 80, 1), (33, 70, 1)])
-def test_fused_iteration_matches_stages_and_oracle(dims):
+@pytest.mark.parametrize("dims,ns", [((96, 80, 1), 5), ((33, 70, 1), 5), ((40, 66, 1), 20)])
+def test_fused_iteration_matches_stages_and_oracle(dims, ns):
     """csb_iteration (residual with fused norms + implicit step, the bench's
     per-step call) against the separate stage entry points and the oracle's
     residual_norms (driver.py:85-90)."""
@@ -232,7 +232,8 @@ def test_fused_iteration_matches_stages_and_oracle(dims):
     from paper_2403_03440_b200.device import SCHEMES, get_engine
     from paper_2403_03440_b200.driver import residual_norms
 
-    spec = C.config0(seed=5, dims=dims)
+    # ns = 20: the species-streaming residual (NSB > 12) with fused norms
+    spec = C.config0(seed=5, dims=dims) if ns == 5 else C.config3(ns, seed=5, dims=dims)
     grid, model, bcs, mech = build_case(spec)
     eng = get_engine(grid, model)
     eng.set_bcs(bcs)
