@@ -1378,7 +1378,8 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     // SMs (512^2: 32 of 148 SMs, 0.649 -> 0.587 ms per iteration); at 1024^2
     // (64 SMs) the concurrent records tiles slow the chains more than they hide
     // (2.23 -> 2.35 ms at ns = 11)
-    const bool overlap = !ev && wb.s2 && only == -1 && 2 * sk.nstrip <= 48 &&
+    const bool overlap = !ev && wb.s2 && only == -1 &&
+                         (2 * sk.nstrip <= 48 || getenv("CSB_FORCE_OVERLAP")) &&
                          !getenv("CSB_NO_OVERLAP");
     cudaError_t e;
     if (overlap) {
