@@ -57,7 +57,13 @@ constexpr int CHAIN_UNROLL = CSB_CHAIN_UNROLL;  // steps of a ring slot unrolled
 // signalling NaN marking a hand-off word not yet written (see the chains)
 constexpr unsigned long long HAND_SENTINEL = 0x7FF4DEADBEEF0001ull;
 constexpr int NFF = 30, NFB = 30, FB_DQ = 25;
-constexpr int WKF = 8;     // flow slot: 8 steps x 30 planes = 60 KiB (measured: 4 is slower)
+#ifndef CSB_WKF
+#define CSB_WKF 8
+#endif
+#ifndef CSB_DMAX
+#define CSB_DMAX 4
+#endif
+constexpr int WKF = CSB_WKF;  // flow slot: 8 steps x 30 planes = 60 KiB (measured: 4 is slower)
 
 // Coupled (CI, frozen chemistry) records, NV = 5 + NSB components:
 //   CF (forward)  invd, hr2, w[NV], b[NV], rhs[NV], upper faces (e[3], sig) x 2
@@ -1224,7 +1230,7 @@ inline size_t wave_role_smem(int D, int WK, int NG, int nh) {
 }
 // deepest ring (2..4) that fits the shared-memory budget, 0 if none
 inline int wave_depth(int WK, int NG, int nh) {
-  for (int D = 4; D >= 2; --D)
+  for (int D = CSB_DMAX; D >= 2; --D)
     if (wave_role_smem(D, WK, NG, nh) <= 210 * 1024) return D;
   return 0;
 }
@@ -1262,7 +1268,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       if (!Dc) return cudaErrorInvalidConfiguration;
     } else {
       Df = wave_depth(WKF, NFF, 5);
-      for (int D = 4; D >= 2 && !Ds; --D)
+      for (int D = CSB_DMAX; D >= 2 && !Ds; --D)
         if (wave_role_smem(D, WKS, NSF, NSB) <= 210 * 1024) Ds = D;
       if (!Df || !Ds) return cudaErrorInvalidConfiguration;
     }
