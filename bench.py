@@ -402,7 +402,7 @@ def fp64_peak_tflops(lib, torch):
     return flops / (a.elapsed_time(b) * 1e-3) / 1e12
 
 
-def block_lu(hbm_peak, nss=(5, 11, 20), N=1 << 20, reps=5):
+def block_lu(hbm_peak, nss=(5, 11, 20, 32), N=1 << 20, reps=5):
     """Batched species block inverse inv(d I - V dOmega) of the coupled
     operator with chemistry (reference implicit.py:362-368) on N = 2^20 cells
     (config-3 cell count) per ns: achieved FP64 TFLOP/s (2 n^3 flops per

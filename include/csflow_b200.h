@@ -204,8 +204,9 @@ int csb_transpose(long long N, int nv, const double* src, double* dst, int to_so
 /* Batched species block inverse of the coupled operator with chemistry:
  * dinv_c = inv(d_c I - V_c dOmega_c) for N cells (implicit.py:362-368,
  * numpy.linalg.inv per cell).  dOm, dinv: [n*n][N] (block row-major, cell
- * minor); d, V: [N] (V may be NULL: 1).  n <= 23.  One thread per cell,
- * in-place Gauss-Jordan with partial pivoting.  flags (device, may be NULL):
+ * minor); d, V: [N] (V may be NULL: 1).  n <= 32.  n <= 23: one thread per
+ * cell (block in shared memory); 24 <= n <= 32: one warp per cell, lane =
+ * column in registers.  In-place Gauss-Jordan with partial pivoting.  flags (device, may be NULL):
  * the context flag-word layout; singular / non-finite blocks set EB_BLOCK. */
 int csb_batched_inverse(int n, long long N, const double* dOm, const double* d, const double* V,
                         double* dinv, unsigned long long* flags, void* stream);

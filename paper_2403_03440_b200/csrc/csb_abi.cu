@@ -804,7 +804,7 @@ int csb_transpose(long long N, int nv, const double* src, double* dst, int to_so
 
 int csb_batched_inverse(int n, long long N, const double* dOm, const double* d, const double* V,
                         double* dinv, unsigned long long* flags, void* stream) {
-  if (n < 1 || n > 23 || N < 0 || !dOm || !d || !dinv) return CSB_E_BADARG;
+  if (n < 1 || n > 32 || N < 0 || !dOm || !d || !dinv) return CSB_E_BADARG;
   if (N == 0) return CSB_OK;
   return launch_block_inverse(n, N, dOm, d, V, dinv, flags, S(stream)) == cudaSuccess ? CSB_OK
                                                                                       : CSB_E_CUDA;

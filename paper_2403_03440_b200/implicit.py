@@ -407,8 +407,9 @@ def species_block_inverse(d, V, dOmega):
     """dinv = inv(d I - V dOmega) per cell: the coupled operator's species
     block with chemistry (reference implicit.py:362-368, numpy.linalg.inv),
     on the device as one batched call (csb_batched_inverse: one thread per
-    cell, in-place Gauss-Jordan with partial pivoting).  d, V: (N,);
-    dOmega: (N, ns, ns) with ns <= 23.  Raises SingularDiagonal like the
+    cell up to 23 species, one warp per cell from 24 to 32; in-place
+    Gauss-Jordan with partial pivoting).  d, V: (N,);
+    dOmega: (N, ns, ns) with ns <= 32.  Raises SingularDiagonal like the
     reference."""
     eng = util_engine()
     torch = eng.torch
@@ -416,8 +417,8 @@ def species_block_inverse(d, V, dOmega):
     if dO.dim() != 3 or dO.shape[1] != dO.shape[2]:
         raise ValueError("dOmega must be (N, ns, ns)")
     N, ns = int(dO.shape[0]), int(dO.shape[1])
-    if ns > 23:
-        raise ValueError("csb_batched_inverse handles ns <= 23 (one cell per thread in shared memory)")
+    if ns > 32:
+        raise ValueError("csb_batched_inverse handles ns <= 32")
     blocks = dO.reshape(N, ns * ns).t().contiguous()
     dd = _dev(eng, d).reshape(N).contiguous()
     vv = _dev(eng, V).reshape(N).contiguous()

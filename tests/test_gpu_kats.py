@@ -292,7 +292,7 @@ def test_nonphysical_state_raises():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("ns", [2, 5, 11, 16, 20, 23])
+@pytest.mark.parametrize("ns", [2, 5, 8, 11, 16, 20, 23, 32])
 def test_species_block_inverse_matches_numpy_inv(ns):
     """csb_batched_inverse against the reference's numpy.linalg.inv of
     d I - V dOmega (implicit.py:362-368) on seeded blocks, including blocks
