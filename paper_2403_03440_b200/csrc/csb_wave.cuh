@@ -80,9 +80,12 @@ constexpr int CI_MAXNSB = 16;  // register-resident CI chain up to here; smem-re
 
 // species slot length: <= 64 KiB per slot at the widest layout (nsI = NSB)
 template <int NSB>
+#ifndef CSB_SP_SLOT_KB
+#define CSB_SP_SLOT_KB 100  // measured: 100 KB slots (8 steps up to ns = 24, 2-deep ring) beat 64 KB (4-step slots) by 7-8% at ns = 16-40
+#endif
 constexpr int wave_wks() {
   int w = 8;  // also the hand-off granularity (a slot starts when its columns are in)
-  while (w > 1 && w * (2 * NSB + 2) * 256 > 64 * 1024) w /= 2;
+  while (w > 1 && w * (2 * NSB + 2) * 256 > CSB_SP_SLOT_KB * 1024) w /= 2;
   return w;
 }
 
