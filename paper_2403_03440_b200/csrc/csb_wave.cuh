@@ -71,9 +71,15 @@ constexpr int WKF = CSB_WKF;  // flow slot: 8 steps x 30 planes = 60 KiB (measur
 template <int NSB>
 constexpr int ci_planes() { return 3 * (5 + NSB) + 10; }
 template <int NSB>
+#ifndef CSB_CI_SLOT_KB
+#define CSB_CI_SLOT_KB 100  // measured: 512^2 CI 0.842 -> 0.817 ms against 64 KB (8-step slots at ns = 5)
+#endif
 constexpr int ci_wk() {
+  // (the larger slots only for the register chain: the smem-resident chain
+  // above CI_MAXNSB also needs its state next to the ring)
+  const int kb = NSB <= 16 ? CSB_CI_SLOT_KB : 64;
   int w = 8;
-  while (w > 1 && w * ci_planes<NSB>() * 256 > 64 * 1024) w /= 2;
+  while (w > 1 && w * ci_planes<NSB>() * 256 > kb * 1024) w /= 2;
   return w;
 }
 constexpr int CI_MAXNSB = 16;  // register-resident CI chain up to here; smem-resident above
