@@ -717,7 +717,10 @@ CSB_DEV void omega_cell(const Model& m, const Mech& mech, double T, const double
 // every shared-memory plane stride and face / cell index divisor is a
 // constant, which removes most of the integer address arithmetic.
 template <int NSB, bool K2D, int FTI = 0, int FTJ = 0>
-__global__ void __launch_bounds__(256, 2) k_residual(const Model* __restrict__ mp, GridDev g, BCDev bc,
+#ifndef CSB_RES_MINB
+#define CSB_RES_MINB 2  // measured: 3 CTAs/SM (80 registers, spills) is 12-29% slower
+#endif
+__global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __restrict__ mp, GridDev g, BCDev bc,
                                                   Mech mech, const double* __restrict__ q,
                                                   double* __restrict__ R, int first_order, int TI_,
                                                   int TJ_, int TK, unsigned long long* flags,
