@@ -505,6 +505,7 @@ struct WaveArgs {
   int only;          // -1: both roles (production); 0/1: one role (timing probe)
   int ci;            // coupled operator: one CI chain per strip (role[0])
   int poll_ns;       // receiver back-off between empty polls
+  int fake_recv;     // probe: strips without upstream still get a receiver arrival per slot
   const int* rdy;    // forward sweep overlapped with the records kernel: tile flags (or null)
   const int* nonplanar;  // == epoch: some cell has z-momentum or its residual != 0 (or null)
   int epoch, rC;     // their launch tag and the records tile length (steps)
@@ -963,7 +964,7 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
   x.empty_bar = empty_bar;
   if (threadIdx.x == 0) {
     for (int b = 0; b < D; ++b) {
-      mbar_init(&full_bar[b], x.has_up ? 2 : 1);  // TMA producer (+ hand-off receiver)
+      mbar_init(&full_bar[b], (x.has_up || a.fake_recv) ? 2 : 1);  // TMA producer (+ hand-off receiver)
       mbar_init(&empty_bar[b], nchain);  // every chain warp releases the slot
     }
     for (int c = 0; c < WK * nh; ++c) hin[HRING * nh + c] = 0.0;
@@ -1010,7 +1011,20 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
     // For each ring slot: the upstream columns its steps need (one per lane,
     // at most WK <= 32), polled until complete, copied into hin, then one
     // arrival on the slot's full barrier (release: the chain's wait acquires).
-    if (!x.has_up) return;
+    if (!x.has_up) {
+      if (a.fake_recv) {  // probe: arrive per slot without any data
+        int buf = 0, phase = 0;
+        for (int ks = 0; ks < x.nslots; ++ks) {
+          if (ks >= D) mbar_wait(&empty_bar[buf], phase ^ 1);
+          if (lane == 0) mbar_arrive(&full_bar[buf]);
+          if (++buf == D) {
+            buf = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      return;
+    }
     // upstream row u of the hand-off buffer holds what the upstream strip's
     // sending row produced at its step u; our receiving row needs, at our step
     // t, the upstream step t + 31 (forward: upstream row 31 -> our row 0) or
@@ -1372,6 +1386,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       wa.only = ci ? -1 : only;
       wa.poll_ns = 16;
       if (const char* ev_p = getenv("CSB_POLL_NS")) wa.poll_ns = atoi(ev_p);  // tuning probe
+      wa.fake_recv = getenv("CSB_FAKE_RECV") ? 1 : 0;                         // timing probe
       wa.rdy = rdy;
       wa.nonplanar = getenv("CSB_NO_PLANAR") ? nullptr : wb.nonplanar;  // (tuning probe)
       wa.epoch = wb.epoch;
