@@ -48,7 +48,10 @@ extern "C" {
 #define CSB_F_ZERO_WAVE (1u << 3)
 #define CSB_F_SINGULAR (1u << 4)
 #define CSB_F_GATE (1u << 5)
-#define CSB_F_KSKIP (1u << 6)
+#define CSB_F_KSKIP (1u << 6)     /* informational: the 2-D fast residual found w != 0 under
+                                      symmetry k-faces and the library re-ran the general path
+                                      on the device (R is valid); later calls of the context
+                                      skip the fast path */
 #define CSB_F_BLOCK (1u << 7)
 #define CSB_F_GATE_DECODE (1u << 8)
 

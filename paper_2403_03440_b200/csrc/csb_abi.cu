@@ -495,6 +495,11 @@ int csb_residual(csb_ctx* c, const double* q, double* R, double* P, int first_or
   const bool k2d = use_k2d(c);
   cudaError_t e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
                                   k2d, c->flags, st);
+  // K2D precondition (w == 0 under symmetry k-faces) checked by that launch:
+  // the general path re-runs on the device when it raised EB_KSKIP
+  if (e == cudaSuccess && k2d)
+    e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order, false,
+                        c->flags, st, NormsOut{nullptr, 0, nullptr, nullptr}, nullptr, c->flags);
   if (e == cudaSuccess && P) e = launch_padded(c->d_model, c->ns, c->g, bc_of(c), q, P, c->flags, st);
   return cuda_check(c, e, "residual");
 }
@@ -786,13 +791,18 @@ int csb_iteration(csb_ctx* c, const double* q, double cfl, int scheme, int offdi
   cudaStream_t st = S(stream);
   if ((r = ensure_face_metrics(c, st))) return r;
   double* R = R_out ? R_out : c->R;
-  bool fused = false;
+  bool fused = false, fused2 = true;
+  const bool k2d = use_k2d(c);
+  const NormsOut nrm{c->norm_partial, c->npart_cap, c->norm_counter, norms3 ? norms3 : c->norms};
   cudaError_t e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
-                                  use_k2d(c), c->flags, st,
-                                  NormsOut{c->norm_partial, c->npart_cap, c->norm_counter,
-                                           norms3 ? norms3 : c->norms},
-                                  &fused);
-  if (e == cudaSuccess && !fused)
+                                  k2d, c->flags, st, nrm, &fused);
+  // device-side fallback to the general path when the K2D precondition
+  // failed (EB_KSKIP: w != 0 under symmetry k-faces); a no-op launch otherwise
+  if (e == cudaSuccess && k2d)
+    e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order, false,
+                        c->flags, st, fused ? nrm : NormsOut{nullptr, 0, nullptr, nullptr}, &fused2,
+                        c->flags);
+  if (e == cudaSuccess && (!fused || !fused2))
     e = launch_norms(c->ns, c->g.N, R, c->partial, norms3 ? norms3 : c->norms, st);
   if (e != cudaSuccess) return cuda_check(c, e, "iteration residual");
   return implicit_impl(c, q, R, cfl, scheme, offdiag_paper, nullptr, q_new, st);

@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #define CSB_DEV __device__ __forceinline__
 
 namespace csb {
@@ -337,6 +339,31 @@ static inline int bucket_of(int ns) {
   return ns <= 2 ? 2 : ns <= 4 ? 4 : ns <= 5 ? 5 : ns <= 6 ? 6 : ns <= 8 ? 8 : ns <= 12 ? 12
        : ns <= 16 ? 16 : ns <= 20 ? 20 : ns <= 24 ? 24 : ns <= 32 ? 32 : ns <= 40 ? 40
        : ns <= 48 ? 48 : 64;
+}
+
+// Tuning / timing probe knobs (environment) exist only in builds with
+// -DCSB_PROBES; production builds ignore them.  The launch-order knobs
+// CSB_NO_OVERLAP / CSB_FORCE_OVERLAP are always honoured (both orders are
+// valid and parity-tested).
+static inline const char* probe_env(const char* name) {
+#ifdef CSB_PROBES
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
+// SMs of the current device (cached per process).
+static inline int device_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+      sms = 148;
+  }
+  return sms;
 }
 
 static inline int grid_for(long long n, int bs) {

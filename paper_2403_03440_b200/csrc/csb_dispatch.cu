@@ -13,7 +13,7 @@ unsigned long long launch_count() { return g_launches.load(std::memory_order_rel
 #define CSB_DECL(b)                                                                               \
   cudaError_t launch_residual_b##b(const Model*, int, const GridDev&, const BCDev&, const Mech&,   \
                                    const double*, double*, int, bool, unsigned long long*,         \
-                                   cudaStream_t, NormsOut, bool*);                                 \
+                                   cudaStream_t, NormsOut, bool*, const unsigned long long*);      \
   cudaError_t launch_padded_b##b(const Model*, int, const GridDev&, const BCDev&, const double*,   \
                                  double*, unsigned long long*, cudaStream_t);                      \
   cudaError_t launch_decode_b##b(const Model*, int, const GridDev&, const double*, double*,        \
@@ -61,10 +61,11 @@ CSB_BUCKET_LIST(CSB_DECL)
 
 cudaError_t launch_residual(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                             const Mech& mech, const double* q, double* R, int first_order, bool k2d,
-                            unsigned long long* flags, cudaStream_t st, NormsOut nrm, bool* fused) {
+                            unsigned long long* flags, cudaStream_t st, NormsOut nrm, bool* fused,
+                            const unsigned long long* guard) {
   note_launches(1);
   if (fused) *fused = false;
-  CSB_ROUTE(launch_residual, mp, ns, g, bc, mech, q, R, first_order, k2d, flags, st, nrm, fused)
+  CSB_ROUTE(launch_residual, mp, ns, g, bc, mech, q, R, first_order, k2d, flags, st, nrm, fused, guard)
 }
 cudaError_t launch_padded(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                           const double* q, double* P, unsigned long long* flags, cudaStream_t st) {

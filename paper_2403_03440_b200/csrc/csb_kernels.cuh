@@ -91,7 +91,7 @@ cudaError_t launch_residual(const Model* mp, int ns, const GridDev& g, const BCD
                             const Mech& mech, const double* q, double* R, int first_order, bool k2d,
                             unsigned long long* flags, cudaStream_t st,
                             NormsOut nrm = NormsOut{nullptr, 0, nullptr, nullptr},
-                            bool* fused = nullptr);
+                            bool* fused = nullptr, const unsigned long long* guard = nullptr);
 cudaError_t launch_padded(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                           const double* q, double* P, unsigned long long* flags, cudaStream_t st);
 

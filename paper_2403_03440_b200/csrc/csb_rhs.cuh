@@ -724,7 +724,12 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
                                                   Mech mech, const double* __restrict__ q,
                                                   double* __restrict__ R, int first_order, int TI_,
                                                   int TJ_, int TK, unsigned long long* flags,
-                                                  NormsOut nrm, int sr_on) {
+                                                  NormsOut nrm, int sr_on,
+                                                  const unsigned long long* __restrict__ guard) {
+  // guarded launch (the general-path fallback queued behind a K2D launch):
+  // runs only when that launch raised EB_KSKIP (w != 0 under symmetry
+  // k-faces), as a persistent grid over the tiles; otherwise exits at once
+  if (guard && !((__ldcg(guard) >> EB_KSKIP) & 1ull)) return;
   const int TI = FTI ? FTI : TI_, TJ = FTJ ? FTJ : TJ_;
   extern __shared__ double smem[];
   __shared__ Model sm;
@@ -751,7 +756,10 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
   const int BX = TI + 2 * NG, BY = TJ + 2 * NG, BZ = K2D ? 1 : TK + 2 * NG;
   const int ldP = BX * BY * BZ;
   const int nti = (g.ni + TI - 1) / TI, ntj = (g.nj + TJ - 1) / TJ;
-  int b = blockIdx.x;
+  const int ntiles = nti * ntj * (K2D ? 1 : (g.nk + TK - 1) / TK);
+  double n_flow = 0.0, n_sp = 0.0, n_rho = 0.0;  // residual_norms partials of this CTA
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int b = tile;
   const int ti = b % nti;
   b /= nti;
   const int tj = b % ntj;
@@ -976,7 +984,6 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
 
   // chemistry source (spatial.py:261-267), the finite check (269-271) and,
   // when requested, the residual norms (driver.py:85-90)
-  double n_flow = 0.0, n_sp = 0.0, n_rho = 0.0;
   const int ncell = K2D ? TI * TJ : ci * cj * ck;
   for (int l = threadIdx.x; l < ncell; l += blockDim.x) {
     const int kk = K2D ? 0 : l % ck;
@@ -1057,6 +1064,8 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
       n_rho += rv[0] * rv[0];
     }
   }
+  __syncthreads();  // next tile restages sP / sF / sR
+  }  // tile loop
   if (nrm.out) {
     // block partials, then the last block reduces all partials in fixed order
     __shared__ double red[3][8];
@@ -1139,7 +1148,7 @@ static inline void pick_tile(int ns, bool k2d, int nk, int& TI, int& TJ, int& TK
     // (tiles below 7 x 16 cells lose more to the halo than they gain:
     // ns = 40 on 7 x 8 at 2 CTAs/SM is 20% slower than 7 x 16 at one)
     int cand[][2] = {{15, 16}, {11, 16}, {7, 16}, {7, 8}, {3, 8}, {3, 4}, {1, 4}};
-    if (const char* e = getenv("CSB_RHS_TILE")) sscanf(e, "%d,%d", &cand[0][0], &cand[0][1]);
+    if (const char* e = probe_env("CSB_RHS_TILE")) sscanf(e, "%d,%d", &cand[0][0], &cand[0][1]);
     for (int pass = 0; pass < 2; ++pass)
       for (auto& c : cand) {
         TI = c[0];
@@ -1179,7 +1188,8 @@ static inline bool residual_in_smem(size_t smem, int cells, int nv, size_t& tota
 
 cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                             const Mech& mech, const double* q, double* R, int first_order, bool k2d,
-                            unsigned long long* flags, cudaStream_t st, NormsOut nrm, bool* fused) {
+                            unsigned long long* flags, cudaStream_t st, NormsOut nrm, bool* fused,
+                            const unsigned long long* guard) {
   int TI, TJ, TK;
   size_t smem;
   pick_tile(ns, k2d, g.nk, TI, TJ, TK, smem);
@@ -1188,20 +1198,22 @@ cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, c
   if (sr_on) smem = smem_sr;
   const long long ntiles = (long long)((g.ni + TI - 1) / TI) * ((g.nj + TJ - 1) / TJ) *
                            (k2d ? 1 : (g.nk + TK - 1) / TK);
-  if (!(nrm.out && ntiles <= nrm.cap)) nrm.out = nullptr;
+  // guarded fallback: a persistent grid (exits at once when not needed)
+  const long long nblk = guard ? std::min<long long>(ntiles, 2LL * device_sms()) : ntiles;
+  if (!(nrm.out && nblk <= nrm.cap)) nrm.out = nullptr;
   if (fused) *fused = nrm.out != nullptr;
   cudaError_t err = cudaSuccess;
   CSB_NS_DISPATCH(ns, {
     if (k2d) {
       auto kfn = TI == 15 && TJ == 16 ? k_residual<NSB, true, 15, 16> : k_residual<NSB, true>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kfn<<<(unsigned)ntiles, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
-                                               nrm, sr_on);
+      kfn<<<(unsigned)nblk, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
+                                             nrm, sr_on, guard);
     } else {
       auto kfn = k_residual<NSB, false>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kfn<<<(unsigned)ntiles, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
-                                               nrm, sr_on);
+      kfn<<<(unsigned)nblk, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
+                                             nrm, sr_on, guard);
     }
     err = cudaGetLastError();
   });

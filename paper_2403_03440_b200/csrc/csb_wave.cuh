@@ -84,16 +84,34 @@ constexpr int ci_wk() {
 }
 constexpr int CI_MAXNSB = 16;  // register-resident CI chain up to here; smem-resident above
 
-// species slot length: <= 64 KiB per slot at the widest layout (nsI = NSB)
-template <int NSB>
+// Species slot length (steps) for the record layout with nsI diagonal planes
+// (PER: nsI = NSB, chemistry; else 1): a slot holds <= CSB_SP_SLOT_KB and a
+// 2-deep ring plus the hand-off ring (HRING + WK rows of NSB words) fits the
+// 210 KiB budget of wave_depth, so every bucket has a valid launch shape
+// (checked by static_assert below for every bucket and both layouts).
 #ifndef CSB_SP_SLOT_KB
 #define CSB_SP_SLOT_KB 100  // measured: 100 KB slots (8 steps up to ns = 24, 2-deep ring) beat 64 KB (4-step slots) by 7-8% at ns = 16-40
 #endif
+constexpr int WAVE_SMEM_BUDGET = 210 * 1024;
+template <int NSB, bool PER>
 constexpr int wave_wks() {
+  constexpr int NG = (PER ? NSB : 1) + NSB + 2;
   int w = 8;  // also the hand-off granularity (a slot starts when its columns are in)
-  while (w > 1 && w * (2 * NSB + 2) * 256 > CSB_SP_SLOT_KB * 1024) w /= 2;
+  while (w > 1 && (w * NG * 256 > CSB_SP_SLOT_KB * 1024 ||
+                   2 * w * NG * 256 + (HRING + w) * NSB * 8 > WAVE_SMEM_BUDGET))
+    w /= 2;
   return w;
 }
+template <int NSB, bool PER>
+constexpr bool wave_species_fits() {
+  constexpr int w = wave_wks<NSB, PER>(), NG = (PER ? NSB : 1) + NSB + 2;
+  return 2 * w * NG * 256 + (HRING + w) * NSB * 8 <= WAVE_SMEM_BUDGET && TQ % w == 0 &&
+         HRING % w == 0;
+}
+#define CSB_CHECK_WKS(b) \
+  static_assert(wave_species_fits<b, true>() && wave_species_fits<b, false>(), "species ring");
+CSB_BUCKET_LIST(CSB_CHECK_WKS)
+#undef CSB_CHECK_WKS
 
 // ---------------------------------------------------------------- PTX helpers
 CSB_DEV unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -679,7 +697,7 @@ constexpr int sp_warps() {
 
 template <int NSB, bool BWD, bool PER>
 CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro, int grp) {
-  constexpr int WK = wave_wks<NSB>();
+  constexpr int WK = wave_wks<NSB, PER>();
   constexpr int SG = NSB / sp_warps<NSB>();   // species of this warp
   constexpr int NI = PER ? NSB : 1, NG = NI + NSB + 2;
   constexpr int PC = BWD ? NI : NI + NSB;   // c_i, c_j planes
@@ -928,7 +946,7 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
                    : a.only == 5                  ? (blockIdx.x & 1)
                                                   : ((blockIdx.x >> 1) & 1);
   const WaveRole ro = kind == 1 ? a.role[1] : a.role[0];
-  const int WK = kind == 2 ? ci_wk<NSB>() : kind ? wave_wks<NSB>() : WKF;
+  const int WK = kind == 2 ? ci_wk<NSB>() : kind ? wave_wks<NSB, PER>() : WKF;
   const int nh = kind == 2 ? 5 + NSB : kind ? NSB : 5;
   const int nchain = kind == 1 ? sp_warps<NSB>() : 1;  // chain warps of this role
   const int D = ro.D, NG = ro.ng;
@@ -1040,7 +1058,10 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
     // hin ring, so one poll round trip covers all of them.  (Measured: with one
     // 4-step slot per poll the receiver, not the chain, set the pace of the
     // ns = 20 species sweep: 311 vs 120 ns per step on 2 strips.)
-    const int Q = max(1, min(WK >= 8 ? 1 : 8 / WK, 512 / nw));
+    // (Q x WK must divide HRING and TQ so a window never wraps the hin ring:
+    // Q is rounded down to a power of two; WK is one already)
+    int Q = max(1, min(WK >= 8 ? 1 : 8 / WK, 512 / nw));
+    while (Q & (Q - 1)) Q &= Q - 1;
     if (Q == 1) {
     // one slot per poll (slots of >= 8 steps)
     int buf = 0, phase = 0;
@@ -1304,7 +1325,8 @@ __global__ void __launch_bounds__(256, NSB <= 8 ? 3 : 2) k_epilogue2d(const Mode
 // large species counts keep 4 CTAs per SM
 inline int epilogue_steps(int ns) {
   int ce = 16;
-  if (const char* e = getenv("CSB_EPI_C")) ce = atoi(e);  // tuning probe
+  if (const char* e = probe_env("CSB_EPI_C")) ce = atoi(e);  // tuning probe
+  if (ce < 2 || TQ % ce) ce = 16;  // must divide T
   while (ce > 2 && (size_t)(5 + ns) * ce * 32 * sizeof(double) > 48 * 1024) ce /= 2;
   return ce;
 }
@@ -1315,7 +1337,7 @@ inline size_t wave_role_smem(int D, int WK, int NG, int nh) {
 // deepest ring (2..4) that fits the shared-memory budget, 0 if none
 inline int wave_depth(int WK, int NG, int nh) {
   for (int D = CSB_DMAX; D >= 2; --D)
-    if (wave_role_smem(D, WK, NG, nh) <= 210 * 1024) return D;
+    if (wave_role_smem(D, WK, NG, nh) <= WAVE_SMEM_BUDGET) return D;
   return 0;
 }
 
@@ -1341,28 +1363,29 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     constexpr int NV = 5 + NSB;
     const int nsI = per_species ? NSB : 1;
     const int NSF = nsI + NSB + 2;
-    constexpr int WKS = wave_wks<NSB>();
+    const int WKS = per_species ? wave_wks<NSB, true>() : wave_wks<NSB, false>();
     constexpr int NGC = ci_planes<NSB>(), WKC = ci_wk<NSB>();
     // large NSB (CI): + the smem-resident chain state (4 x NV x 32 doubles)
     const size_t ci_extra = NSB > CI_MAXNSB ? (size_t)4 * NV * 32 * sizeof(double) : 0;
     int Df = 0, Ds = 0, Dc = 0;
     if (ci) {
       for (int D = 4; D >= 2 && !Dc; --D)
-        if (wave_role_smem(D, WKC, NGC, NV) + ci_extra <= 210 * 1024) Dc = D;
+        if (wave_role_smem(D, WKC, NGC, NV) + ci_extra <= WAVE_SMEM_BUDGET) Dc = D;
       if (!Dc) return cudaErrorInvalidConfiguration;
     } else {
       Df = wave_depth(WKF, NFF, 5);
       for (int D = CSB_DMAX; D >= 2 && !Ds; --D)
-        if (wave_role_smem(D, WKS, NSF, NSB) <= 210 * 1024) Ds = D;
+        if (wave_role_smem(D, WKS, NSF, NSB) <= WAVE_SMEM_BUDGET) Ds = D;
       if (!Df || !Ds) return cudaErrorInvalidConfiguration;
     }
     // ---------------- records tile length C (steps) and shared memory
     int C = 4;  // measured: 4 steps per tile with 4 CTAs/SM beats 8 (1 CTA/SM less)
-    if (const char* ev_c = getenv("CSB_REC_C")) C = atoi(ev_c);  // tuning probe
+    if (const char* ev_c = probe_env("CSB_REC_C")) C = atoi(ev_c);  // tuning probe
     auto rsm_of = [&](int c) {
       const int ncp = ci ? 2 + 3 * NV : 16 + nsI + NSB;
       return ((size_t)ncp * c * 32 + 12 * (size_t)(c + 2) * 34) * sizeof(double);
     };
+    if (C < 1 || sk.T % C) C = 4;  // a tile length must divide T (T is a multiple of TQ = 16)
     while (C > 1 && rsm_of(C) > 200 * 1024) C /= 2;
     const size_t rsm = rsm_of(C);
     auto krec = ci ? k_records2d<NSB, true> : k_records2d<NSB, false>;
@@ -1374,7 +1397,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     };
     // ---------------- one sweep
     int only = -1;
-    if (const char* ev_o = getenv("CSB_WAVE_ONLY")) only = atoi(ev_o);  // timing probe
+    if (const char* ev_o = probe_env("CSB_WAVE_ONLY")) only = atoi(ev_o);  // timing probe
     const long long hrows = (long long)sk.T + 2 * HPAD;
     auto launch_pass = [&](bool bwd, cudaStream_t s, const int* rdy) -> cudaError_t {
       WaveArgs wa{};
@@ -1385,15 +1408,15 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       wa.ci = ci ? 1 : 0;
       wa.only = ci ? -1 : only;
       wa.poll_ns = 16;
-      if (const char* ev_p = getenv("CSB_POLL_NS")) wa.poll_ns = atoi(ev_p);  // tuning probe
-      wa.fake_recv = getenv("CSB_FAKE_RECV") ? 1 : 0;                         // timing probe
+      if (const char* ev_p = probe_env("CSB_POLL_NS")) wa.poll_ns = atoi(ev_p);  // tuning probe
+      wa.fake_recv = probe_env("CSB_FAKE_RECV") ? 1 : 0;                         // timing probe
       wa.rdy = rdy;
-      wa.nonplanar = getenv("CSB_NO_PLANAR") ? nullptr : wb.nonplanar;  // (tuning probe)
+      wa.nonplanar = probe_env("CSB_NO_PLANAR") ? nullptr : wb.nonplanar;  // (tuning probe)
       wa.epoch = wb.epoch;
       wa.rC = C;
       wa.dbg = nullptr;
       static unsigned long long* dbg = nullptr;
-      if (getenv("CSB_WAVE_DBG")) {
+      if (probe_env("CSB_WAVE_DBG")) {
         if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 16 * 2 * 4096);
         cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 16 * 2 * sk.nstrip, s);
         wa.dbg = dbg;
@@ -1469,8 +1492,16 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     // SMs (512^2: 32 of 148 SMs, 0.649 -> 0.587 ms per iteration); at 1024^2
     // (64 SMs) the concurrent records tiles slow the chains more than they hide
     // (2.23 -> 2.35 ms at ns = 11)
+    // The sweep CTAs (one per SM: ~200 KB of shared memory each) spin on the
+    // records tiles, so the records kernel must keep SMs of its own: the
+    // overlap is used while the sweeps hold at most a third of the device
+    // (48 of 148 SMs on B200), forced overlap only while 8 SMs stay free.
+    // (the threshold counts 2 CTAs per strip for CI too, as measured)
+    const int sms = device_sms();
+    const int nsweep = ci ? sk.nstrip : 2 * sk.nstrip;
     const bool overlap = !ev && wb.s2 && only == -1 &&
-                         (2 * sk.nstrip <= 48 || getenv("CSB_FORCE_OVERLAP")) &&
+                         (2 * sk.nstrip <= sms * 48 / 148 ||
+                          (getenv("CSB_FORCE_OVERLAP") && nsweep <= sms - 8)) &&
                          !getenv("CSB_NO_OVERLAP");
     cudaError_t e;
     if (overlap) {

@@ -18,17 +18,16 @@ def residual_device(eng, qs, first_order=False, padded=False, R=None):
     ni, nj, nk = eng.dims
     R = eng.empty(eng.nv, eng.N) if R is None else R
     P = eng.empty(6 + eng.ns, (ni + 4) * (nj + 4) * (nk + 4)) if padded else None
-    for _attempt in range(2):
-        eng._chk(eng.lib.csb_residual(eng.ctx, qs.data_ptr(), R.data_ptr(),
-                                      P.data_ptr() if P is not None else None,
-                                      int(bool(first_order)), ctypes.c_void_p(eng.stream)),
-                 "residual")
-        flags, cell, _ = eng.status()
-        if flags & F_KSKIP:  # 2-D fast path invalid (w != 0): redo on the general path
-            continue
-        if flags:
-            eng.raise_for(flags, cell, "assemble_residual", order=("decode",))
-        break
+    eng._chk(eng.lib.csb_residual(eng.ctx, qs.data_ptr(), R.data_ptr(),
+                                  P.data_ptr() if P is not None else None,
+                                  int(bool(first_order)), ctypes.c_void_p(eng.stream)),
+             "residual")
+    # F_KSKIP only records that the library re-ran the 2-D fast path's
+    # tiles on the general path (w != 0 under symmetry k-faces); R is valid
+    flags, cell, _ = eng.status()
+    flags &= ~F_KSKIP
+    if flags:
+        eng.raise_for(flags, cell, "assemble_residual", order=("decode",))
     return R, P
 
 
