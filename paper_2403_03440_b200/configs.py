@@ -328,3 +328,19 @@ def build_case(spec):
         mech = Mechanism(tuple(Reaction(np.asarray(r.nu_r, float), np.asarray(r.nu_p, float), r.Af,
                                         r.bf, r.Eaf, backward=r.back) for r in spec.reactions))
     return grid, model, bcs, mech
+
+
+def freestream_of(spec, model):
+    """The freestream ``CellPrimitive`` of a case with a far-field boundary
+    (``Case.freestream``), else the first cell's state."""
+    from .mixture import make_primitive
+    for b in spec.bcs.values():
+        if b.fs is not None:
+            rho, u, T, Y = b.fs
+            return make_primitive(model, rho=rho, u=u, T=T, Y=Y)
+    q = spec.q.reshape(-1, spec.nv)[0]
+    Y = q[5:] / q[0]
+    M, cp, Rs, bs = _thermo_arrays(spec.species)
+    u = q[1:4] / q[0]
+    T = (q[4] / q[0] - 0.5 * u @ u - Y @ bs) / (Y @ cp - Y @ Rs)
+    return make_primitive(model, rho=q[0], u=u, T=T, Y=Y)

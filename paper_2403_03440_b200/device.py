@@ -237,6 +237,15 @@ class Engine:
             return aos.to(like.device)
         return aos.cpu().numpy()
 
+    def from_soa_into(self, t, host):
+        """SoA (nc, N) device tensor -> caller-owned AoS host tensor (N, nc)."""
+        nc, n = t.shape
+        aos = self.empty(n, nc)
+        self._chk(self.lib.csb_transpose(n, nc, t.data_ptr(), aos.data_ptr(), 0,
+                                         ctypes.c_void_p(self.stream)), "transpose")
+        host.copy_(aos)
+        return host
+
     def cells_out(self, t, like):
         """(N,) device tensor -> (ni, nj, nk) array in the caller's flavour."""
         t = t.reshape(self.dims)

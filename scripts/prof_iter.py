@@ -2,7 +2,9 @@
 config, for ncu captures of the per-iteration kernels.
 
     python scripts/prof_iter.py [config] [ns] [iters] [scheme]
-      config 1: 512^2 air5 box; config 3: 1024^2 box with ns species
+      config 1: 512^2 air5 box; config 3: 1024^2 box with ns species;
+      config 2: 1024^2 O-grid ns=11; config 4: 4096x2048 O-grid ns=11
+      (freestream start state at the ramp's first CFL)
       scheme CS1 (default) | CI
 
 Run it once plainly (exit 0), then under
@@ -29,7 +31,13 @@ def main():
     ns = int(a[1]) if len(a) > 1 else 11
     iters = int(a[2]) if len(a) > 2 else 3
     scheme = a[3] if len(a) > 3 else "CS1"
-    spec = C.config1(seed=1) if cfg == 1 else C.config3(ns, seed=3)
+    if cfg == 4:
+        spec = C.config4()
+        spec.cfl = 1.0
+    elif cfg == 2:
+        spec = C.config2()
+    else:
+        spec = C.config1(seed=1) if cfg == 1 else C.config3(ns, seed=3)
     grid, model, bcs, mech = C.build_case(spec)
     eng = get_engine(grid, model)
     eng.set_bcs(bcs)
