@@ -201,6 +201,24 @@ int csb_profile_step(csb_ctx* ctx, const double* q, const double* R, double cfl,
 int csb_iteration(csb_ctx* ctx, const double* q, double cfl, int scheme, int offdiag_paper,
                   int first_order, double* q_new, double* R_out, double* norms3, void* stream);
 
+/* ---------------------------------------------------------- dual time */
+/* Unsteady right-hand side (implicit.py:47-56 dual_time_rhs):
+ * rhs = -R - V [(1 + theta)(q_m - q_n) - theta (q_n - q_nm1)] / dt for N
+ * cells, all SoA (5 + ns) x N, vol[N] the cell volumes; dt > 0 and finite
+ * (steady mode, rhs = -R, needs no call). */
+int csb_dual_time_rhs(csb_ctx* ctx, long long N, const double* vol, const double* R, const double* q_m,
+                      const double* q_n, const double* q_nm1, double theta, double dt, double* rhs,
+                      void* stream);
+/* One implicit step of the dual-time inner loop (driver.py:232-251 with
+ * dt): rhs as formed by csb_dual_time_rhs, (1 + theta) V / dt added to the
+ * diagonal (implicit.py:346-348); species closure and gate as
+ * csb_implicit_step.  Runs the generic hyperplane sweeps. */
+int csb_implicit_step_rhs(csb_ctx* ctx, const double* q, const double* rhs, double cfl, int scheme,
+                          int offdiag_paper, double theta, double dt, double* q_new, void* stream);
+/* out[0] = sum x^2 over n values (deterministic order; the dual-time inner
+ * residual norm, driver.py:341). */
+int csb_sum_squares(csb_ctx* ctx, long long n, const double* x, double* out, void* stream);
+
 /* AoS [N][nv] <-> SoA [nv][N] (device). */
 int csb_transpose(long long N, int nv, const double* src, double* dst, int to_soa, void* stream);
 
@@ -218,6 +236,49 @@ int csb_batched_inverse(int n, long long N, const double* dOm, const double* d, 
  * per thread, iters x 128 DFMA each (2 flops per DFMA).  scratch: 1 double
  * (device).  Used by bench.py as the measured FP64 peak of the roofline. */
 int csb_fp64_peak(int iters, double* scratch, void* stream);
+
+/* ------------------------------------------------------- setup on device */
+/* Node fill of the grid generators (grid.py:102-111 generate_box, 139-162
+ * generate_cylinder_ogrid) from their 1-D axes (host-computed, numpy's
+ * linspace / cos / sin / radial distribution): mode 0 (box)
+ * node(i,j,k) = (a[i], b[j], c[k]); mode 1 (cylinder)
+ * node(i,j,k) = (b[j] a[i], b[j] s[i], c[k]) with a = cos, s = sin, b = r.
+ * nodes: device (n0, n1, n2, 3) AoS; a, s, b, c device vectors. */
+int csb_fill_nodes(int mode, int n0, int n1, int n2, const double* a, const double* s,
+                   const double* b, const double* c, double* nodes, void* stream);
+
+/* Metric terms (grid.py:51-99 compute_metrics) from device nodes
+ * (ni+1, nj+1, nk+1, 3) AoS: face vectors Si/Sj/Sk in the library's SoA face
+ * layout, volumes vol[N]; numpy's rounding order (bit-identical metrics).
+ * scratch: NF0 + NF1 + NF2 doubles; bad: 2 words (device): bad[0] != 0 when a
+ * cell has V <= 1e-30 or non-finite V (DegenerateCell), bad[1] = the first
+ * such cell. */
+int csb_grid_metrics(int ni, int nj, int nk, const double* nodes, double* Si, double* Sj,
+                     double* Sk, double* vol, double* scratch, unsigned long long* bad,
+                     void* stream);
+
+/* make_primitive / prim_to_cons (mixture.py:310-351) for n states: u (n x 3)
+ * and Y (n x ns, used as given) AoS, two of rho, p, T (n each; the third is
+ * NULL and derived from p = rho R(Y) T).  out (nullable): the csb_cons_to_prim
+ * layout [rho, u0, u1, u2, p, T, c, gamma, h, Ek, R, cp, Y...] x n SoA;
+ * q (nullable): conservative vector (5 + ns) x n SoA.  Non-positive rho, p or
+ * T sets CSB_F_DECODE (NonPhysicalState).  Needs the model and workspace. */
+int csb_primitive(csb_ctx* ctx, long long n, const double* rho, const double* u, const double* p,
+                  const double* T, const double* Y, double* out, double* q, void* stream);
+
+/* Wall-normal heat flux on one noslip_isothermal face (driver.py:132-184):
+ * one-sided second-order dT/dn through T_wall and the first two cell
+ * centres, k at (T_wall, Y of the first cell).  q: device SoA state; slab:
+ * the three node planes nearest the wall along the face's axis (plane 0 =
+ * wall), AoS (3, m1+1, m2+1, 3) over the two other axes in increasing
+ * order.  qw, pw (device, m1 x m2): heat flux (W/m^2, positive into the
+ * wall) and the first cell's pressure. */
+int csb_wall_heat_flux(csb_ctx* ctx, int face, const double* q, const double* slab, double* qw,
+                       double* pw, void* stream);
+
+/* numpy.argmax(key) (first maximum, NaN first) and val at it
+ * (driver.py:187-205 stagnation monitor): out3 = [key_max, val_at, index]. */
+int csb_argmax_pick(long long n, const double* key, const double* val, double* out3, void* stream);
 
 #ifdef __cplusplus
 }

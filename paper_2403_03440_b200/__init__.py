@@ -8,10 +8,13 @@ signatures); the compute runs in the sm_100a library
 
 from .boundary import BoundaryCondition  # noqa: F401
 from .errors import (BadDims, CsflowError, DegenerateCell, Diverged, ExtensionMissing,  # noqa: F401
-                     MissingBC, NonPhysicalState, NoWallBoundary, SingularDiagonal, ZeroWavespeed)
+                     MissingBC, MultiBlockUnsupported, NonPhysicalState, NoWallBoundary,
+                     ParseError, SingularDiagonal, ZeroWavespeed)
 from .grid import StructuredGrid, compute_metrics, generate_box, generate_cylinder_ogrid  # noqa: F401
-from .mixture import (CellPrimitive, MixtureModel, SpeciesData, cloned_mixture,  # noqa: F401
-                      cons_to_prim, make_primitive, nitrogen_like, prim_to_cons)
+from .configs import cloned_mixture, nitrogen_like  # noqa: F401
+from .mixture import (CellPrimitive, MixtureModel, SpeciesData, cons_to_prim,  # noqa: F401
+                      make_primitive, prim_to_cons)
+from .plot3d import read_plot3d, write_plot3d  # noqa: F401
 
 __version__ = "0.1.0"
 

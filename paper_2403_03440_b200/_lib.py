@@ -56,6 +56,14 @@ SIGNATURES = {
     "csb_transpose": (_i, [_ll, _i, _dp, _dp, _i, _p]),
     "csb_batched_inverse": (_i, [_i, _ll, _dp, _dp, _dp, _dp, _dp, _p]),
     "csb_fp64_peak": (_i, [_i, _dp, _p]),
+    "csb_dual_time_rhs": (_i, [_p, _ll, _dp, _dp, _dp, _dp, _dp, _d, _d, _dp, _p]),
+    "csb_implicit_step_rhs": (_i, [_p, _dp, _dp, _d, _i, _i, _d, _d, _dp, _p]),
+    "csb_sum_squares": (_i, [_p, _ll, _dp, _dp, _p]),
+    "csb_fill_nodes": (_i, [_i, _i, _i, _i, _dp, _dp, _dp, _dp, _dp, _p]),
+    "csb_grid_metrics": (_i, [_i, _i, _i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _p]),
+    "csb_primitive": (_i, [_p, _ll, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _p]),
+    "csb_wall_heat_flux": (_i, [_p, _i, _dp, _dp, _dp, _dp, _p]),
+    "csb_argmax_pick": (_i, [_ll, _dp, _dp, _dp, _p]),
 }
 
 _LIB = None

@@ -49,9 +49,25 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose=False, force=False, extra_flags=()):
+def build(verbose=False, force=False, extra_flags=(), tag=None):
+    """Compile and link the library.  ``tag`` builds an experiment variant
+    (``extra_flags`` such as -DCSB_RES_MINB=3) into _variants/<tag>/ with its
+    own object directory; load it with CSB_LIB_PATH."""
+    global OBJDIR, LIB
+    saved = (OBJDIR, LIB)
+    if tag:
+        OBJDIR = os.path.join(ROOT, "build", f"obj_{tag}")
+        LIB = os.path.join(ROOT, "_variants", tag, "libcsflow_b200.so")
+        os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    try:
+        return _build(verbose, force, extra_flags)
+    finally:
+        OBJDIR, LIB = saved
+
+
+def _build(verbose, force, extra_flags):
     os.makedirs(OBJDIR, exist_ok=True)
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     cc = nvcc()
     hdrs = _headers()
     jobs = []
@@ -90,5 +106,7 @@ def build(verbose=False, force=False, extra_flags=()):
 
 
 if __name__ == "__main__":
-    build(verbose="-v" in sys.argv, force="-f" in sys.argv)
-    print(LIB)
+    args = [a for a in sys.argv[1:] if not a.startswith("-") or a.startswith("-D")]
+    tag = next((a[6:] for a in sys.argv[1:] if a.startswith("--tag=")), None)
+    defs = [a for a in sys.argv[1:] if a.startswith("-D")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, extra_flags=defs, tag=tag))

@@ -109,6 +109,22 @@ class CaseSpec:
 
 # ----------------------------------------------------------------- species
 
+# Nitrogen-like species of the paper's species-scaling benchmark (reference
+# mixture.py:416-425): M, cp, hf, Tref, mu_ref, T_mu, S_mu
+NITROGEN_LIKE = (0.028, 1039.0, 0.0, 0.0, 1.663e-5, 273.15, 107.0)
+
+
+def nitrogen_like(name: str = "N2"):
+    from .mixture import SpeciesData
+    return SpeciesData(name, *NITROGEN_LIKE)
+
+
+def cloned_mixture(ns: int, Pr: float = 0.72, Sc: float = 0.7):
+    """ns identical nitrogen-like species (the paper's scaling mixture)."""
+    from .mixture import MixtureModel
+    return MixtureModel([nitrogen_like(f"N2_{i:04d}") for i in range(ns)], Pr=Pr, Sc=Sc)
+
+
 def air5_species():
     return [SpeciesSpec(n, M, cp, hf, 298.15, 1.7e-5, 273.15, 110.0) for n, M, cp, hf in AIR5]
 
@@ -305,15 +321,19 @@ def config4(seed=4, dims=(4096, 2048, 1)):
 
 # ------------------------------------------------------------ product objects
 
+def model_of(spec):
+    from .mixture import MixtureModel, SpeciesData
+    return MixtureModel([SpeciesData(s.name, s.M, s.cp, s.hf, s.Tref, s.mu_ref, s.T_mu, s.S_mu)
+                         for s in spec.species], Pr=spec.Pr, Sc=spec.Sc)
+
+
 def build_case(spec):
     """(grid, model, bcs, mech) drop-in objects for a CaseSpec."""
     from .boundary import BoundaryCondition
     from .chemistry import Mechanism, Reaction
     from .grid import compute_metrics
-    from .mixture import MixtureModel, SpeciesData, make_primitive
-    model = MixtureModel(species=tuple(SpeciesData(s.name, s.M, s.cp, s.hf, s.Tref, s.mu_ref,
-                                                   s.T_mu, s.S_mu) for s in spec.species),
-                         Pr=spec.Pr, Sc=spec.Sc)
+    from .mixture import make_primitive
+    model = model_of(spec)
     grid = compute_metrics(spec.nodes)
     bcs = {}
     for name in FACES:

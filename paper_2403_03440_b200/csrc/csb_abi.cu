@@ -10,6 +10,21 @@
 
 using namespace csb;
 
+// csb_grid.cu
+cudaError_t csb_launch_fill_nodes(int mode, int n0, int n1, int n2, const double* a, const double* s,
+                                  const double* b, const double* c, double* nodes, cudaStream_t st);
+cudaError_t csb_launch_metrics(int ni, int nj, int nk, const double* nodes, double* Si, double* Sj,
+                               double* Sk, double* vol, double* scratch,
+                               unsigned long long* bad, cudaStream_t st);
+cudaError_t csb_launch_primitive(const Model* mp, long long n, const double* rho, const double* u,
+                                 const double* p, const double* T, const double* Y, double* out,
+                                 double* q, unsigned long long* flags, cudaStream_t st);
+cudaError_t csb_launch_wall_flux(const Model* mp, int ns, const GridDev& g, int axis, int side,
+                                 double Tw, const double* q, const double* slab, double* qw,
+                                 double* pw, unsigned long long* flags, cudaStream_t st);
+cudaError_t csb_launch_argmax_pick(long long n, const double* key, const double* val, double* out,
+                                   cudaStream_t st);
+
 struct csb_ctx {
   int ns = 0;
   bool has_model = false, has_grid = false, has_ws = false;
@@ -681,16 +696,23 @@ int csb_residual_norms(csb_ctx* c, long long N, const double* R, double* out3, v
 }
 
 // path: 0 auto, 1 generic (hyperplane sweeps), 2 2-D wavefront
+// One implicit step.  rhs_is_R: `R` is the residual (rhs = -R, steady);
+// otherwise `R` is the right-hand side itself (dual time, csb_dual_time_rhs)
+// and theta, dt add (1 + theta) V / dt to the diagonal (implicit.py:346-348).
 static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cfl, int scheme,
                          int offdiag_paper, const double* dOm_in, double* q_new, cudaStream_t st,
-                         int path = 0, double* dq_out = nullptr, cudaEvent_t* ev = nullptr) {
+                         int path = 0, double* dq_out = nullptr, cudaEvent_t* ev = nullptr,
+                         double theta = 0.0, double dt = 0.0, bool rhs_is_R = true) {
   if (int r0 = ensure_face_metrics(c, st)) return r0;
   const bool chem = mech_of(c).nrx > 0;
   const bool full = chem && scheme == SCH_CI;
+  const bool dual = dt > 0.0 && std::isfinite(dt);
   if (full && !c->ws_block) return fail(c, CSB_E_STATE, "CI with chemistry needs block workspace");
-  // the coupled operator takes the wavefront path when frozen
+  // the coupled operator takes the wavefront path when frozen; dual-time
+  // steps (extra diagonal and rhs terms) take the generic hyperplane path
   const bool ci_wave = scheme != SCH_CI || !chem;
-  const bool wave = path != 1 && c->wave_ok && !c->wave_disabled && ci_wave && c->geom2d_ok;
+  const bool wave = path != 1 && c->wave_ok && !c->wave_disabled && ci_wave && c->geom2d_ok &&
+                    rhs_is_R && !dual;
   if (path == 2 && !wave) return fail(c, CSB_E_STATE, "2-D wavefront path not applicable");
   if (wave) {
     cudaError_t e = cudaSuccess;
@@ -737,12 +759,12 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
   if (r) return r;
   OpDev& op = c->op;
   op.dom_full = full ? 1 : 0;
-  r = assemble_impl(c, q, c->dtau, scheme, offdiag_paper, 0.0, 0.0, dOm_in, true, st);
+  r = assemble_impl(c, q, c->dtau, scheme, offdiag_paper, theta, dual ? dt : 0.0, dOm_in, true, st);
   if (r) return r;
   // rhs = -R: the sweeps negate on load (exact)
   double* dq = dq_out ? dq_out : c->dq;
   cudaError_t e = cudaMemsetAsync(dq, 0, sizeof(double) * (5 + c->ns) * c->g.N, st);
-  op.neg_rhs = 1;
+  op.neg_rhs = rhs_is_R ? 1 : 0;
   if (e == cudaSuccess) e = launch_sweeps(c->d_model, c->ns, c->g, op, R, dq, nullptr, c->flags, st);
   op.neg_rhs = 0;
   if (e == cudaSuccess) e = launch_update(c->d_model, c->ns, c->g, scheme, q, dq, q_new, c->flags, st);
@@ -808,6 +830,36 @@ int csb_iteration(csb_ctx* c, const double* q, double cfl, int scheme, int offdi
   return implicit_impl(c, q, R, cfl, scheme, offdiag_paper, nullptr, q_new, st);
 }
 
+int csb_dual_time_rhs(csb_ctx* c, long long N, const double* vol, const double* R, const double* q_m,
+                      const double* q_n, const double* q_nm1, double theta, double dt, double* rhs,
+                      void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  if (N < 0 || !vol || !R || !q_m || !q_n || !q_nm1 || !rhs) return CSB_E_BADARG;
+  if (!(dt > 0.0) || !std::isfinite(dt))
+    return fail(c, CSB_E_BADARG, "dual_time_rhs: dt must be positive and finite (steady: rhs = -R)");
+  if (N == 0) return CSB_OK;
+  return cuda_check(c, launch_dual_rhs(N, 5 + c->ns, R, q_m, q_n, q_nm1, vol, theta, dt, rhs,
+                                       S(stream)),
+                    "dual time rhs");
+}
+
+int csb_implicit_step_rhs(csb_ctx* c, const double* q, const double* rhs, double cfl, int scheme,
+                          int offdiag_paper, double theta, double dt, double* q_new,
+                          void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  return implicit_impl(c, q, rhs, cfl, scheme, offdiag_paper, nullptr, q_new, S(stream), 1, nullptr,
+                       nullptr, theta, dt, false);
+}
+
+int csb_sum_squares(csb_ctx* c, long long n, const double* x, double* out, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  if (n < 0 || !x || !out) return CSB_E_BADARG;
+  return cuda_check(c, launch_sumsq(n, x, c->partial, out, S(stream)), "sum of squares");
+}
+
 int csb_transpose(long long N, int nv, const double* src, double* dst, int to_soa, void* stream) {
   return launch_transpose(N, nv, src, dst, to_soa, S(stream)) == cudaSuccess ? CSB_OK : CSB_E_CUDA;
 }
@@ -818,6 +870,63 @@ int csb_batched_inverse(int n, long long N, const double* dOm, const double* d, 
   if (N == 0) return CSB_OK;
   return launch_block_inverse(n, N, dOm, d, V, dinv, flags, S(stream)) == cudaSuccess ? CSB_OK
                                                                                       : CSB_E_CUDA;
+}
+
+int csb_fill_nodes(int mode, int n0, int n1, int n2, const double* a, const double* s,
+                   const double* b, const double* c, double* nodes, void* stream) {
+  if ((mode != 0 && mode != 1) || n0 < 1 || n1 < 1 || n2 < 1 || !a || !b || !c || !nodes ||
+      (mode == 1 && !s))
+    return CSB_E_BADARG;
+  return csb_launch_fill_nodes(mode, n0, n1, n2, a, s, b, c, nodes, S(stream)) == cudaSuccess
+             ? CSB_OK
+             : CSB_E_CUDA;
+}
+
+int csb_grid_metrics(int ni, int nj, int nk, const double* nodes, double* Si, double* Sj,
+                     double* Sk, double* vol, double* scratch, unsigned long long* bad,
+                     void* stream) {
+  if (ni < 1 || nj < 1 || nk < 1 || !nodes || !Si || !Sj || !Sk || !vol || !scratch || !bad)
+    return CSB_E_BADARG;
+  cudaStream_t st = S(stream);
+  const unsigned long long init[2] = {0ull, ~0ull};
+  if (cudaMemcpyAsync(bad, init, sizeof(init), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return CSB_E_CUDA;
+  return csb_launch_metrics(ni, nj, nk, nodes, Si, Sj, Sk, vol, scratch, bad, st) == cudaSuccess
+             ? CSB_OK
+             : CSB_E_CUDA;
+}
+
+int csb_primitive(csb_ctx* c, long long n, const double* rho, const double* u, const double* p,
+                  const double* T, const double* Y, double* out, double* q, void* stream) {
+  if (!c) return CSB_E_BADARG;
+  if (!c->has_model) return fail(c, CSB_E_STATE, "model not set");
+  if (!c->has_ws) return fail(c, CSB_E_STATE, "workspace not set");
+  const int given = (rho != nullptr) + (p != nullptr) + (T != nullptr);
+  if (n < 0 || !u || !Y || given < 2 || (!out && !q))
+    return fail(c, CSB_E_BADARG, "primitive: need u, Y and two of (rho, p, T)");
+  if (n == 0) return CSB_OK;
+  return cuda_check(c, csb_launch_primitive(c->d_model, n, rho, u, p, T, Y, out, q, c->flags, S(stream)),
+                    "primitive");
+}
+
+int csb_wall_heat_flux(csb_ctx* c, int face, const double* q, const double* slab, double* qw,
+                       double* pw, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  if (face < 0 || face > 5 || !q || !slab || !qw || !pw) return CSB_E_BADARG;
+  if (c->bc_kind[face] != CSB_BC_WALL)
+    return fail(c, CSB_E_BADARG, "wall_heat_flux: face is not a noslip_isothermal wall");
+  const int axis = face / 2, side = face % 2;
+  const int dims[3] = {c->g.ni, c->g.nj, c->g.nk};
+  if (dims[axis] < 2) return fail(c, CSB_E_BADARG, "wall_heat_flux: need two cells off the wall");
+  return cuda_check(c, csb_launch_wall_flux(c->d_model, c->ns, c->g, axis, side, c->bc_Tw[face], q,
+                                            slab, qw, pw, c->flags, S(stream)),
+                    "wall heat flux");
+}
+
+int csb_argmax_pick(long long n, const double* key, const double* val, double* out3, void* stream) {
+  if (n < 0 || !key || !val || !out3) return CSB_E_BADARG;
+  return csb_launch_argmax_pick(n, key, val, out3, S(stream)) == cudaSuccess ? CSB_OK : CSB_E_CUDA;
 }
 
 int csb_fp64_peak(int iters, double* scratch, void* stream) {

@@ -130,6 +130,11 @@ cudaError_t launch_correct(int mode, long long rows, int ns, const double* rs, c
                            cudaStream_t st);
 cudaError_t launch_transpose(long long N, int nv, const double* src, double* dst, int to_soa,
                              cudaStream_t st);
+cudaError_t launch_dual_rhs(long long N, int nv, const double* R, const double* qm,
+                            const double* qn, const double* qnm1, const double* vol, double theta,
+                            double dt, double* out, cudaStream_t st);
+cudaError_t launch_sumsq(long long n, const double* x, double* partial, double* out,
+                         cudaStream_t st);
 cudaError_t launch_export_op(const Model* mdl, int ns, const GridDev& g, const OpDev& op,
                              const double* q, int what, double* dst, cudaStream_t st);
 cudaError_t launch_dtau_arrays(long long N, const double* li, const double* lv, const double* lS,

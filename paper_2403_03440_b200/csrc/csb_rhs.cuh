@@ -230,8 +230,11 @@ CSB_DEV void muscl_pair(const double* sP, int ldP, int imm, int im, int ip, int 
 // instead of holding 2 x (5 + NSB) face values in registers (which spilled:
 // ns = 40 residual 6.7 ms per 10^6 cells); species values are recomputed per
 // pass from shared memory with the same arithmetic, so results are identical.
+#ifndef CSB_STREAM_MIN
+#define CSB_STREAM_MIN 12
+#endif
 template <int NSB>
-constexpr bool stream_species() { return NSB > 12; }
+constexpr bool stream_species() { return NSB > CSB_STREAM_MIN; }
 
 // Face flux = convective part (face_conv, writes F) + viscous part
 // (face_visc, adds to F), evaluated in two passes so that their register

@@ -82,6 +82,44 @@ __global__ void k_norms_final(int nblocks, const double* partial, double* out) {
   }
 }
 
+// Dual-time right-hand side (implicit.py:47-56):
+//   rhs = -R - V [(1 + theta)(Q^m - Q^n) - theta (Q^n - Q^{n-1})] / dt
+// in numpy's operation order (no FMA contraction), SoA (nv, N).
+__global__ void k_dual_rhs(long long N, int nv, const double* __restrict__ R,
+                           const double* __restrict__ qm, const double* __restrict__ qn,
+                           const double* __restrict__ qnm1, const double* __restrict__ vol,
+                           double theta, double dt, double* __restrict__ out) {
+  const long long total = N * nv;
+  const double a = __dadd_rn(1.0, theta);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long c = e % N;
+    const double src = __dsub_rn(__dmul_rn(a, __dsub_rn(qm[e], qn[e])),
+                                 __dmul_rn(theta, __dsub_rn(qn[e], qnm1[e])));
+    out[e] = __dsub_rn(-R[e], __ddiv_rn(__dmul_rn(vol[c], src), dt));
+  }
+}
+
+// Sum of squares of n values, deterministic two-level reduction (fixed
+// block count and order): the inner-residual norm of the dual-time loop.
+__global__ void k_sumsq_partial(long long n, const double* __restrict__ x, double* partial) {
+  __shared__ double sh[NORM_BS / 32];
+  double v = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    v += x[e] * x[e];
+  const double t = block_sum<NORM_BS>(v, sh);
+  if (threadIdx.x == 0) partial[blockIdx.x] = t;
+}
+
+__global__ void k_sumsq_final(int nblocks, const double* partial, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double v = 0.0;
+    for (int i = 0; i < nblocks; ++i) v += partial[i];
+    out[0] = v;
+  }
+}
+
 // AoS (N, nv) <-> SoA (nv, N)
 __global__ void k_transpose(long long N, int nv, const double* __restrict__ src,
                             double* __restrict__ dst, int to_soa) {
@@ -113,6 +151,23 @@ cudaError_t launch_norms(int ns, long long N, const double* R, double* partial, 
   note_launches(2);
   k_norms_partial<<<nb, NORM_BS, 0, st>>>(ns, N, R, partial);
   k_norms_final<<<1, 32, 0, st>>>(nb, partial, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dual_rhs(long long N, int nv, const double* R, const double* qm,
+                            const double* qn, const double* qnm1, const double* vol, double theta,
+                            double dt, double* out, cudaStream_t st) {
+  note_launches(1);
+  k_dual_rhs<<<grid_for(N * nv, 256), 256, 0, st>>>(N, nv, R, qm, qn, qnm1, vol, theta, dt, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sumsq(long long n, const double* x, double* partial, double* out,
+                         cudaStream_t st) {
+  const int nb = 296;
+  note_launches(2);
+  k_sumsq_partial<<<nb, NORM_BS, 0, st>>>(n, x, partial);
+  k_sumsq_final<<<1, 32, 0, st>>>(nb, partial, out);
   return cudaGetLastError();
 }
 

@@ -19,7 +19,7 @@ from . import _lib
 from .boundary import BC_KINDS, FACE_NAMES, validate_bcs
 from .errors import (DeviceError, ExtensionMissing, MissingBC, NonPhysicalState,
                      SingularDiagonal, ZeroWavespeed)
-from .mixture import padded_vector
+from .mixture import padded_vector, species_table
 
 F_DECODE, F_FACE_T, F_RES_NONFINITE, F_ZERO_WAVE = 1, 2, 4, 8
 F_SINGULAR, F_GATE, F_KSKIP, F_BLOCK, F_GATE_DECODE = 16, 32, 64, 128, 256
@@ -54,28 +54,33 @@ class Engine:
         self.lib = _lib.load()
         self.device = torch.device(device if device is not None else "cuda")
         if grid is None:  # grid-free engine: model, mechanism and flags only
-            from .grid import compute_metrics, generate_box
-            grid = compute_metrics(generate_box(1.0, (1, 1, 1)))
+            grid = _unit_grid(self.device)
         self.grid = grid
         self.model = model
-        self.ns = model.ns
-        self.nv = 5 + model.ns
+        self.ns = len(model.species)
+        self.nv = 5 + self.ns
         self.dims = tuple(grid.dims)
         self.N = int(np.prod(self.dims))
         ctx = ctypes.c_void_p()
         self._chk(self.lib.csb_create(ctypes.byref(ctx)), "create")
         self.ctx = ctx
-        tab = model.table()
+        tab = species_table(model)
         self._keep = [tab]
-        self._chk(self.lib.csb_set_model(ctx, model.ns, *[_lib.hp(tab[k]) for k in
-                                                          ("M", "cp", "hf", "Tref", "mu_ref",
-                                                           "T_mu", "S_mu")],
+        self._chk(self.lib.csb_set_model(ctx, self.ns, *[_lib.hp(tab[k]) for k in
+                                                         ("M", "cp", "hf", "Tref", "mu_ref",
+                                                          "T_mu", "S_mu")],
                                          float(model.Pr), float(model.Sc)), "set_model")
-        soa = lambda a: torch.from_numpy(np.ascontiguousarray(np.moveaxis(np.asarray(a, float), -1, 0))
-                                         ).to(self.device)
-        self.S = [soa(grid.Si), soa(grid.Sj), soa(grid.Sk)]
-        self.vol = torch.from_numpy(np.ascontiguousarray(grid.volume, dtype=float)).to(self.device)
-        self.J = torch.from_numpy(np.ascontiguousarray(grid.J, dtype=float)).to(self.device)
+        dm = getattr(grid, "device_metrics", None)
+        if callable(dm):  # this package's grids: metrics already on the device
+            S, vol = dm(self.device)
+            self.S, self.vol = list(S), vol
+        else:  # any grid with the reference's attributes (duck typing)
+            soa = lambda a: torch.from_numpy(
+                np.ascontiguousarray(np.moveaxis(np.asarray(a, float), -1, 0).reshape(3, -1))
+            ).to(self.device)
+            self.S = [soa(grid.Si), soa(grid.Sj), soa(grid.Sk)]
+            self.vol = torch.from_numpy(np.ascontiguousarray(grid.volume, dtype=float).reshape(-1)
+                                        ).to(self.device)
         ni, nj, nk = self.dims
         self._chk(self.lib.csb_set_grid(ctx, ni, nj, nk, *[t.data_ptr() for t in self.S],
                                         self.vol.data_ptr()), "set_grid")
@@ -254,6 +259,35 @@ class Engine:
         return t.cpu().numpy()
 
 
+class _UnitGrid:
+    """1 x 1 x 1 unit box: the grid of grid-free engines (element-wise calls)."""
+
+    dims = (1, 1, 1)
+
+    def __init__(self, device):
+        torch = torch_mod()
+        f = dict(dtype=torch.float64, device=device)
+        self._S = []
+        for d in range(3):  # two unit faces per direction, normal along axis d
+            S = torch.zeros((3, 2), **f)
+            S[d] = 1.0
+            self._S.append(S)
+        self._vol = torch.ones(1, **f)
+
+    def device_metrics(self, device):
+        return self._S, self._vol
+
+
+_UNIT = {}
+
+
+def _unit_grid(device):
+    g = _UNIT.get(str(device))
+    if g is None:
+        g = _UNIT[str(device)] = _UnitGrid(device)
+    return g
+
+
 class SoA:
     """A field already resident on the device in the library layout (nc, N)."""
 
@@ -274,6 +308,19 @@ class _NoGrid:
 
 
 _NOGRID = _NoGrid()
+
+
+_NS_MODELS = {}
+
+
+def engine_for_ns(ns):
+    """Grid-free engine for element-wise calls that only need the component
+    count (norms, dual-time rhs): a cloned ns-species mixture."""
+    m = _NS_MODELS.get(ns)
+    if m is None:
+        from .configs import cloned_mixture
+        m = _NS_MODELS[ns] = cloned_mixture(ns)
+    return get_engine(None, m)
 
 
 def get_engine(grid, model, device=None):

@@ -20,9 +20,9 @@ import numpy as np
 
 from .boundary import FACE_NAMES
 from .device import (F_DECODE, F_FACE_T, F_GATE, F_GATE_DECODE, F_KSKIP, F_RES_NONFINITE,
-                     SCHEMES, SoA, get_engine, is_torch)
+                     SCHEMES, SoA, engine_for_ns, get_engine, is_torch)
 from .errors import Diverged, NonPhysicalState, NoWallBoundary
-from .mixture import CellPrimitive, MixtureModel, cloned_mixture, prim_to_cons, transport
+from .mixture import CellPrimitive, prim_to_cons
 from .spatial import residual_device
 
 MAX_STEP_RETRIES = 5  # driver.py:35
@@ -33,7 +33,7 @@ class Case:
     """Everything one solver run needs (driver.py:38-75)."""
 
     grid: object
-    model: MixtureModel
+    model: object
     bcs: dict
     freestream: CellPrimitive
     mech: object = None
@@ -109,16 +109,6 @@ class ConvergenceHistory:
         return None
 
 
-_NORM_MODELS = {}
-
-
-def _norm_engine(ns):
-    m = _NORM_MODELS.get(ns)
-    if m is None:
-        m = _NORM_MODELS[ns] = cloned_mixture(ns)
-    return get_engine(None, m)
-
-
 def _norms_device(eng, R_t, out=None):
     out = eng.empty(4) if out is None else out
     eng._chk(eng.lib.csb_residual_norms(eng.ctx, R_t.shape[1], R_t.data_ptr(), out.data_ptr(),
@@ -130,10 +120,10 @@ def residual_norms(R) -> GroupedResidual:
     """Grouped L2 norms (driver.py:85-90) as one device reduction."""
     if isinstance(R, SoA):
         t = R.t
-        eng = _norm_engine(t.shape[0] - 5)
+        eng = engine_for_ns(t.shape[0] - 5)
     else:
         nv = int(np.shape(R)[-1])
-        eng = _norm_engine(nv - 5)
+        eng = engine_for_ns(nv - 5)
         t = eng.to_soa(R, nv)
     v = _norms_device(eng, t).cpu().numpy()
     return GroupedResidual(flow=float(v[0]), species=float(v[1]), density=float(v[2]))
@@ -170,97 +160,77 @@ def _wall_faces(bcs):
 
 
 class _WallGeom:
-    """Wall-distance factors per wall face (setup: node geometry only)."""
+    """Per wall face: the three node planes nearest the wall (plane 0 = the
+    wall) uploaded once, the input csb_wall_heat_flux reads its geometry from
+    (face normal, face and cell centroids, wall distances)."""
 
-    def __init__(self, grid, bcs):
-        nodes = grid.nodes
-        cc = 0.125 * (nodes[:-1, :-1, :-1] + nodes[1:, :-1, :-1] + nodes[:-1, 1:, :-1]
-                      + nodes[:-1, :-1, 1:] + nodes[1:, 1:, :-1] + nodes[1:, :-1, 1:]
-                      + nodes[:-1, 1:, 1:] + nodes[1:, 1:, 1:])
+    def __init__(self, eng, grid, bcs):
+        nodes = np.asarray(grid.nodes, dtype=float)
         self.faces = {}
         for name in _wall_faces(bcs):
             fid = FACE_NAMES.index(name)
             axis, side = divmod(fid, 2)
-            S = np.moveaxis(grid.face_areas(axis), axis, 0)[-1 if side else 0]
-            nhat = S / np.linalg.norm(S, axis=-1, keepdims=True)
-            nhat = nhat.copy() if side == 0 else -nhat
-            nm = np.moveaxis(nodes, axis, 0)[-1 if side else 0]
-            fc = 0.25 * (nm[:-1, :-1] + nm[1:, :-1] + nm[:-1, 1:] + nm[1:, 1:])
-            ccm = np.moveaxis(cc, axis, 0)
-            c1 = ccm[-1 if side else 0]
-            c2 = ccm[-2 if side else 1]
-            d1 = np.abs(np.einsum("...c,...c->...", c1 - fc, nhat))
-            d2 = np.abs(np.einsum("...c,...c->...", c2 - fc, nhat))
-            self.faces[name] = (axis, side, d1, d2)
+            n = eng.dims[axis]
+            planes = [n, n - 1, n - 2] if side else [0, 1, 2]
+            slab = np.ascontiguousarray(np.moveaxis(nodes, axis, 0)[planes])
+            shape = tuple(d for a, d in enumerate(eng.dims) if a != axis)
+            self.faces[name] = (fid, shape, eng.torch.from_numpy(slab).to(eng.device))
 
 
-def _wall_rows(eng, q_soa, axis, side):
-    """Decoded primitives of the first two cell layers next to a wall face."""
-    from .mixture import _prim_from_raw
-    ni, nj, nk = eng.dims
-    n = eng.dims[axis]
-    idx = np.arange(eng.N).reshape(eng.dims)
-    take = lambda layer: np.take(idx, layer, axis=axis)
-    l1 = take(n - 1 if side else 0)
-    l2 = take(n - 2 if side else 1)
-    sel = eng.torch.as_tensor(np.concatenate([l1.ravel(), l2.ravel()]), device=eng.device)
-    sub = q_soa[:, sel].contiguous()
-    m = sub.shape[1]
-    out = eng.empty(12 + eng.ns, m)
-    eng._chk(eng.lib.csb_cons_to_prim(eng.ctx, m, sub.data_ptr(), out.data_ptr(),
-                                      ctypes.c_void_p(eng.stream)), "wall rows")
-    prim = _prim_from_raw(out, (m,), eng.ns, None)
-    h = m // 2
-    shp = l1.shape
-    cut = lambda a, k: np.asarray(a)[k * h:(k + 1) * h].reshape(shp + np.asarray(a).shape[1:])
-    return ({"T": cut(prim.T, 0), "p": cut(prim.p, 0), "Y": cut(prim.Y, 0)},
-            {"T": cut(prim.T, 1), "p": cut(prim.p, 1)})
-
-
-def _wall_heat_flux_device(eng, q_soa, geom, bcs, model):
+def _wall_flux_device(eng, q_soa, geom):
+    """{face: (qw, p1)} device tensors shaped like the wall (driver.py:132-184)."""
     out = {}
-    for name, (axis, side, d1, d2) in geom.faces.items():
-        P1, P2 = _wall_rows(eng, q_soa, axis, side)
-        Tw = bcs[name].T_wall
-        dTdn = (((P1["T"] - Tw) * d2 ** 2 - (P2["T"] - Tw) * d1 ** 2) / (d1 * d2 * (d2 - d1)))
-        Y = P1["Y"]
-        rho_w = P1["p"] / ((Y @ model.R_s) * Tw)
-        ws = CellPrimitive(rho=rho_w, u=np.zeros(rho_w.shape + (3,)), p=P1["p"],
-                           T=np.full_like(rho_w, Tw), Y=Y, c=None, gamma=None, h=None, Ek=None)
-        _, k_w, _ = transport(ws, model)
-        out[name] = (k_w * dTdn, P1["p"])
+    for name, (fid, shape, slab) in geom.faces.items():
+        qw = eng.empty(*shape)
+        pw = eng.empty(*shape)
+        eng._chk(eng.lib.csb_wall_heat_flux(eng.ctx, fid, q_soa.data_ptr(), slab.data_ptr(),
+                                            qw.data_ptr(), pw.data_ptr(),
+                                            ctypes.c_void_p(eng.stream)), "wall_heat_flux")
+        out[name] = (qw, pw)
     return out
 
 
 def wall_heat_flux(P_or_q, grid, bcs, model):
-    """Wall-normal heat flux per wall face (driver.py:132-184).  Accepts the
-    conservative field (any flavour) or a padded primitive array."""
+    """Wall-normal heat flux (W/m^2, positive into the wall) per wall face
+    (driver.py:132-184), computed on the device.  Accepts the padded
+    primitive array P of the reference (ni+4, nj+4, nk+4, 6+ns) or the
+    conservative field (any flavour)."""
     if not _wall_faces(bcs):
         raise NoWallBoundary("no noslip_isothermal boundary in this case")
     eng = get_engine(grid, model)
+    eng.set_bcs(bcs)
     arr = P_or_q
-    if not isinstance(arr, SoA) and np.shape(arr)[:3] == tuple(n + 4 for n in grid.dims):
-        a = np.asarray(arr)[2:-2, 2:-2, 2:-2]
-        ns = model.ns
-        Y = a[..., 5:5 + ns]
-        from .mixture import make_primitive
-        prim = make_primitive(model, rho=a[..., 0], u=a[..., 1:4], T=a[..., 5 + ns], Y=Y)
+    if not isinstance(arr, SoA) and tuple(np.shape(arr)[:3]) == tuple(n + 4 for n in grid.dims):
+        # interior of P -> conservative (rho, u, T, Y of the padded layout)
+        a = arr[2:-2, 2:-2, 2:-2]
+        ns = eng.ns
+        prim = CellPrimitive(rho=a[..., 0], u=a[..., 1:4], p=a[..., 4], T=a[..., 5 + ns],
+                             Y=a[..., 5:5 + ns], c=None, gamma=None, h=None, Ek=None)
         arr = prim_to_cons(prim, model)
     qs = eng.to_soa(arr, eng.nv)
-    res = _wall_heat_flux_device(eng, qs, _WallGeom(grid, bcs), bcs, model)
-    return {k: v[0] for k, v in res.items()}
+    res = _wall_flux_device(eng, qs, _WallGeom(eng, grid, bcs))
+    eng.check("wall_heat_flux", order=("decode",))
+    like = P_or_q if is_torch(P_or_q) else None
+    return {k: (v[0] if like is not None else v[0].cpu().numpy()) for k, v in res.items()}
 
 
-def _stagnation_monitor_device(eng, q_soa, geom, bcs, model):
-    """driver.py:187-205: heat flux at the wall cell with the peak pressure."""
+def _stagnation_monitor_device(eng, q_soa, geom):
+    """Heat flux at the wall cell holding the peak wall pressure
+    (driver.py:187-205): per face a device argmax over p1, then the first
+    face with the strictly largest peak."""
     if not geom.faces:
         return float("nan")
+    picks = []
+    for name, (qw, pw) in _wall_flux_device(eng, q_soa, geom).items():
+        o = eng.empty(3)
+        eng._chk(eng.lib.csb_argmax_pick(pw.numel(), pw.data_ptr(), qw.data_ptr(), o.data_ptr(),
+                                         ctypes.c_void_p(eng.stream)), "stagnation monitor")
+        picks.append(o)
+    vals = eng.torch.stack(picks).cpu().numpy()
     best, best_p = float("nan"), -np.inf
-    for name, (qw, p1) in _wall_heat_flux_device(eng, q_soa, geom, bcs, model).items():
-        idx = np.unravel_index(int(np.argmax(p1)), p1.shape)
-        if p1[idx] > best_p:
-            best_p = float(p1[idx])
-            best = float(qw[idx])
+    for pmax, qv, _ in vals:
+        if pmax > best_p:
+            best_p, best = float(pmax), float(qv)
     return best
 
 
@@ -298,18 +268,50 @@ class _Stepper:
         secs = self.ev0.elapsed_time(self.ev1) * 1e-3
         return flags, cell, secs
 
+    def implicit_dual(self, q_t, rhs_t, cfl, theta, dt, out_t):
+        """One dual-time implicit step from a formed rhs; (flags, cell, seconds)."""
+        eng = self.eng
+        self.ev0.record()
+        eng._chk(eng.lib.csb_implicit_step_rhs(eng.ctx, q_t.data_ptr(), rhs_t.data_ptr(), float(cfl),
+                                               self.scheme, self.paper, float(theta), float(dt),
+                                               out_t.data_ptr(), ctypes.c_void_p(eng.stream)),
+                 "_implicit_step")
+        self.ev1.record()
+        flags, cell, cnt = eng.status()
+        return flags, cell, self.ev0.elapsed_time(self.ev1) * 1e-3
+
+    def dual_rhs(self, R_t, qm_t, qn_t, qnm1_t, theta, dt, out_t):
+        eng = self.eng
+        eng._chk(eng.lib.csb_dual_time_rhs(eng.ctx, eng.N, eng.vol.data_ptr(), R_t.data_ptr(),
+                                           qm_t.data_ptr(), qn_t.data_ptr(), qnm1_t.data_ptr(),
+                                           float(theta), float(dt), out_t.data_ptr(),
+                                           ctypes.c_void_p(eng.stream)), "dual_time_rhs")
+        return out_t
+
+
+def _is_dual(dt):
+    if dt is None or not np.isfinite(dt):
+        return False
+    if dt <= 0.0:
+        raise ValueError(f"physical time step must be positive, got {dt!r}")
+    return True
+
 
 def _implicit_step(case, q, R, cfl, theta=0.0, dt=None, q_n=None, q_nm1=None):
     """One LU-SGS update at fixed CFL; returns (q_new, implicit_seconds)
-    (driver.py:232-251).  Steady mode only (dual time is out of scope)."""
-    if dt is not None:
-        raise NotImplementedError("dual-time stepping (unsteady_solve) is out of scope")
+    (driver.py:232-251).  With a physical dt the right-hand side is the
+    dual-time one and (1 + theta) V / dt joins the diagonal."""
     st = _Stepper(case)
     eng = st.eng
     qs = eng.to_soa(q, eng.nv)
     Rs = eng.to_soa(R, eng.nv)
     out = eng.empty(eng.nv, eng.N)
-    flags, cell, secs = st.implicit(qs, Rs, cfl, out)
+    if _is_dual(dt):
+        rhs = st.dual_rhs(Rs, qs, eng.to_soa(q_n, eng.nv), eng.to_soa(q_nm1, eng.nv), theta, dt,
+                          eng.empty(eng.nv, eng.N))
+        flags, cell, secs = st.implicit_dual(qs, rhs, cfl, theta, dt, out)
+    else:
+        flags, cell, secs = st.implicit(qs, Rs, cfl, out)
     flags &= ~F_KSKIP
     if flags:
         eng.raise_for(flags, cell, "_implicit_step")
@@ -348,13 +350,17 @@ def implicit_step_raw(case, q, R, cfl, dom_override=None, path=0, want_dq=False)
     return res
 
 
-def _step_device(st, q_t, R_t, cfl, out_t):
-    """_step_with_retries (driver.py:254-263) on device buffers.
+def _step_device(st, q_t, R_t, cfl, out_t, dual=None):
+    """_step_with_retries (driver.py:254-263) on device buffers; ``dual`` =
+    (rhs, theta, dt) runs dual-time steps from the formed rhs.
     Returns (cfl_used, implicit_seconds, retries)."""
     eng = st.eng
     total = 0.0
     for attempt in range(MAX_STEP_RETRIES + 1):
-        flags, cell, secs = st.implicit(q_t, R_t, cfl, out_t)
+        if dual is None:
+            flags, cell, secs = st.implicit(q_t, R_t, cfl, out_t)
+        else:
+            flags, cell, secs = st.implicit_dual(q_t, dual[0], cfl, dual[1], dual[2], out_t)
         total += secs
         flags &= ~F_KSKIP
         # first failure in the reference's stage order (driver.py:235-250):
@@ -396,7 +402,7 @@ def steady_solve(case, q0=None, *, return_device=False):
     cfl_scale = 1.0
     samples = []
     walls = bool(_wall_faces(case.bcs))
-    geom = _WallGeom(case.grid, case.bcs) if walls else None
+    geom = _WallGeom(eng, case.grid, case.bcs) if walls else None
     for it in range(1, case.max_iters + 1):
         t0 = time.perf_counter()
         residual_device(eng, q, case.first_order, R=st.R)
@@ -407,8 +413,7 @@ def steady_solve(case, q0=None, *, return_device=False):
         sample = float("nan")
         if case.monitor_rel_change is not None or walls:
             if it % case.monitor_every == 0 or it == 1:
-                sample = _stagnation_monitor_device(eng, q, geom, case.bcs, case.model) \
-                    if walls else float("nan")
+                sample = _stagnation_monitor_device(eng, q, geom) if walls else float("nan")
                 samples.append(sample)
         cfl_now = case.cfl_at(it - 1) * cfl_scale
         if case.stop_on_absolute_floor and norms.density <= ref_floor:
@@ -443,5 +448,73 @@ def steady_solve(case, q0=None, *, return_device=False):
     return eng.from_soa(q, like, tuple(eng.dims) + (eng.nv,)), hist
 
 
+def _step_with_retries(case, q, R, cfl, theta=0.0, dt=None, q_n=None, q_nm1=None):
+    """Implicit step with CFL halving on NonPhysicalState (driver.py:254-263);
+    returns ((q_new, implicit_seconds), cfl_used)."""
+    st = _Stepper(case)
+    eng = st.eng
+    qs, Rs = eng.to_soa(q, eng.nv), eng.to_soa(R, eng.nv)
+    out = eng.empty(eng.nv, eng.N)
+    dual = None
+    if _is_dual(dt):
+        dual = (st.dual_rhs(Rs, qs, eng.to_soa(q_n, eng.nv), eng.to_soa(q_nm1, eng.nv), theta, dt,
+                            eng.empty(eng.nv, eng.N)), theta, dt)
+    cfl_used, secs, _ = _step_device(st, qs, Rs, cfl, out, dual)
+    if isinstance(q, SoA):
+        return (SoA(out, eng.dims), secs), cfl_used
+    return (eng.from_soa(out, q, tuple(eng.dims) + (eng.nv,)), secs), cfl_used
+
+
+def unsteady_solve(case, q0=None):
+    """Dual-time unsteady march; returns (snapshots, times, ConvergenceHistory)
+    (driver.py:320-359).  Physical step 1 runs first order in time
+    (theta = 0); each physical step iterates in pseudo time until the inner
+    residual |rhs| has dropped ``inner_orders`` decades or ``inner_max``
+    iterations ran.  Everything stays on the device; one small read per inner
+    iteration (the rhs norm) drives the stopping test."""
+    if case.dt is None or not np.isfinite(case.dt) or case.dt <= 0:
+        raise ValueError("unsteady_solve requires a positive physical dt")
+    st = _Stepper(case)
+    eng = st.eng
+    nv, N = eng.nv, eng.N
+    q_init = case.initial_field() if q0 is None else q0
+    q_n = eng.to_soa(q_init, nv).clone()
+    q_nm1 = q_n.clone()
+    like = q0 if (q0 is not None and is_torch(q0)) else np.empty(0)
+    shape = tuple(eng.dims) + (nv,)
+    snap = lambda t: eng.from_soa(t, like, shape)
+    snapshots, times = [snap(q_n)], [0.0]
+    hist = ConvergenceHistory(metadata={"scheme": case.scheme, "dt": case.dt, "theta": case.theta})
+    rhs = eng.empty(nv, N)
+    q_next = eng.empty(nv, N)
+    ss = eng.empty(1)
+    for step in range(1, case.n_steps + 1):
+        theta = 0.0 if step == 1 else case.theta
+        q_m = q_n.clone()
+        inner0 = None
+        for _inner in range(1, case.inner_max + 1):
+            t0 = time.perf_counter()
+            residual_device(eng, q_m, case.first_order, R=st.R)
+            st.dual_rhs(st.R, q_m, q_n, q_nm1, theta, case.dt, rhs)
+            eng._chk(eng.lib.csb_sum_squares(eng.ctx, nv * N, rhs.data_ptr(), ss.data_ptr(),
+                                             ctypes.c_void_p(eng.stream)), "inner residual")
+            rnorm = float(np.sqrt(ss.item()))
+            if inner0 is None:
+                inner0 = max(rnorm, 1e-300)
+            if not np.isfinite(rnorm):
+                raise Diverged(f"non-finite inner residual at step {step}")
+            if rnorm <= inner0 * 10.0 ** (-case.inner_orders) or rnorm == 0.0:
+                break
+            _, t_imp, _ = _step_device(st, q_m, st.R, case.cfl, q_next, (rhs, theta, case.dt))
+            q_m, q_next = q_next, q_m
+            hist.record(len(hist.iters) + 1, GroupedResidual(rnorm, rnorm, rnorm), float("nan"),
+                        time.perf_counter() - t0, t_imp, case.cfl)
+        q_nm1, q_n = q_n, q_m
+        snapshots.append(snap(q_n))
+        times.append(step * case.dt)
+    return snapshots, times, hist
+
+
 __all__ = ["Case", "ConvergenceHistory", "GroupedResidual", "MAX_STEP_RETRIES", "residual_norms",
-           "steady_solve", "wall_heat_flux", "_apply_update", "_implicit_step"]
+           "steady_solve", "unsteady_solve", "wall_heat_flux", "_apply_update", "_implicit_step",
+           "_step_with_retries"]

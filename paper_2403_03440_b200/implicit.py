@@ -18,16 +18,19 @@ import numpy as np
 
 from .device import OP_FIELDS, SCHEMES, SoA, get_engine, is_torch
 from .errors import NonPhysicalState, SingularDiagonal
-from .mixture import EPS_NEG, MixtureModel, nitrogen_like
+from .mixture import EPS_NEG
 
 MODES = ("CI", "CS1", "CS2")
 
-_UTIL_MODEL = MixtureModel(species=(nitrogen_like(),), Pr=0.72, Sc=0.7)
+_UTIL_MODEL = []
 
 
 def util_engine():
     """Grid-free engine for element-wise utilities (flags + scratch only)."""
-    return get_engine(None, _UTIL_MODEL)
+    if not _UTIL_MODEL:
+        from .configs import cloned_mixture
+        _UTIL_MODEL.append(cloned_mixture(1))
+    return get_engine(None, _UTIL_MODEL[0])
 
 
 def _dev(eng, x):
@@ -70,6 +73,28 @@ def local_time_step(lam_inv, lam_vis, lam_S, cfl, J):
     eng.check("local_time_step", order=("zero",))
     like = lam_inv if is_torch(lam_inv) else None
     return _out(eng, out, like, shape)
+
+
+def dual_time_rhs(R, q_m, q_n, q_nm1, theta, dt, volume):
+    """RHS = -R - V [(1 + theta)(Q^m - Q^n) - theta (Q^n - Q^{n-1})] / dt
+    (implicit.py:47-56) on the device; steady mode (dt None or inf) is -R."""
+    if dt is None or not np.isfinite(dt):
+        return -R if is_torch(R) else -np.asarray(R)
+    from .device import engine_for_ns
+    shape = tuple(R.shape)
+    nv = shape[-1]
+    eng = engine_for_ns(nv - 5)
+    n = int(np.prod(shape[:-1])) if len(shape) > 1 else 1
+    soa = lambda x: eng.to_soa(_dev(eng, x).reshape(n, nv) if is_torch(x) else
+                               np.broadcast_to(np.asarray(x, dtype=float), shape).reshape(n, nv), nv)
+    V = _dev(eng, volume).expand(shape[:-1]).contiguous().reshape(n) if len(shape) > 1 else \
+        _dev(eng, volume).reshape(1)
+    out = eng.empty(nv, n)
+    eng._chk(eng.lib.csb_dual_time_rhs(eng.ctx, n, V.data_ptr(), soa(R).data_ptr(), soa(q_m).data_ptr(),
+                                       soa(q_n).data_ptr(), soa(q_nm1).data_ptr(), float(theta),
+                                       float(dt), out.data_ptr(), ctypes.c_void_p(eng.stream)),
+             "dual_time_rhs")
+    return eng.from_soa(out, R if is_torch(R) else np.empty(0), shape)
 
 
 def _q_of(prim, model):
@@ -264,85 +289,6 @@ class ImplicitOperator:
         t = self._field("dinv", ns * ns, tuple(self._eng.dims) + (ns * ns,))
         return t.reshape(tuple(self._eng.dims) + (ns, ns))
 
-    # -- dense materialisation (the reference's test oracle, implicit.py:246-326)
-    def _np(self, x):
-        return x.detach().cpu().numpy() if is_torch(x) else np.asarray(x)
-
-    def _block(self, cell, S, lam, sign, flow_only=False):
-        n = 5 if flow_only else self.nvar
-        w = self._np(self.w)[cell][:n]
-        b = self._np(self.b)[cell][:n]
-        rho = float(self._np(self.rho)[cell])
-        u = self._np(self.u)[cell]
-        U = float(u @ S)
-        a = np.zeros(n)
-        a[0] = -U / rho
-        a[1:4] = S / rho
-        v = np.zeros(n)
-        v[1:4] = S
-        v[4] = U
-        A = np.outer(w, a) + np.outer(v, b)
-        A[np.diag_indices(n)] += U + sign * lam
-        return 0.5 * A
-
-    def offdiag_block(self, cell, d, side):
-        nb = list(cell)
-        nb[d] += 1 if side else -1
-        nb = tuple(nb)
-        f = list(cell)
-        if side:
-            f[d] += 1
-        f = tuple(f)
-        S = self.grid.face_areas(d)[f]
-        lam = float(self._np(self.lam_face[d])[f])
-        n = self.nvar
-        if self.mode == "CI":
-            blk = self._block(nb, S, lam, +1.0 if side == 0 else -1.0)
-            return -blk if side == 0 else blk
-        out = np.zeros((n, n))
-        flow = self._block(nb, S, lam, +1.0 if side == 0 else -1.0, flow_only=True)
-        out[:5, :5] = -flow if side == 0 else flow
-        lam_sp = float(self._np(self.lam_face_sp[d])[f])
-        U_nb = float(self._np(self.u)[nb] @ S)
-        coeff = self.sp_scale * (U_nb + lam_sp) if side == 0 else self.sp_scale * (U_nb - lam_sp)
-        out[5:, 5:] = np.eye(n - 5) * (-coeff if side == 0 else coeff)
-        return out
-
-    def diag_block(self, cell):
-        n = self.nvar
-        D = np.eye(n) * float(self._np(self.d_scal)[cell])
-        if self.mode == "CI":
-            vd = self.vdom
-            if vd is not None:
-                D[5:, 5:] -= self._np(vd)[cell]
-        else:
-            D[5:, 5:] = np.diag(self._np(self.d_species)[cell])
-        return D
-
-    def dense_factored_matrix(self):
-        """(D+L) D^-1 (D+U) as one dense matrix (small grids; test oracle)."""
-        ni, nj, nk = self.grid.dims
-        n = self.nvar
-        N = ni * nj * nk
-        idx = lambda i, j, k: (i * nj + j) * nk + k
-        D = np.zeros((N * n, N * n))
-        L = np.zeros_like(D)
-        U = np.zeros_like(D)
-        unit = ((1, 0, 0), (0, 1, 0), (0, 0, 1))
-        for i in range(ni):
-            for j in range(nj):
-                for k in range(nk):
-                    r = idx(i, j, k) * n
-                    D[r:r + n, r:r + n] = self.diag_block((i, j, k))
-                    for d, (di, dj, dk) in enumerate(unit):
-                        if (i, j, k)[d] > 0:
-                            c = idx(i - di, j - dj, k - dk) * n
-                            L[r:r + n, c:c + n] = self.offdiag_block((i, j, k), d, 0)
-                        if (i, j, k)[d] < (ni, nj, nk)[d] - 1:
-                            c = idx(i + di, j + dj, k + dk) * n
-                            U[r:r + n, c:c + n] = self.offdiag_block((i, j, k), d, 1)
-        return (D + L) @ np.linalg.inv(D) @ (D + U)
-
 
 def _dtau_device(eng, dtau):
     torch = eng.torch
@@ -444,6 +390,6 @@ def correct_normalize_cs2(rho_s, d_rho_s, d_rho, eps_neg: float = EPS_NEG):
     return _correct(2, rho_s, d_rho_s, d_rho, eps_neg)
 
 
-__all__ = ["MODES", "ImplicitOperator", "assemble_lhs", "cell_spectral_radii",
+__all__ = ["MODES", "ImplicitOperator", "assemble_lhs", "cell_spectral_radii", "dual_time_rhs",
            "correct_increment_cs1", "correct_normalize_cs2", "local_time_step", "SingularDiagonal",
            "species_block_inverse"]

@@ -39,9 +39,11 @@ import csflow.lusgs as ref_lusgs  # noqa: E402
 from csflow.boundary import BoundaryCondition  # noqa: E402
 from csflow.chemistry import (Mechanism, Reaction, production_rates, source_jacobian,  # noqa: E402
                               source_spectral_radius)
-from csflow.driver import Case, residual_norms, steady_solve  # noqa: E402
+from csflow.driver import (Case, _implicit_step, _stagnation_monitor, residual_norms,  # noqa: E402
+                           steady_solve, unsteady_solve, wall_heat_flux)
 from csflow.grid import compute_metrics  # noqa: E402
-from csflow.implicit import assemble_lhs, cell_spectral_radii, local_time_step  # noqa: E402
+from csflow.implicit import (assemble_lhs, cell_spectral_radii, dual_time_rhs,  # noqa: E402
+                             local_time_step)
 from csflow.lusgs import lusgs_solve  # noqa: E402
 from csflow.mixture import (MixtureModel, SpeciesData, cons_to_prim, make_primitive,  # noqa: E402
                             prim_to_cons)
@@ -144,6 +146,12 @@ def one_iteration(name, spec, schemes, offdiag="symmetrized", first_order=False)
                              return_padded=True)
     put(name, "R", R)
     put(name, "P", P)
+    walls = [f for f in FACES if spec.bcs[f].kind == "noslip_isothermal"]
+    if walls:  # wall heat flux + stagnation monitor (driver.py:132-205)
+        qw = wall_heat_flux(P, grid, bcs, model)
+        for f in walls:
+            put(name, f"qw_{f}", qw[f])
+        put(name, "q_stag", _stagnation_monitor(P, grid, bcs, model))
     put(name, "first_order", first_order)
     R1 = assemble_residual(q, grid, bcs, mech, model, first_order=True)
     put(name, "R_first_order", R1)
@@ -321,6 +329,7 @@ def march_case():
         put(spec.name, "res_species", hist.res_species)
         put(spec.name, "res_density", hist.res_density)
         put(spec.name, "cfl_used", hist.cfl)
+        put(spec.name, "q_stag_hist", hist.q_stag)
         put(spec.name, "q_final", q)
         put(spec.name, "ramp", [5.0, 2.0, 10])
 
@@ -352,6 +361,65 @@ def march_c4_case():
     put(name, "fs_prim", np.concatenate(([rho], u, [T], Y)))
 
 
+def generators_case():
+    """Reference grid generators (grid.py:102-162) for the device node fill."""
+    from csflow.grid import generate_box, generate_cylinder_ogrid
+    put("gen", "box", generate_box((0.3, 0.2, 0.1), (7, 5, 3)))
+    put("gen", "ogrid", generate_cylinder_ogrid(1.0, 3.5, (20, 16, 2), stretch=1.05))
+    put("gen", "ogrid_first_cell", generate_cylinder_ogrid(0.045, 0.145, (8, 16, 1),
+                                                           first_cell=1e-4))
+    put("gen", "ogrid_quarter", generate_cylinder_ogrid(0.045, 0.2, (12, 9, 1),
+                                                        theta_deg=(180.0, 90.0), span=0.02))
+
+
+def dual_time_case():
+    """Dual-time stepping (implicit.py:47-56, 346-348; driver.py:320-359):
+    the unsteady right-hand side, one implicit step with the (1+theta)V/dt
+    diagonal, and a short unsteady_solve, on a perturbed 3-D box with a
+    binary mixture (the reference's box_case idiom, test_driver.py)."""
+    rng = np.random.default_rng(71)
+    a = C.SpeciesSpec("A", 0.028, 1039.0, 0.0, 0.0, 1.663e-5, 273.15, 107.0)
+    b = C.SpeciesSpec("B", 0.032, 918.0, 2.5e5, 298.15, 1.919e-5, 273.15, 139.0)
+    sp = [a, b]
+    dims = (5, 4, 3)
+    nodes = C.box_nodes((5e-3, 4e-3, 3e-3), dims)
+    Y0 = np.array([0.6, 0.4])
+    fs = (1.0, (80.0, -20.0, 10.0), 400.0, Y0)
+    bcs_spec = {f: C.BCSpec("farfield", fs=fs) for f in FACES}
+    bcs_spec["kmin"] = C.BCSpec("noslip_isothermal", T_wall=350.0)
+    rho = 1.0 + 0.05 * rng.standard_normal(dims)
+    vel = np.array([80.0, -20.0, 10.0]) + 5.0 * rng.standard_normal(dims + (3,))
+    T = 400.0 + 20.0 * rng.standard_normal(dims)
+    Yp = np.clip(0.6 + 0.05 * rng.standard_normal(dims), 0.3, 0.9)
+    Y = np.stack([Yp, 1.0 - Yp], axis=-1)
+    q = C.encode_state(rho, vel, T, Y, sp)
+    spec = C.CaseSpec("dual", nodes, sp, bcs_spec, q, 5.0)
+    store_inputs("dual", spec)
+    model = ref_model(spec)
+    grid = compute_metrics(nodes)
+    bcs = ref_bcs(spec, model)
+    q_n = q * (1.0 + 1e-3 * rng.standard_normal(q.shape))
+    q_nm1 = q * (1.0 + 1e-3 * rng.standard_normal(q.shape))
+    R = assemble_residual(q, grid, bcs, None, model)
+    put("dual", "q_n", q_n)
+    put("dual", "q_nm1", q_nm1)
+    theta, dt = 2.0, 2e-6
+    put("dual", "theta_dt", [theta, dt])
+    put("dual", "rhs", dual_time_rhs(R, q, q_n, q_nm1, theta, dt, grid.volume))
+    put("dual", "rhs_theta0", dual_time_rhs(R, q, q_n, q_nm1, 0.0, dt, grid.volume))
+    fr = make_primitive(model, rho=fs[0], u=fs[1], T=fs[2], Y=fs[3])
+    for sch in ("CS1", "CI"):
+        case = Case(grid=grid, model=model, bcs=bcs, freestream=fr, scheme=sch, cfl=5.0)
+        qn, _ = _implicit_step(case, q, R, 5.0, theta, dt, q_n, q_nm1)
+        put("dual", f"{sch}/q_new", qn)
+    case = Case(grid=grid, model=model, bcs=bcs, freestream=fr, scheme="CS1", cfl=5.0,
+                dt=2e-6, theta=2.0, n_steps=3, inner_max=6, inner_orders=3.0)
+    snaps, times, hist = unsteady_solve(case, q0=q)
+    put("dual", "snapshots", np.stack(snaps))
+    put("dual", "times", times)
+    put("dual", "inner_res", hist.res_flow)
+
+
 def main():
     spec = C.config0(seed=11, dims=(8, 6, 1))
     one_iteration("box_air5", spec, ("CI", "CS1", "CS2"))
@@ -364,6 +432,8 @@ def main():
     chem_rates_case()
     march_case()
     march_c4_case()
+    generators_case()
+    dual_time_case()
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **OUT)
     print(f"wrote {path}: {len(OUT)} arrays, {os.path.getsize(path) / 1e6:.2f} MB")

@@ -12,6 +12,8 @@ pkg/tests/test_driver.py (fixed point 40-50, norms 53-66).
 import numpy as np
 import pytest
 
+from dense_operator import dense_factored_matrix
+
 pytestmark = pytest.mark.gpu
 
 
@@ -94,7 +96,7 @@ def test_lusgs_matches_dense_factored_solve(mode, with_chem):
     grid, q, op = _uniform_operator(model, mode, mech=mech, seed=5)
     rhs = np.random.default_rng(6).standard_normal(q.shape) * 100.0
     dq = lusgs.lusgs_solve(op, rhs)
-    expect = np.linalg.solve(op.dense_factored_matrix(), rhs.reshape(-1)).reshape(q.shape)
+    expect = np.linalg.solve(dense_factored_matrix(op, grid), rhs.reshape(-1)).reshape(q.shape)
     np.testing.assert_allclose(dq, expect, atol=1e-12 * np.max(np.abs(expect)))
 
 
@@ -105,7 +107,7 @@ def test_lusgs_paper_offdiag_variant_matches_dense(mode):
                                     species_offdiag="paper")
     rhs = np.random.default_rng(9).standard_normal(q.shape)
     dq = lusgs.lusgs_solve(op, rhs)
-    expect = np.linalg.solve(op.dense_factored_matrix(), rhs.reshape(-1)).reshape(q.shape)
+    expect = np.linalg.solve(dense_factored_matrix(op, grid), rhs.reshape(-1)).reshape(q.shape)
     np.testing.assert_allclose(dq, expect, atol=1e-12 * np.max(np.abs(expect)))
 
 

@@ -287,6 +287,12 @@ def test_steady_march_matches_reference_history(name):
         assert got.shape == ref.shape
         assert np.max(np.abs(np.log10(got) - np.log10(ref))) <= 1e-9, key
     assert comp_relerr(q, get(name, "q_final")) <= 1e-9
+    # stagnation heat-flux monitor samples (device wall flux, driver.py:187-205)
+    got_qs, ref_qs = np.asarray(hist.q_stag, float), get(name, "q_stag_hist")
+    assert np.array_equal(np.isnan(got_qs), np.isnan(ref_qs))
+    m = ~np.isnan(ref_qs)
+    assert m.sum() >= 6
+    assert np.max(np.abs(got_qs[m] - ref_qs[m]) / np.abs(ref_qs[m])) <= 1e-9
 
 
 def test_config4_reduced_march_matches_reference_history():
