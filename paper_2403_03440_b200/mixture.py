@@ -189,7 +189,7 @@ def _primitive_call(model, rho, u, p, T, Y, want_prim, want_q):
     shape = tuple(np.broadcast_shapes(*shapes))
     n = int(np.prod(shape)) if shape else 1
     dev = lambda x, tail=(): (None if x is None else torch.from_numpy(
-        np.ascontiguousarray(np.broadcast_to(x, shape + tail), dtype=float).reshape(-1)).to(eng.device))
+        np.array(np.broadcast_to(x, shape + tail), dtype=float).reshape(-1)).to(eng.device))
     tr, tp, tT = dev(rho), dev(p), dev(T)
     tu, tY = dev(u, (3,)), dev(Y, (ns,))
     out = eng.empty(12 + ns, n) if want_prim else None
