@@ -228,28 +228,39 @@ __global__ void k_wall_flux(const Model* __restrict__ mp, GridDev g, int axis, i
     double nh[3];
 #pragma unroll
     for (int x = 0; x < 3; ++x) nh[x] = side ? -__ddiv_rn(S[x], nrm) : __ddiv_rn(S[x], nrm);
+    // centroids in numpy's summation order (driver.py:147-149, 161-163): the
+    // wall distances are differences of O(1) positions that agree to ~1e-5
+    // relative on stretched wall grids, so every rounding is reproduced
+    // (slab plane of cell layer l, normal node offset o: side 0 l + o,
+    // side 1 l + 1 - o)
     double fc[3], cc[2][3];
+    const int offs[8][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1},
+                            {1, 1, 0}, {1, 0, 1}, {0, 1, 1}, {1, 1, 1}};
 #pragma unroll
     for (int x = 0; x < 3; ++x) {
-      fc[x] = 0.25 * (((node(0, t1, t2, x) + node(0, t1 + 1, t2, x)) + node(0, t1, t2 + 1, x)) +
-                      node(0, t1 + 1, t2 + 1, x));
+      fc[x] = __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(node(0, t1, t2, x), node(0, t1 + 1, t2, x)),
+                                                  node(0, t1, t2 + 1, x)),
+                                        node(0, t1 + 1, t2 + 1, x)));
 #pragma unroll
       for (int l = 0; l < 2; ++l) {
         double acc = 0.0;
 #pragma unroll
-        for (int pl = 0; pl < 2; ++pl)
-#pragma unroll
-          for (int d1 = 0; d1 < 2; ++d1)
-#pragma unroll
-            for (int d2 = 0; d2 < 2; ++d2) acc += node(l + pl, t1 + d1, t2 + d2, x);
-        cc[l][x] = 0.125 * acc;
+        for (int v = 0; v < 8; ++v) {
+          const int on = offs[v][axis], o1 = offs[v][a1], o2 = offs[v][a2];
+          const double nv = node(side ? l + 1 - on : l + on, t1 + o1, t2 + o2, x);
+          acc = v == 0 ? nv : __dadd_rn(acc, nv);
+        }
+        cc[l][x] = __dmul_rn(0.125, acc);
       }
     }
     double dist[2];
 #pragma unroll
-    for (int l = 0; l < 2; ++l)
-      dist[l] = fabs(((cc[l][0] - fc[0]) * nh[0] + (cc[l][1] - fc[1]) * nh[1]) +
-                     (cc[l][2] - fc[2]) * nh[2]);
+    for (int l = 0; l < 2; ++l) {  // |einsum(c - fc, nhat)|: (x0 + x2) + x1
+      const double e0 = __dmul_rn(__dsub_rn(cc[l][0], fc[0]), nh[0]);
+      const double e1 = __dmul_rn(__dsub_rn(cc[l][1], fc[1]), nh[1]);
+      const double e2 = __dmul_rn(__dsub_rn(cc[l][2], fc[2]), nh[2]);
+      dist[l] = fabs(__dadd_rn(__dadd_rn(e0, e2), e1));
+    }
     // first two cells off the wall
     int ci[3];
     ci[a1] = t1;
@@ -263,7 +274,9 @@ __global__ void k_wall_flux(const Model* __restrict__ mp, GridDev g, int axis, i
     ok = decode<NSB>(m, q + c2, g.N, P2) && ok;
     if (!ok) raise_flag(flags, EB_DECODE, c1);
     const double d1 = dist[0], d2 = dist[1];
-    const double dTdn = ((P1.T - Tw) * (d2 * d2) - (P2.T - Tw) * (d1 * d1)) / (d1 * d2 * (d2 - d1));
+    const double dTdn = __ddiv_rn(__dsub_rn(__dmul_rn(P1.T - Tw, __dmul_rn(d2, d2)),
+                                            __dmul_rn(P2.T - Tw, __dmul_rn(d1, d1))),
+                                  __dmul_rn(__dmul_rn(d1, d2), __dsub_rn(d2, d1)));
     double mu, kc, D;
     transport<NSB>(m, Tw, P1.Y, P1.p / (P1.R * Tw), mu, kc, D);
     qw[e] = kc * dTdn;

@@ -90,9 +90,11 @@ def dual_time_rhs(R, q_m, q_n, q_nm1, theta, dt, volume):
     V = _dev(eng, volume).expand(shape[:-1]).contiguous().reshape(n) if len(shape) > 1 else \
         _dev(eng, volume).reshape(1)
     out = eng.empty(nv, n)
-    eng._chk(eng.lib.csb_dual_time_rhs(eng.ctx, n, V.data_ptr(), soa(R).data_ptr(), soa(q_m).data_ptr(),
-                                       soa(q_n).data_ptr(), soa(q_nm1).data_ptr(), float(theta),
-                                       float(dt), out.data_ptr(), ctypes.c_void_p(eng.stream)),
+    # (named: a temporary's data_ptr() would dangle before the launch)
+    tR, tm, tn, tnm1 = soa(R), soa(q_m), soa(q_n), soa(q_nm1)
+    eng._chk(eng.lib.csb_dual_time_rhs(eng.ctx, n, V.data_ptr(), tR.data_ptr(), tm.data_ptr(),
+                                       tn.data_ptr(), tnm1.data_ptr(), float(theta), float(dt),
+                                       out.data_ptr(), ctypes.c_void_p(eng.stream)),
              "dual_time_rhs")
     return eng.from_soa(out, R if is_torch(R) else np.empty(0), shape)
 

@@ -178,7 +178,7 @@ def test_wall_heat_flux_matches_reference(case, face):
         got = driver.wall_heat_flux(src, grid, bcs, model)
         assert set(got) == {face}
         assert got[face].shape == ref.shape
-        assert np.max(np.abs(got[face] - ref)) <= 1e-11 * np.max(np.abs(ref))
+        assert np.max(np.abs(got[face] - ref)) <= 1e-12 * np.max(np.abs(ref))
     eng = driver.get_engine(grid, model)
     eng.set_bcs(bcs)
     geom = driver._WallGeom(eng, grid, bcs)
