@@ -32,6 +32,7 @@ struct csb_ctx {
   Model* d_model = nullptr;
   std::vector<Reaction> rx;
   Reaction* d_rx = nullptr;
+  int* d_sprx = nullptr;  // [ns + 1] offsets | reaction lists (Mech::sp_off / sp_rx)
   int nrx_active = 0;
   GridDev g{};
   int geom2d_ok = 0;
@@ -81,6 +82,8 @@ Mech mech_of(const csb_ctx* c) {
   Mech m;
   m.nrx = c->nrx_active;
   m.rx = c->d_rx;
+  m.sp_off = c->d_sprx;
+  m.sp_rx = c->d_sprx ? c->d_sprx + c->ns + 1 : nullptr;
   return m;
 }
 
@@ -293,6 +296,7 @@ void csb_destroy(csb_ctx* c) {
   if (!c) return;
   if (c->d_model) cudaFree(c->d_model);
   if (c->d_rx) cudaFree(c->d_rx);
+  if (c->d_sprx) cudaFree(c->d_sprx);
   if (c->d_fs) cudaFree(c->d_fs);
   if (c->wb.s2) cudaStreamDestroy(c->wb.s2);
   if (c->wb.e1) cudaEventDestroy(c->wb.e1);
@@ -384,6 +388,29 @@ int csb_set_mechanism(csb_ctx* c, int nrx, const double* nu_r, const double* nu_
       return fail(c, CSB_E_CUDA, "cudaMalloc(reactions)");
     cudaError_t e = cudaMemcpy(c->d_rx, v.data(), sizeof(Reaction) * v.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_check(c, e, "upload reactions");
+  }
+  // species -> reactions CSR for the sparse finite-difference Jacobian
+  if (c->d_sprx) {
+    cudaFree(c->d_sprx);
+    c->d_sprx = nullptr;
+  }
+  if (!v.empty()) {
+    std::vector<int> off(ns + 1, 0), lst;
+    for (int s = 0; s < ns; ++s) {
+      for (int r = 0; r < (int)v.size(); ++r) {
+        bool dep = false;
+        for (int t = 0; t < v[r].nr; ++t) dep |= v[r].rs[t] == s;
+        for (int t = 0; t < v[r].np && v[r].has_back; ++t) dep |= v[r].ps[t] == s;
+        if (dep) lst.push_back(r);
+      }
+      off[s + 1] = (int)lst.size();
+    }
+    std::vector<int> all(off);
+    all.insert(all.end(), lst.begin(), lst.end());
+    if (cudaMalloc(&c->d_sprx, sizeof(int) * all.size()) != cudaSuccess)
+      return fail(c, CSB_E_CUDA, "cudaMalloc(species-reaction map)");
+    cudaError_t e = cudaMemcpy(c->d_sprx, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_check(c, e, "upload species-reaction map");
   }
   c->rx = v;
   c->nrx_active = (enabled && nrx > 0) ? nrx : 0;

@@ -68,6 +68,10 @@ struct Reaction {
 struct Mech {
   int nrx;  // 0 = frozen
   const Reaction* rx;
+  // species -> reactions whose rate depends on it (reactant or product),
+  // CSR: reactions of species s at sp_rx[sp_off[s] .. sp_off[s + 1])
+  const int* sp_off;
+  const int* sp_rx;
 };
 
 struct GridDev {

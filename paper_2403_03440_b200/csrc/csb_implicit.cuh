@@ -64,9 +64,39 @@ __global__ void k_decode(const Model* __restrict__ mp, GridDev g, const double* 
 }
 
 // ------------------------------------------------- source Jacobian (FD, T fixed)
-// chemistry.py:76-104.  dom_full: write all ns*ns entries ([s*ns+r][N]),
-// else the diagonal [s][N].  lamS: row-sum bound.  dom_in (optional):
-// injected dOmega used instead of the finite differences.
+// chemistry.py:76-104: dOmega[:, r] = (omega(rho_s + h e_r) - omega(rho_s - h e_r)) / (2 h),
+// h = max(1e-8 |rho_r|, 1e-12 rho), T held fixed.  The two perturbed states
+// differ only in species r, so only the reactions whose rate depends on
+// species r (Mech::sp_off / sp_rx) contribute to column r: each of them is
+// evaluated at the two states exactly as the reference evaluates it (rate
+// constants, then the concentration factors in stoichiometric order) and the
+// difference of the two rates is scattered with the net stoichiometry.  This
+// is the reference's finite difference without the rounding noise its two
+// full sums leave in the untouched reactions (within the FD-noise
+// bound), at O(reactions per species) instead of O(ns x reactions) rate
+// evaluations per column.  A non-finite perturbed rate makes the column NaN,
+// as it does in the reference.  dom_full: all ns*ns entries ([s*ns+r][N]),
+// else the diagonal [s][N].  lamS: row-sum bound max_s sum_r |dOmega_sr|.
+// dom_in (optional): injected dOmega instead of the differences.
+CSB_DEV double rate_at(const Reaction& rx, double T, const double* conc, int r, double cr) {
+  double rate = rx.Af * pow(T, rx.bf) * exp(-rx.Eaf / (R_U * T));
+  for (int t = 0; t < rx.nr; ++t) {
+    const double c = rx.rs[t] == r ? cr : conc[rx.rs[t]];
+    const double nu = rx.rn[t];
+    rate = rate * (nu == 1.0 ? c : (nu == 2.0 ? c * c : pow(c, nu)));
+  }
+  if (rx.has_back) {
+    double rb = rx.Ab * pow(T, rx.bb) * exp(-rx.Eab / (R_U * T));
+    for (int t = 0; t < rx.np; ++t) {
+      const double c = rx.ps[t] == r ? cr : conc[rx.ps[t]];
+      const double nu = rx.pn[t];
+      rb = rb * (nu == 1.0 ? c : (nu == 2.0 ? c * c : pow(c, nu)));
+    }
+    rate = rate - rb;
+  }
+  return rate;
+}
+
 template <int NSB>
 __global__ void k_source_jac(const Model* __restrict__ mp, GridDev g, Mech mech,
                              const double* __restrict__ q, double* __restrict__ dom, int dom_full,
@@ -78,48 +108,37 @@ __global__ void k_source_jac(const Model* __restrict__ mp, GridDev g, Mech mech,
        c += (long long)gridDim.x * blockDim.x) {
     Cell<NSB> cs;
     if (!decode<NSB>(m, q + c, g.N, cs)) raise_flag(flags, EB_DECODE, c);
-    double rowsum[NSB];
+    double rowsum[NSB], rs[NSB], conc[NSB], acc[NSB];
 #pragma unroll
-    for (int s = 0; s < NSB; ++s) rowsum[s] = 0.0;
-    double rs[NSB];
-#pragma unroll
-    for (int s = 0; s < NSB; ++s) rs[s] = (s < ns) ? cs.rho * cs.Y[s] : 0.0;
+    for (int s = 0; s < NSB; ++s) {
+      rowsum[s] = 0.0;
+      rs[s] = (s < ns) ? cs.rho * cs.Y[s] : 0.0;
+      conc[s] = (s < ns) ? rs[s] / m.M[s] : 0.0;
+    }
     for (int r = 0; r < ns; ++r) {
-      double col[NSB];
       if (dom_in) {
-#pragma unroll
-        for (int s = 0; s < NSB; ++s)
-          if (s < ns) col[s] = dom_in[((long long)s * ns + r) * g.N + c];
+        for (int s = 0; s < ns; ++s) acc[s] = dom_in[((long long)s * ns + r) * g.N + c];
       } else {
         const double h = npmax(1e-8 * fabs(rs[r]), 1e-12 * cs.rho);
-        double up[NSB], dn[NSB], op[NSB], om[NSB];
-#pragma unroll
-        for (int s = 0; s < NSB; ++s) {
-          up[s] = rs[s];
-          dn[s] = rs[s];
+        const double cup = (rs[r] + h) / m.M[r], cdn = (rs[r] - h) / m.M[r];
+        for (int s = 0; s < ns; ++s) acc[s] = 0.0;
+        bool bad = false;
+        for (int l = mech.sp_off[r]; l < mech.sp_off[r + 1]; ++l) {
+          const Reaction& rx = mech.rx[mech.sp_rx[l]];
+          const double a = rate_at(rx, cs.T, conc, r, cup);
+          const double b = rate_at(rx, cs.T, conc, r, cdn);
+          bad |= !finite(a) || !finite(b);
+          const double d = a - b;
+          for (int t = 0; t < rx.nd; ++t) acc[rx.ds[t]] += rx.dn[t] * d;
         }
-        // dynamic index into register arrays: do it with an unrolled select
-#pragma unroll
-        for (int s = 0; s < NSB; ++s)
-          if (s == r) {
-            up[s] = rs[s] + h;
-            dn[s] = rs[s] - h;
-          }
-        omega_cell_impl<NSB>(m, mech, cs.T, up, op);
-        omega_cell_impl<NSB>(m, mech, cs.T, dn, om);
         const double h2 = 2.0 * h;
-#pragma unroll
-        for (int s = 0; s < NSB; ++s)
-          if (s < ns) col[s] = (op[s] - om[s]) / h2;
+        for (int s = 0; s < ns; ++s) acc[s] = bad ? NAN : (acc[s] * m.M[s]) / h2;
       }
-#pragma unroll
-      for (int s = 0; s < NSB; ++s) {
-        if (s < ns) {
-          rowsum[s] += fabs(col[s]);
-          if (dom_full) dom[((long long)s * ns + r) * g.N + c] = col[s];
-          else if (s == r) dom[(long long)s * g.N + c] = col[s];
-        }
+      for (int s = 0; s < ns; ++s) {
+        rowsum[s] += fabs(acc[s]);
+        if (dom_full) dom[((long long)s * ns + r) * g.N + c] = acc[s];
       }
+      if (!dom_full) dom[(long long)r * g.N + c] = acc[r];
     }
     double mx = rowsum[0];
 #pragma unroll
