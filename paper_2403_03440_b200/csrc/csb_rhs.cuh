@@ -629,6 +629,25 @@ CSB_DEV bool face_visc2d(const Model& m, const double* sP, int ldP, int im, int 
   return ok;
 }
 
+// 2-D face enumeration of a tile: thread index f -> face (fi, fj) and its
+// flux-buffer slot fi * FY + fj (FY = TJ + (D == 1)).  j-faces enumerate the
+// TI x TJ faces in rows of TJ first and the tile's last face column (fj = TJ)
+// after them, so that with TJ = 16 every half warp reads one row of 16
+// consecutive cells from each staged plane: no shared-memory bank conflicts
+// (rows of TJ + 1 = 17 put two words of a half warp on one bank pair; measured
+// 1.43 wavefronts per ideal on the species MUSCL loads at config 4).
+template <int D>
+CSB_DEV void face_of2d(int f, int TI, int TJ, int& fi, int& fj) {
+  if (D == 0) {
+    fi = f / TJ;
+    fj = f % TJ;
+  } else {
+    const int m = TI * TJ;
+    fi = f < m ? f / TJ : f - m;
+    fj = f < m ? f % TJ : TJ;
+  }
+}
+
 template <int NSB, int D>
 CSB_DEV void visc_pass2d(const Model& m, const GridDev& g, const double* sP, int ldP, double* sF,
                          int maxf, int i0, int j0, int ci, int cj, int BY, int TIc, int TJc,
@@ -640,8 +659,10 @@ CSB_DEV void visc_pass2d(const Model& m, const GridDev& g, const double* sP, int
   const int nf = FX * FY;
   const int sd = D == 0 ? BY : 1, st = D == 0 ? 1 : BY;
   for (int f = threadIdx.x; f < nf; f += blockDim.x) {
-    const int fj = f % FY, fi = f / FY;
+    int fi, fj;
+    face_of2d<D>(f, TIc, TJc, fi, fj);
     if (fi >= fx || fj >= fy) continue;
+    const int fs = fi * FY + fj;  // flux-buffer slot
     const int ip = (fi + NG) * BY + (fj + NG);
     const int im = ip - sd;
     const int gi = i0 + fi, gj = j0 + fj;
@@ -667,7 +688,7 @@ CSB_DEV void visc_pass2d(const Model& m, const GridDev& g, const double* sP, int
     } else {
       face_metric2d<D>(g, gi, gj, S, xn, xt, hasm, hasp, cellm, cellp);
     }
-    if (!face_visc2d<NSB, D>(m, sP, ldP, im, ip, st, S, xn, xt, sF + f, maxf))
+    if (!face_visc2d<NSB, D>(m, sP, ldP, im, ip, st, S, xn, xt, sF + fs, maxf))
       raise_flag(flags, EB_FACE_T, hasp ? cellp : cellm);
   }
 }
@@ -872,9 +893,16 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
     for (int f = threadIdx.x; f < nf; f += blockDim.x) {
       // (d == 1 ? ... : ...) keeps both divisors compile-time with a fixed tile
       const int fk = K2D ? 0 : f % fz;
-      const int fj = K2D ? (d == 1 ? f % (TJ + 1) : f % TJ) : (f / fz) % fy;
-      const int fi = K2D ? (d == 1 ? f / (TJ + 1) : f / TJ) : f / (fz * fy);
+      int fi, fj;
+      if (K2D) {
+        if (d == 0) face_of2d<0>(f, TI, TJ, fi, fj);
+        else face_of2d<1>(f, TI, TJ, fi, fj);
+      } else {
+        fj = (f / fz) % fy;
+        fi = f / (fz * fy);
+      }
       if (K2D && (fi >= fx || fj >= fy)) continue;
+      const int fs = K2D ? fi * FY + fj : f;  // flux-buffer slot
       // local (staged) coordinates of the "p" cell (upper side of the face)
       int lx = fi + NG, ly = fj + NG, lz = K2D ? 0 : fk + NG;
       const int sd = d == 0 ? strideX : (d == 1 ? strideY : strideZ);
@@ -884,7 +912,7 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
       const int gi = i0 + fi, gj = j0 + fj, gk = k0 + fk;
       double S[3];
       load_S(g, d, face_index(g, d, gi, gj, gk), S);
-      if (!face_conv<NSB>(m, sP, ldP, imm, im, ip, ipp, S, first_order != 0, sF + f, maxf)) {
+      if (!face_conv<NSB>(m, sP, ldP, imm, im, ip, ipp, S, first_order != 0, sF + fs, maxf)) {
         const int nd = d == 0 ? g.ni : (d == 1 ? g.nj : g.nk);
         const int pos = d == 0 ? gi : (d == 1 ? gj : gk);
         int cm[3] = {gi, gj, gk};
