@@ -280,6 +280,51 @@ int csb_wall_heat_flux(csb_ctx* ctx, int face, const double* q, const double* sl
  * (driver.py:187-205 stagnation monitor): out3 = [key_max, val_at, index]. */
 int csb_argmax_pick(long long n, const double* key, const double* val, double* out3, void* stream);
 
+/* ------------------------------------------------------ device-resident march */
+/* Parameters of a steady march (driver.py:266-317, Case fields). */
+typedef struct csb_march_params {
+  int scheme;          /* CSB_CI / CSB_CS1 / CSB_CS2 */
+  int offdiag_paper;   /* species_offdiag == "paper" */
+  int first_order;
+  int max_retries;     /* CFL halvings per iteration before Diverged (driver.py:35: 5) */
+  double abs_floor;    /* stop when the density residual <= this (< 0: off), driver.py:288-291 */
+  double drop_factor;  /* stop when it <= first density residual x this (10^-orders; < 0: off) */
+} csb_march_params;
+
+/* Stop codes of csb_march_state (ints4[1]). */
+#define CSB_MARCH_RUNNING 0
+#define CSB_MARCH_CONVERGED_ABSOLUTE 1
+#define CSB_MARCH_CONVERGED_DROP 2
+#define CSB_MARCH_CONVERGED_PLATEAU 3
+#define CSB_MARCH_NAN_NORM 4          /* Diverged (driver.py:281-283) */
+#define CSB_MARCH_RETRIES 5           /* Diverged (driver.py:259-262) */
+#define CSB_MARCH_ZERO_WAVESPEED 6    /* ZeroWavespeed */
+#define CSB_MARCH_SINGULAR 7          /* SingularDiagonal */
+#define CSB_MARCH_RESIDUAL 8          /* NonPhysicalState raised by the residual */
+
+/* Build the march graph for these buffers (steady_solve's loop on the
+ * device: residual + norms, stop tests, ramped CFL x cfl_scale, the implicit
+ * step with device-side halving retries, cfl_scale recovery; one CUDA graph
+ * with conditional nodes, iterations alternating q -> q_alt -> q).  Runs one
+ * untimed warm-up step (q_alt scratch).  hist: device [rows][6] rows of
+ * (res_flow, res_species, res_density, CFL used, retries, stop code) for
+ * iterations 1..rows; cfl_tab: device [rows], Case.cfl_at(it) for
+ * it = 0..rows-1 (driver.py:71-75).  Resets the march state. */
+int csb_march_begin(csb_ctx* ctx, const csb_march_params* params, double* q, double* q_alt,
+                    double* hist, int rows, const double* cfl_tab, void* stream);
+/* Run iterations until iteration it_last is recorded or the march stops.
+ * plateau_at: iteration at which the monitor-plateau stop fires (0: none;
+ * decided by the host from the heat-flux samples, driver.py:300-306);
+ * clear_parity: the caller copied q_alt into q. */
+int csb_march_run(csb_ctx* ctx, int it_last, int plateau_at, int clear_parity, void* stream);
+/* Read the march state (synchronises): ints4 = (iterations recorded, stop
+ * code, parity [1: the latest state is in q_alt], retries of the last
+ * iteration); reals4 = (cfl_scale, last CFL tried, first density residual,
+ * CFL of the current iteration). */
+int csb_march_state(csb_ctx* ctx, int* ints4, double* reals4, void* stream);
+/* Release the march graph. */
+void csb_march_end(csb_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

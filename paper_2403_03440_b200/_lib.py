@@ -59,12 +59,23 @@ SIGNATURES = {
     "csb_dual_time_rhs": (_i, [_p, _ll, _dp, _dp, _dp, _dp, _dp, _d, _d, _dp, _p]),
     "csb_implicit_step_rhs": (_i, [_p, _dp, _dp, _d, _i, _i, _d, _d, _dp, _p]),
     "csb_sum_squares": (_i, [_p, _ll, _dp, _dp, _p]),
+    "csb_march_begin": (_i, [_p, _p, _dp, _dp, _dp, _i, _dp, _p]),
+    "csb_march_run": (_i, [_p, _i, _i, _i, _p]),
+    "csb_march_state": (_i, [_p, ctypes.POINTER(_i), ctypes.POINTER(_d), _p]),
+    "csb_march_end": (None, [_p]),
     "csb_fill_nodes": (_i, [_i, _i, _i, _i, _dp, _dp, _dp, _dp, _dp, _p]),
     "csb_grid_metrics": (_i, [_i, _i, _i, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _p]),
     "csb_primitive": (_i, [_p, _ll, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _p]),
     "csb_wall_heat_flux": (_i, [_p, _i, _dp, _dp, _dp, _dp, _p]),
     "csb_argmax_pick": (_i, [_ll, _dp, _dp, _dp, _p]),
 }
+
+class MarchParams(ctypes.Structure):
+    """csb_march_params (include/csflow_b200.h)."""
+
+    _fields_ = [("scheme", _i), ("offdiag_paper", _i), ("first_order", _i), ("max_retries", _i),
+                ("abs_floor", _d), ("drop_factor", _d)]
+
 
 _LIB = None
 

@@ -7,6 +7,7 @@
 #include "../../include/csflow_b200.h"
 #include "csb_common.cuh"
 #include "csb_kernels.cuh"
+#include "csb_march.cuh"
 
 using namespace csb;
 
@@ -50,6 +51,12 @@ struct csb_ctx {
   unsigned long long* flags = nullptr;
   OpDev op{};
   double *dtau = nullptr, *R = nullptr, *dq = nullptr, *partial = nullptr, *norms = nullptr;
+  double* cfl_dev = nullptr;  // the step's CFL on the device (kernels read it: graph-safe)
+  bool march_capture = false; // csb_march is capturing: cfl_dev is set by its controller
+  // device march (csb_march.cuh): one instantiated graph per buffer set
+  MarchState* march_st = nullptr;
+  cudaGraphExec_t march_exec = nullptr;
+  cudaGraph_t march_graph = nullptr;
   double* dom_scratch = nullptr;
   double* norm_partial = nullptr;
   double* fm_buf[2] = {nullptr, nullptr};  // static 2-D face metrics (workspace)
@@ -201,6 +208,7 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
     c->fm_buf[1] = k.take<double>((size_t)6 * c->g.NF[1]);
   }
   c->norms = k.take<double>(4);
+  c->cfl_dev = k.take<double>(1);
   // 2-D wavefront path buffers (csb_wave.cuh): strip-skewed planes
   c->wave_ok = false;
   if (c->g.nk == 1) {
@@ -223,6 +231,7 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
     c->wb.prog = k.take<int>(2);
     c->wb.rdy = k.take<int>((size_t)sk.nstrip * sk.T);
     c->wb.nonplanar = k.take<int>(1);
+    c->wb.epoch = k.take<int>(1);
     c->wb.nsI = 0;
     c->wave_ok = true;
   }
@@ -246,6 +255,7 @@ int zero_wave_records(csb_ctx* c, cudaStream_t st) {
   if (cudaMemsetAsync(w.rdy, 0, (size_t)w.sk.nstrip * w.sk.T * sizeof(int), st) != cudaSuccess)
     return 1;
   if (cudaMemsetAsync(w.nonplanar, 0, sizeof(int), st) != cudaSuccess) return 1;
+  if (cudaMemsetAsync(w.epoch, 0, sizeof(int), st) != cudaSuccess) return 1;
   return 0;
 }
 
@@ -299,6 +309,9 @@ void csb_destroy(csb_ctx* c) {
   if (c->d_sprx) cudaFree(c->d_sprx);
   if (c->d_fs) cudaFree(c->d_fs);
   if (c->wb.s2) cudaStreamDestroy(c->wb.s2);
+  if (c->march_exec) cudaGraphExecDestroy(c->march_exec);
+  if (c->march_graph) cudaGraphDestroy(c->march_graph);
+  if (c->march_st) cudaFree(c->march_st);
   if (c->wb.e1) cudaEventDestroy(c->wb.e1);
   if (c->wb.e2) cudaEventDestroy(c->wb.e2);
   delete c;
@@ -581,7 +594,7 @@ int csb_spectral_radii(csb_ctx* c, const double* q, double* lam_inv, double* lam
                        void* stream) {
   int r = ready(c);
   if (r) return r;
-  return cuda_check(c, launch_time_step(c->d_model, c->ns, c->g, q, 1.0, nullptr, nullptr, lam_inv,
+  return cuda_check(c, launch_time_step(c->d_model, c->ns, c->g, q, nullptr, nullptr, nullptr, lam_inv,
                                         lam_vis, c->flags, S(stream)),
                     "spectral radii");
 }
@@ -595,7 +608,7 @@ int csb_local_time_step(csb_ctx* c, long long N, const double* lam_inv, const do
                     "local_time_step");
 }
 
-static int time_step_impl(csb_ctx* c, const double* q, double cfl, const double* dOm_in,
+static int time_step_impl(csb_ctx* c, const double* q, const double* cfl, const double* dOm_in,
                           double* dtau, bool full_dom, cudaStream_t st) {
   const bool chem = mech_of(c).nrx > 0;
   const double* lamS = nullptr;
@@ -615,7 +628,9 @@ int csb_time_step(csb_ctx* c, const double* q, double cfl, const double* dOm_in,
                   void* stream) {
   int r = ready(c);
   if (r) return r;
-  return time_step_impl(c, q, cfl, dOm_in, dtau, c->ws_block, S(stream));
+  cudaError_t e = launch_set_double(c->cfl_dev, cfl, S(stream));
+  if (e != cudaSuccess) return cuda_check(c, e, "time step");
+  return time_step_impl(c, q, c->cfl_dev, dOm_in, dtau, c->ws_block, S(stream));
 }
 
 static int assemble_impl(csb_ctx* c, const double* q, const double* dtau, int scheme,
@@ -723,6 +738,26 @@ int csb_residual_norms(csb_ctx* c, long long N, const double* R, double* out3, v
 }
 
 // path: 0 auto, 1 generic (hyperplane sweeps), 2 2-D wavefront
+// Residual + grouped norms of one iteration (driver.py:85-90, 279): the
+// fused residual kernel, its device-side general-path fallback when the K2D
+// precondition fails (EB_KSKIP: w != 0 under symmetry k-faces; a no-op
+// launch otherwise), and the standalone norms when they could not be fused.
+static cudaError_t residual_norms_impl(csb_ctx* c, const double* q, double* R, int first_order,
+                                       double* norms3, cudaStream_t st) {
+  bool fused = false, fused2 = true;
+  const bool k2d = use_k2d(c);
+  const NormsOut nrm{c->norm_partial, c->npart_cap, c->norm_counter, norms3};
+  cudaError_t e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
+                                  k2d, c->flags, st, nrm, &fused);
+  if (e == cudaSuccess && k2d)
+    e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order, false,
+                        c->flags, st, fused ? nrm : NormsOut{nullptr, 0, nullptr, nullptr}, &fused2,
+                        c->flags);
+  if (e == cudaSuccess && (!fused || !fused2))
+    e = launch_norms(c->ns, c->g.N, R, c->partial, norms3, st);
+  return e;
+}
+
 // One implicit step.  rhs_is_R: `R` is the residual (rhs = -R, steady);
 // otherwise `R` is the right-hand side itself (dual time, csb_dual_time_rhs)
 // and theta, dt add (1 + theta) V / dt to the diagonal (implicit.py:346-348).
@@ -731,6 +766,10 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
                          int path = 0, double* dq_out = nullptr, cudaEvent_t* ev = nullptr,
                          double theta = 0.0, double dt = 0.0, bool rhs_is_R = true) {
   if (int r0 = ensure_face_metrics(c, st)) return r0;
+  if (!c->march_capture) {  // (in a captured march the controller kernel sets it)
+    cudaError_t e0 = launch_set_double(c->cfl_dev, cfl, st);
+    if (e0 != cudaSuccess) return cuda_check(c, e0, "implicit step");
+  }
   const bool chem = mech_of(c).nrx > 0;
   const bool full = chem && scheme == SCH_CI;
   const bool dual = dt > 0.0 && std::isfinite(dt);
@@ -770,9 +809,8 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
           cudaEventCreateWithFlags(&c->wb.e2, cudaEventDisableTiming) != cudaSuccess)
         e = cudaErrorUnknown;
     }
-    c->wb.epoch += 1;
     if (e == cudaSuccess)
-      e = launch_wave_step(c->d_model, c->ns, c->g, c->wb, q, R, cfl, lamS, domd, dstride,
+      e = launch_wave_step(c->d_model, c->ns, c->g, c->wb, q, R, c->cfl_dev, lamS, domd, dstride,
                            chem ? 1 : 0, scheme, offdiag_paper ? 1.0 : 0.5, q_new, dq_out, c->flags,
                            st, ev);
     if (e == cudaErrorInvalidConfiguration && path == 0) {
@@ -782,7 +820,7 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
       return cuda_check(c, e, "implicit step (wavefront)");
     }
   }
-  int r = time_step_impl(c, q, cfl, dOm_in, c->dtau, full, st);
+  int r = time_step_impl(c, q, c->cfl_dev, dOm_in, c->dtau, full, st);
   if (r) return r;
   OpDev& op = c->op;
   op.dom_full = full ? 1 : 0;
@@ -840,19 +878,7 @@ int csb_iteration(csb_ctx* c, const double* q, double cfl, int scheme, int offdi
   cudaStream_t st = S(stream);
   if ((r = ensure_face_metrics(c, st))) return r;
   double* R = R_out ? R_out : c->R;
-  bool fused = false, fused2 = true;
-  const bool k2d = use_k2d(c);
-  const NormsOut nrm{c->norm_partial, c->npart_cap, c->norm_counter, norms3 ? norms3 : c->norms};
-  cudaError_t e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
-                                  k2d, c->flags, st, nrm, &fused);
-  // device-side fallback to the general path when the K2D precondition
-  // failed (EB_KSKIP: w != 0 under symmetry k-faces); a no-op launch otherwise
-  if (e == cudaSuccess && k2d)
-    e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order, false,
-                        c->flags, st, fused ? nrm : NormsOut{nullptr, 0, nullptr, nullptr}, &fused2,
-                        c->flags);
-  if (e == cudaSuccess && (!fused || !fused2))
-    e = launch_norms(c->ns, c->g.N, R, c->partial, norms3 ? norms3 : c->norms, st);
+  cudaError_t e = residual_norms_impl(c, q, R, first_order, norms3 ? norms3 : c->norms, st);
   if (e != cudaSuccess) return cuda_check(c, e, "iteration residual");
   return implicit_impl(c, q, R, cfl, scheme, offdiag_paper, nullptr, q_new, st);
 }
@@ -959,6 +985,218 @@ int csb_argmax_pick(long long n, const double* key, const double* val, double* o
 int csb_fp64_peak(int iters, double* scratch, void* stream) {
   if (iters < 1 || !scratch) return CSB_E_BADARG;
   return launch_fp64_peak(iters, scratch, S(stream)) == cudaSuccess ? CSB_OK : CSB_E_CUDA;
+}
+
+// ------------------------------------------------------------ device march
+}  // extern "C"
+
+namespace {
+
+// A conditional handle on the graph the stream is capturing into.
+cudaError_t new_handle(cudaStream_t s, cudaGraphConditionalHandle* h) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  cudaError_t e = cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, nullptr, nullptr);
+  if (e != cudaSuccess) return e;
+  return cudaGraphConditionalHandleCreate(h, g, 0, cudaGraphCondAssignDefault);
+}
+
+// Appends a conditional node on handle h after the stream's current capture
+// dependencies and returns its body graph.
+cudaError_t add_cond_node(cudaStream_t s, cudaGraphConditionalHandle h,
+                          cudaGraphConditionalNodeType type, cudaGraph_t* body) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g;
+  const cudaGraphNode_t* deps;
+  size_t nd;
+  cudaError_t e = cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd);
+  if (e != cudaSuccess) return e;
+  cudaGraphNodeParams p{};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = type;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  if ((e = cudaGraphAddNode(&node, g, deps, nd, &p)) != cudaSuccess) return e;
+  *body = p.conditional.phGraph_out[0];
+  return cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
+}
+
+struct MarchBuild {
+  csb_ctx* c;
+  MarchCfg cfg;
+  int scheme, paper, first_order;
+  cudaStream_t lv[6];  // one capture stream per nesting level
+};
+
+cudaError_t begin_body(cudaStream_t s, cudaGraph_t body) {
+  return cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+}
+cudaError_t end_body(cudaStream_t s) {
+  cudaGraph_t g;
+  return cudaStreamEndCapture(s, &g);
+}
+
+// One pseudo-time iteration qin -> qout captured on nesting level L
+// (structure in csb_march.cuh).
+cudaError_t capture_iteration(MarchBuild& b, int L, const double* qin, double* qout) {
+  csb_ctx* c = b.c;
+  cudaStream_t s = b.lv[L], s1 = b.lv[L + 1], s2 = b.lv[L + 2];
+  cudaError_t e = residual_norms_impl(c, qin, c->R, b.first_order, c->norms, s);
+  cudaGraphConditionalHandle hstep, hretry;
+  cudaGraph_t gstep, gretry;
+  if (e == cudaSuccess) e = new_handle(s, &hstep);
+  if (e != cudaSuccess) return e;
+  k_march_pre<<<1, 1, 0, s>>>(b.cfg, hstep);
+  if ((e = add_cond_node(s, hstep, cudaGraphCondTypeIf, &gstep)) != cudaSuccess) return e;
+  // IF(step): retry loop, then the bookkeeping of the accepted step
+  if ((e = begin_body(s1, gstep)) != cudaSuccess) return e;
+  if ((e = new_handle(s1, &hretry)) == cudaSuccess) {
+    k_cond_set<<<1, 1, 0, s1>>>(hretry, 1u);
+    e = add_cond_node(s1, hretry, cudaGraphCondTypeWhile, &gretry);
+  }
+  if (e == cudaSuccess) e = begin_body(s2, gretry);
+  if (e == cudaSuccess) {
+    int r = implicit_impl(c, qin, c->R, 0.0, b.scheme, b.paper, nullptr, qout, s2);
+    if (r != CSB_OK) e = cudaErrorUnknown;
+    k_march_after<<<1, 1, 0, s2>>>(b.cfg, hretry);
+    cudaError_t e2 = end_body(s2);
+    if (e == cudaSuccess) e = e2;
+  }
+  if (e == cudaSuccess) k_march_post<<<1, 1, 0, s1>>>(b.cfg);
+  cudaError_t e1 = end_body(s1);
+  return e != cudaSuccess ? e : e1;
+}
+
+cudaError_t build_march(MarchBuild& b, const double* q, double* q_alt, cudaGraph_t* out) {
+  cudaStream_t s0 = b.lv[0], s1 = b.lv[1], s2 = b.lv[2];
+  cudaError_t e = cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return e;
+  cudaGraphConditionalHandle hloop, hb;
+  cudaGraph_t gloop, gb;
+  if ((e = new_handle(s0, &hloop)) == cudaSuccess) {
+    k_march_cond<<<1, 1, 0, s0>>>(b.cfg, hloop);
+    e = add_cond_node(s0, hloop, cudaGraphCondTypeWhile, &gloop);
+  }
+  if (e == cudaSuccess && (e = begin_body(s1, gloop)) == cudaSuccess) {
+    e = capture_iteration(b, 1, q, q_alt);  // iteration A (levels 1..3)
+    if (e == cudaSuccess && (e = new_handle(s1, &hb)) == cudaSuccess) {
+      k_march_cond<<<1, 1, 0, s1>>>(b.cfg, hb);
+      e = add_cond_node(s1, hb, cudaGraphCondTypeIf, &gb);
+    }
+    if (e == cudaSuccess && (e = begin_body(s2, gb)) == cudaSuccess) {
+      e = capture_iteration(b, 2, q_alt, const_cast<double*>(q));  // iteration B (levels 2..4)
+      cudaError_t e2 = end_body(s2);
+      if (e == cudaSuccess) e = e2;
+    }
+    if (e == cudaSuccess) k_march_cond<<<1, 1, 0, s1>>>(b.cfg, hloop);
+    cudaError_t e1 = end_body(s1);
+    if (e == cudaSuccess) e = e1;
+  }
+  cudaGraph_t g = nullptr;
+  cudaError_t e0 = cudaStreamEndCapture(s0, &g);
+  if (e == cudaSuccess) e = e0;
+  if (e != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    return e;
+  }
+  *out = g;
+  return cudaSuccess;
+}
+
+}  // namespace
+
+extern "C" {
+
+void csb_march_end(csb_ctx* c) {
+  if (!c) return;
+  if (c->march_exec) cudaGraphExecDestroy(c->march_exec);
+  if (c->march_graph) cudaGraphDestroy(c->march_graph);
+  c->march_exec = nullptr;
+  c->march_graph = nullptr;
+}
+
+int csb_march_begin(csb_ctx* c, const csb_march_params* p, double* q, double* q_alt, double* hist,
+                    int rows, const double* cfl_tab, void* stream) {
+  int r = ready(c);
+  if (r) return r;
+  if (!p || !q || !q_alt || !hist || rows < 1 || !cfl_tab) return CSB_E_BADARG;
+  if (p->scheme < 0 || p->scheme > 2) return fail(c, CSB_E_BADARG, "march: unknown scheme");
+  if ((r = check_bcs(c))) return r;
+  if ((r = sync_fs(c))) return r;
+  cudaStream_t st = S(stream);
+  if ((r = ensure_face_metrics(c, st))) return r;
+  csb_march_end(c);
+  if (!c->march_st && cudaMalloc(&c->march_st, sizeof(MarchState)) != cudaSuccess)
+    return fail(c, CSB_E_CUDA, "cudaMalloc(march state)");
+  // warm-up step outside the capture: lazily created streams, record
+  // layouts and padding zeros are in place before the graph is built
+  cudaError_t e = residual_norms_impl(c, q, c->R, p->first_order, c->norms, st);
+  if (e != cudaSuccess) return cuda_check(c, e, "march warm-up");
+  if ((r = implicit_impl(c, q, c->R, 1.0, p->scheme, p->offdiag_paper, nullptr, q_alt, st)))
+    return r;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_check(c, e, "march warm-up");
+  MarchBuild b{};
+  b.c = c;
+  b.scheme = p->scheme;
+  b.paper = p->offdiag_paper;
+  b.first_order = p->first_order;
+  b.cfg.st = c->march_st;
+  b.cfg.hist = hist;
+  b.cfg.rows = rows;
+  b.cfg.cfl_tab = cfl_tab;
+  b.cfg.norms = c->norms;
+  b.cfg.cfl_dev = c->cfl_dev;
+  b.cfg.flags = c->flags;
+  b.cfg.abs_floor = p->abs_floor;
+  b.cfg.drop_factor = p->drop_factor;
+  b.cfg.max_retries = p->max_retries;
+  for (auto& x : b.lv)
+    if (cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(c, CSB_E_CUDA, "march: stream");
+  c->march_capture = true;
+  c->wb.serial = 1;
+  cudaGraph_t g = nullptr;
+  e = build_march(b, q, q_alt, &g);
+  c->march_capture = false;
+  c->wb.serial = 0;
+  for (auto& x : b.lv) cudaStreamDestroy(x);
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&c->march_exec, g, 0);
+  if (e != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return cuda_check(c, e, "march graph");
+  }
+  c->march_graph = g;
+  k_march_init<<<1, 1, 0, st>>>(c->march_st);
+  if ((r = reset_flags(c, st))) return r;
+  return cuda_check(c, cudaGetLastError(), "march init");
+}
+
+int csb_march_run(csb_ctx* c, int it_last, int plateau_at, int clear_parity, void* stream) {
+  if (!c || !c->march_exec) return c ? fail(c, CSB_E_STATE, "march: csb_march_begin first") : CSB_E_BADARG;
+  cudaStream_t st = S(stream);
+  k_march_chunk<<<1, 1, 0, st>>>(c->march_st, it_last, plateau_at, clear_parity);
+  note_launches(1);
+  return cuda_check(c, cudaGraphLaunch(c->march_exec, st), "march chunk");
+}
+
+int csb_march_state(csb_ctx* c, int* ints4, double* reals4, void* stream) {
+  if (!c || !c->march_st || !ints4 || !reals4) return CSB_E_BADARG;
+  MarchState h;
+  cudaStream_t st = S(stream);
+  cudaError_t e = cudaMemcpyAsync(&h, c->march_st, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_check(c, e, "march state");
+  ints4[0] = h.it;
+  ints4[1] = h.stop;
+  ints4[2] = h.parity;
+  ints4[3] = h.attempt;
+  reals4[0] = h.cfl_scale;
+  reals4[1] = h.cfl_try;
+  reals4[2] = h.res0;
+  reals4[3] = h.cfl_now;
+  return CSB_OK;
 }
 
 }  // extern "C"

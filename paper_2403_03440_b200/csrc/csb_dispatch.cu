@@ -23,7 +23,7 @@ unsigned long long launch_count() { return g_launches.load(std::memory_order_rel
                                           unsigned long long*, cudaStream_t);                      \
   cudaError_t launch_production_b##b(const Model*, int, const GridDev&, const Mech&,               \
                                      const double*, double*, unsigned long long*, cudaStream_t);   \
-  cudaError_t launch_time_step_b##b(const Model*, int, const GridDev&, const double*, double,      \
+  cudaError_t launch_time_step_b##b(const Model*, int, const GridDev&, const double*, const double*,\
                                     const double*, double*, double*, double*,                      \
                                     unsigned long long*, cudaStream_t);                            \
   cudaError_t launch_assemble_cell_b##b(const Model*, int, const GridDev&, const double*,          \
@@ -36,7 +36,7 @@ unsigned long long launch_count() { return g_launches.load(std::memory_order_rel
   cudaError_t launch_export_op_b##b(const Model*, int, const GridDev&, const OpDev&,               \
                                     const double*, int, double*, cudaStream_t);                    \
   cudaError_t launch_wave_step_b##b(const Model*, int, const GridDev&, const WaveBufs&,            \
-                                    const double*, const double*, double, const double*,           \
+                                    const double*, const double*, const double*, const double*,    \
                                     const double*, int, int, int, double, double*, double*,        \
                                     unsigned long long*, cudaStream_t, cudaEvent_t*);
 CSB_BUCKET_LIST(CSB_DECL)
@@ -90,7 +90,7 @@ cudaError_t launch_production(const Model* mp, int ns, const GridDev& g, const M
   note_launches(1);
   CSB_ROUTE(launch_production, mp, ns, g, mech, q, om, flags, st)
 }
-cudaError_t launch_time_step(const Model* mp, int ns, const GridDev& g, const double* q, double cfl,
+cudaError_t launch_time_step(const Model* mp, int ns, const GridDev& g, const double* q, const double* cfl,
                              const double* lamS, double* dtau, double* lam_inv, double* lam_vis,
                              unsigned long long* flags, cudaStream_t st) {
   note_launches(1);
@@ -120,7 +120,7 @@ cudaError_t launch_export_op(const Model* mdl, int ns, const GridDev& g, const O
 }
 
 cudaError_t launch_wave_step(const Model* mp, int ns, const GridDev& g, const WaveBufs& wb,
-                             const double* q, const double* R, double cfl, const double* lamS,
+                             const double* q, const double* R, const double* cfl, const double* lamS,
                              const double* domd, int dom_stride, int per_species, int scheme,
                              double sp_scale, double* qn, double* dq_std,
                              unsigned long long* flags, cudaStream_t st, cudaEvent_t* ev) {

@@ -181,7 +181,7 @@ CSB_DEV void cell_metric(const GridDev& g, int d, int i, int j, int k, double Sc
 
 template <int NSB>
 __global__ void k_time_step(const Model* __restrict__ mp, GridDev g, const double* __restrict__ q,
-                            double cfl, const double* __restrict__ lamS, double* __restrict__ dtau,
+                            const double* __restrict__ cfl_p, const double* __restrict__ lamS, double* __restrict__ dtau,
                             double* __restrict__ lam_inv, double* __restrict__ lam_vis,
                             unsigned long long* flags) {
   const Model& m = *mp;
@@ -209,7 +209,7 @@ __global__ void k_time_step(const Model* __restrict__ mp, GridDev g, const doubl
     const double den = J * (((li[0] + li[1]) + li[2]) + ((lv[0] + lv[1]) + lv[2])) +
                        (lamS ? lamS[c] : 0.0);
     if (!(den > 0.0)) raise_flag(flags, EB_ZERO_WAVE, c);
-    if (dtau) dtau[c] = cfl / den;
+    if (dtau) dtau[c] = *cfl_p / den;
   }
 }
 
@@ -312,7 +312,7 @@ cudaError_t CSB_BK(launch_production)(const Model* mp, int ns, const GridDev& g,
   return cudaGetLastError();
 }
 
-cudaError_t CSB_BK(launch_time_step)(const Model* mp, int ns, const GridDev& g, const double* q, double cfl,
+cudaError_t CSB_BK(launch_time_step)(const Model* mp, int ns, const GridDev& g, const double* q, const double* cfl,
                              const double* lamS, double* dtau, double* lam_inv, double* lam_vis,
                              unsigned long long* flags, cudaStream_t st) {
   CSB_NS_DISPATCH(ns, {

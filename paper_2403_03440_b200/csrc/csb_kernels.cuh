@@ -64,13 +64,15 @@ struct WaveBufs {
   // for the tiles of each ring slot (csb_wave.cuh)
   int* rdy;       // [nstrip][T] (tiles of >= 1 step)
   int* nonplanar; // == epoch when the step is not planar (csb_wave.cuh k_hand_reset)
-  int epoch;      // this launch's tag (incremented per implicit step)
+  int* epoch;     // device: this step's tag, bumped on the device at the start of every
+                  // wavefront step (graph replays see a fresh tag each time)
   cudaStream_t s2;
   cudaEvent_t e1, e2;
+  int serial;     // no records / forward-sweep overlap (graph capture: single stream)
 };
 
 cudaError_t launch_wave_step(const Model* mp, int ns, const GridDev& g, const WaveBufs& wb,
-                             const double* q, const double* R, double cfl, const double* lamS,
+                             const double* q, const double* R, const double* cfl, const double* lamS,
                              const double* domd, int dom_stride, int per_species, int scheme,
                              double sp_scale, double* qn, double* dq_std,
                              unsigned long long* flags, cudaStream_t st,
@@ -103,7 +105,7 @@ cudaError_t launch_source_jacobian(const Model* mp, int ns, const GridDev& g, co
 cudaError_t launch_production(const Model* mp, int ns, const GridDev& g, const Mech& mech,
                               const double* q, double* om, unsigned long long* flags,
                               cudaStream_t st);
-cudaError_t launch_time_step(const Model* mp, int ns, const GridDev& g, const double* q, double cfl,
+cudaError_t launch_time_step(const Model* mp, int ns, const GridDev& g, const double* q, const double* cfl,
                              const double* lamS, double* dtau, double* lam_inv, double* lam_vis,
                              unsigned long long* flags, cudaStream_t st);
 cudaError_t launch_assemble(const Model* mp, int ns, const GridDev& g, const double* q,
@@ -143,6 +145,7 @@ cudaError_t launch_dtau_arrays(long long N, const double* li, const double* lv, 
 cudaError_t launch_check_2d(const GridDev& g, int* ok, cudaStream_t st);
 cudaError_t launch_face_metrics2d(const GridDev& g, double* fm0, double* fm1, cudaStream_t st);
 cudaError_t launch_cell_metrics(const GridDev& g, double* cm, cudaStream_t st);
+cudaError_t launch_set_double(double* dst, double v, cudaStream_t st);
 void note_launches(unsigned long long n);
 unsigned long long launch_count();
 

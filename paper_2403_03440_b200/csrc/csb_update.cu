@@ -154,6 +154,14 @@ cudaError_t launch_norms(int ns, long long N, const double* R, double* partial, 
   return cudaGetLastError();
 }
 
+__global__ void k_set_double(double* dst, double v) { *dst = v; }
+
+cudaError_t launch_set_double(double* dst, double v, cudaStream_t st) {
+  note_launches(1);
+  k_set_double<<<1, 1, 0, st>>>(dst, v);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_dual_rhs(long long N, int nv, const double* R, const double* qm,
                             const double* qn, const double* qnm1, const double* vol, double theta,
                             double dt, double* out, cudaStream_t st) {

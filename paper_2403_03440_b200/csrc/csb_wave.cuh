@@ -161,12 +161,15 @@ CSB_DEV long long gaddr(const Skew& k, int NG, int s, int t, int p, int r) {
   return (((long long)s * k.T + t) * NG + p) * 32 + r;
 }
 
+static __global__ void k_epoch_bump(int* e) { *e += 1; }
+
 // ============================================================== hand-off reset
 // Both sweeps' strip hand-off rows: signalling-NaN sentinel in the data rows,
 // zero in the HPAD pad rows (one thread per row).
 static __global__ void k_hand_reset(double* __restrict__ hand, int nstrip, int T, int nhf, int nhs,
                                     long long N, const double* __restrict__ q3,
-                                    const double* __restrict__ R3, int* flag, int epoch) {
+                                    const double* __restrict__ R3, int* flag, const int* epoch_p) {
+  const int epoch = *epoch_p;
   // planarity of the step (chain_flow PL): epoch stored when any cell has a
   // nonzero (or non-finite) z-momentum q3 or z-momentum residual R3
   {
@@ -201,7 +204,7 @@ CSB_DEV void publish_tile(const WaveBufs& wb, int s, int ib) {
   __syncthreads();
   if (threadIdx.x == 0) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(wb.rdy + (long long)s * wb.sk.T + ib),
-                 "r"(wb.epoch)
+                 "r"(*wb.epoch)
                  : "memory");
   }
 }
@@ -223,7 +226,7 @@ template <int NSB, bool CI>
 // registers removes the spills: ns = 11 records 493 -> 400 us at 1024^2)
 __global__ void __launch_bounds__(256, NSB <= 8 ? 4 : 3) k_records2d(const Model* __restrict__ mp, GridDev g, Skew sk,
                                                    const double* __restrict__ q,
-                                                   const double* __restrict__ R, double cfl,
+                                                   const double* __restrict__ R, const double* __restrict__ cfl_p,
                                                    const double* __restrict__ lamS,
                                                    const double* __restrict__ domd, int dom_stride,
                                                    int per_species, double sp_scale, WaveBufs wb,
@@ -309,7 +312,7 @@ __global__ void __launch_bounds__(256, NSB <= 8 ? 4 : 3) k_records2d(const Model
     const double den = J * (((li[0] + li[1]) + li[2]) + ((lv[0] + lv[1]) + lv[2])) +
                        (lamS ? lamS[c] : 0.0);
     if (!(den > 0.0)) raise_flag(flags, EB_ZERO_WAVE, c);
-    const double dtau = cfl / den;
+    const double dtau = *cfl_p / den;
     const double base = V / dtau;
     if constexpr (CI) {
       // CI: one scalar diagonal with the unified radius (implicit.py:362-373)
@@ -526,7 +529,8 @@ struct WaveArgs {
   int fake_recv;     // probe: strips without upstream still get a receiver arrival per slot
   const int* rdy;    // forward sweep overlapped with the records kernel: tile flags (or null)
   const int* nonplanar;  // == epoch: some cell has z-momentum or its residual != 0 (or null)
-  int epoch, rC;     // their launch tag and the records tile length (steps)
+  const int* epoch;  // the step's tag (device)
+  int rC;            // records tile length (steps)
   unsigned long long* dbg;  // timing probe: [CTA][4] globaltimer stamps (or null)
   WaveRole role[2];  // 0 flow, 1 species
 };
@@ -995,6 +999,7 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
   if (warp == nchain) {
     // ---------------------------------------------------- producer (TMA)
     if (lane == 0) {
+      const int ep = a.rdy ? *a.epoch : 0;
       int buf = 0, phase = 0;
       for (int ks = 0; ks < x.nslots; ++ks) {
         const int k = BWD ? x.nslots - 1 - ks : ks;
@@ -1005,7 +1010,7 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
           // (async proxy) after the acquire
           const int* f = a.rdy + (long long)s * T;
           for (int b = (k * WK) / a.rC; b <= (k * WK + WK - 1) / a.rC; ++b)
-            while (ld_acquire(f + b) != a.epoch) __nanosleep(64);
+            while (ld_acquire(f + b) != ep) __nanosleep(64);
           asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         const unsigned bytes = (unsigned)(slot * 8);
@@ -1052,7 +1057,7 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
     const double* src = ro.hand + ((long long)up * (T + 2 * HPAD) + HPAD) * nh;
     const int nw = WK * nh;  // words per slot (<= 256)
     // planar step: the flow chains neither send nor read hand-off word 3
-    const bool skip3 = BWD && kind == 0 && a.nonplanar && ld_relaxed(a.nonplanar) != a.epoch;
+    const bool skip3 = BWD && kind == 0 && a.nonplanar && ld_relaxed(a.nonplanar) != *a.epoch;
     // Windows of Q consecutive slots (Q x WK >= 8 steps, <= 512 words): the
     // window's hand-off rows are contiguous both in the L2 buffer and in the
     // hin ring, so one poll round trip covers all of them.  (Measured: with one
@@ -1170,7 +1175,7 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
     // (backward sweep only -- measured: the planar forward chain is faster on
     // one strip, 147 -> 130 ns per step, but its multi-strip pipeline is
     // slower, 512^2 199 -> 216 us; the planar backward sweep gains 207 -> 200)
-    if (BWD && a.nonplanar && ld_relaxed(a.nonplanar) != a.epoch) chain_flow<BWD, true>(x, ro);
+    if (BWD && a.nonplanar && ld_relaxed(a.nonplanar) != *a.epoch) chain_flow<BWD, true>(x, ro);
     else chain_flow<BWD, false>(x, ro);
   } else if (kind == 1) {
     chain_species<NSB, BWD, PER>(x, ro, warp);
@@ -1351,7 +1356,7 @@ inline int wave_depth(int WK, int NG, int nh) {
 // only for its own records tiles (WaveBufs::rdy).  CSB_NO_OVERLAP=1 restores
 // the serial order.
 cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, const WaveBufs& wb,
-                                     const double* q, const double* R, double cfl,
+                                     const double* q, const double* R, const double* cfl,
                                      const double* lamS, const double* domd, int dom_stride,
                                      int per_species, int scheme, double sp_scale, double* qn,
                                      double* dq_std, unsigned long long* flags, cudaStream_t st,
@@ -1484,7 +1489,8 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       return cudaGetLastError();
     };
     // ---------------- the step
-    note_launches(1);
+    note_launches(2);
+    k_epoch_bump<<<1, 1, 0, st>>>(wb.epoch);  // fresh tag for this step (graph replays too)
     k_hand_reset<<<grid_for(std::max(4LL * sk.nstrip * hrows, g.N), 256), 256, 0, st>>>(
         wb.hand, sk.nstrip, sk.T, ci ? NV : 5, ci ? 0 : NSB, g.N, q + 3 * g.N, R + 3 * g.N,
         wb.nonplanar, wb.epoch);
@@ -1499,7 +1505,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     // (the threshold counts 2 CTAs per strip for CI too, as measured)
     const int sms = device_sms();
     const int nsweep = ci ? sk.nstrip : 2 * sk.nstrip;
-    const bool overlap = !ev && wb.s2 && only == -1 &&
+    const bool overlap = !ev && wb.s2 && !wb.serial && only == -1 &&
                          (2 * sk.nstrip <= sms * 48 / 148 ||
                           (getenv("CSB_FORCE_OVERLAP") && nsweep <= sms - 8)) &&
                          !getenv("CSB_NO_OVERLAP");

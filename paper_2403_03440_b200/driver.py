@@ -387,8 +387,127 @@ def _reference_density_residual(case) -> float:
     return float(inf.rho) * speed * max(areas) * np.sqrt(case.grid.ncells)
 
 
-def steady_solve(case, q0=None, *, return_device=False):
-    """March to steady state; returns (q, ConvergenceHistory) (driver.py:266-317)."""
+def steady_solve(case, q0=None, *, return_device=False, device_march=True):
+    """March to steady state; returns (q, ConvergenceHistory) (driver.py:266-317).
+
+    The loop runs on the device (csb_march_*): one CUDA graph per chunk of
+    iterations takes every decision of the reference's loop -- residual
+    norms, NaN check, absolute-floor / residual-drop / monitor-plateau stops,
+    the ramped CFL times cfl_scale, the CFL-halving retries of each implicit
+    step and the x1.2 recovery -- so the host reads the history once per
+    chunk.  Chunks end where the stagnation heat-flux monitor samples the
+    state (every ``monitor_every`` iterations and at iteration 1), which the
+    host evaluates on the device between chunks and turns into the plateau
+    decision.  ``device_march=False`` runs the host-driven loop."""
+    if not device_march:
+        return _steady_solve_host(case, q0, return_device=return_device)
+    from ._lib import MarchParams
+    st = _Stepper(case)
+    eng = st.eng
+    torch = eng.torch
+    nv, N = eng.nv, eng.N
+    q_init = case.initial_field() if q0 is None else q0
+    q = eng.to_soa(q_init, nv).clone()
+    q_alt = eng.empty(nv, N)
+    rows = max(int(case.max_iters), 1)
+    hist_dev = eng.zeros(rows, 6)
+    cfl_tab = torch.tensor([case.cfl_at(i) for i in range(rows)], dtype=torch.float64,
+                           device=eng.device)
+    orders = case.residual_drop_orders
+    params = MarchParams(st.scheme, st.paper, int(bool(case.first_order)), MAX_STEP_RETRIES,
+                         1e-12 * _reference_density_residual(case) if case.stop_on_absolute_floor
+                         else -1.0,
+                         10.0 ** (-orders) if np.isfinite(orders) else -1.0)
+    stream = ctypes.c_void_p(eng.stream)
+    eng._chk(eng.lib.csb_march_begin(eng.ctx, ctypes.byref(params), q.data_ptr(),
+                                     q_alt.data_ptr(), hist_dev.data_ptr(), rows,
+                                     cfl_tab.data_ptr(), stream), "steady_solve")
+    hist = ConvergenceHistory(metadata={
+        "scheme": case.scheme, "cfl": case.cfl, "cfl_ramp": case.cfl_ramp,
+        "monitor_every": case.monitor_every, "monitor_window": case.monitor_window,
+        "device_march": True,
+    })
+    walls = bool(_wall_faces(case.bcs))
+    geom = _WallGeom(eng, case.grid, case.bcs) if walls else None
+    monitoring = case.monitor_rel_change is not None or walls
+    every = max(int(case.monitor_every), 1)
+    samples, sample_at = [], {}
+    ints = (ctypes.c_int * 4)()
+    reals = (ctypes.c_double * 4)()
+    done, clear = 0, 0
+    try:
+        while done < case.max_iters:
+            it_next = done + 1
+            plateau_at = 0
+            if monitoring and (it_next % every == 0 or it_next == 1):
+                sample = _stagnation_monitor_device(eng, q, geom) if walls else float("nan")
+                samples.append(sample)
+                sample_at[it_next] = sample
+                if case.monitor_rel_change is not None and len(samples) >= case.monitor_window:
+                    w = np.array(samples[-case.monitor_window:])
+                    if np.all(np.isfinite(w)) and np.max(np.abs(w - w[-1])) \
+                            <= case.monitor_rel_change * max(abs(w[-1]), 1e-300):
+                        plateau_at = it_next
+            it_last = (it_next // every + 1) * every - 1 if monitoring else case.max_iters
+            it_last = min(max(it_last, it_next), case.max_iters)
+            t0 = time.perf_counter()
+            eng._chk(eng.lib.csb_march_run(eng.ctx, it_last, plateau_at, clear, stream),
+                     "steady_solve")
+            eng._chk(eng.lib.csb_march_state(eng.ctx, ints, reals, stream), "steady_solve")
+            wall = time.perf_counter() - t0
+            it_now, stop, parity = ints[0], ints[1], ints[2]
+            if it_now > done:
+                rows_new = hist_dev[done:it_now].cpu().numpy()
+                per = wall / (it_now - done)
+                for k, row in enumerate(rows_new):
+                    it = done + 1 + k
+                    hist.record(it, GroupedResidual(float(row[0]), float(row[1]), float(row[2])),
+                                sample_at.get(it, float("nan")), per,
+                                per if row[5] == 0 else 0.0, float(row[3]), int(row[4]))
+            done = it_now
+            clear = 0
+            if parity:
+                q.copy_(q_alt)
+                clear = 1
+            if stop:
+                _march_stop(eng, stop, done, reals, hist)
+                break
+        else:
+            hist.reason = "max_iters"
+    finally:
+        eng.lib.csb_march_end(eng.ctx)
+    if return_device:
+        return SoA(q, eng.dims), hist
+    like = q0 if (q0 is not None and is_torch(q0)) else np.empty(0)
+    return eng.from_soa(q, like, tuple(eng.dims) + (eng.nv,)), hist
+
+
+_MARCH_REASONS = {1: "converged_absolute", 2: "converged_residual_drop",
+                  3: "converged_monitor_plateau"}
+
+
+def _march_stop(eng, stop, done, reals, hist):
+    """Map a device stop code onto the reference's outcome (driver.py:266-317)."""
+    if stop in _MARCH_REASONS:
+        hist.reason = _MARCH_REASONS[stop]
+        return
+    if stop == 4:
+        raise Diverged(f"non-finite residual norm at iteration {done + 1}")
+    if stop == 5:
+        raise Diverged(f"step failed after {MAX_STEP_RETRIES} CFL halvings (CFL={reals[1]:g})")
+    flags, cell, _ = eng.status()
+    flags &= ~F_KSKIP
+    if stop == 8:
+        eng.raise_for(flags, cell, "assemble_residual", order=("decode",))
+        raise NonPhysicalState("assemble_residual: non-physical state")
+    eng.raise_for(flags, cell, "_implicit_step", order=("zero", "singular"))
+    raise Diverged(f"march stopped (code {stop})")
+
+
+def _steady_solve_host(case, q0=None, *, return_device=False):
+    """steady_solve with the loop on the host: one residual + norms read and
+    one fused implicit step (+ flag read) per iteration.  Kept as the A/B
+    reference of the device march."""
     st = _Stepper(case)
     eng = st.eng
     q_init = case.initial_field() if q0 is None else q0
