@@ -200,6 +200,7 @@ static __global__ void k_hand_reset(double* __restrict__ hand, int nstrip, int T
 
 // records tile (strip s, step block ib) stored: publish the launch epoch
 CSB_DEV void publish_tile(const WaveBufs& wb, int s, int ib) {
+  if (!wb.rdy) return;  // serial order: no concurrent forward sweep reads the flags
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1325,6 +1326,139 @@ __global__ void __launch_bounds__(256, NSB <= 8 ? 3 : 2) k_epilogue2d(const Mode
   }
 }
 
+// Large species counts (NSB > 24): the same closure + gate with the species
+// streamed instead of held in three register arrays of 5 + NSB doubles (which
+// capped the kernel at 2 CTAs per SM with spills): every species pass
+// recomputes o_s from q (L1) and dq (shared memory) with pinned rounding
+// (__d*_rn), so every pass sees the value that was stored.
+template <int NSB>
+CSB_DEV double closure_species(int scheme, double qs, double ds, double tot, double defect,
+                               double rnew, double rawsum) {
+  if (scheme == SCH_CS1)  // rho_s + drho_s + (rho_s / sum rho_s)(drho - sum drho_s)
+    return __dadd_rn(__dadd_rn(qs, ds), __dmul_rn(__ddiv_rn(qs, tot), defect));
+  if (scheme == SCH_CS2)  // (sum rho_s + drho)(rho_s + drho_s) / sum(rho_s + drho_s)
+    return __ddiv_rn(__dmul_rn(rnew, __dadd_rn(qs, ds)), rawsum);
+  return __dadd_rn(qs, ds);  // CI (the last species is reconstructed)
+}
+
+#ifndef CSB_EPI_MINB
+#define CSB_EPI_MINB 4
+#endif
+template <int NSB>
+__global__ void __launch_bounds__(256, CSB_EPI_MINB) k_epilogue2d_s(const Model* __restrict__ mp, GridDev g,
+                                                      Skew sk, int scheme,
+                                                      const double* __restrict__ q,
+                                                      const double* __restrict__ fw,
+                                                      const double* __restrict__ sw,
+                                                      double* __restrict__ qn,
+                                                      double* __restrict__ dq_std, int C,
+                                                      unsigned long long* flags) {
+  extern __shared__ double es[];
+  const Model& m = *mp;
+  const int ns = m.ns, nv = 5 + ns;
+  const int ncb = sk.T / C;
+  const int s = blockIdx.x / ncb, ib = blockIdx.x % ncb;
+  const int t0 = ib * C, j0 = s * 32;
+  const int CT = C * 32;
+  const long long N = g.N;
+  for (int e = threadIdx.x; e < CT; e += blockDim.x) {
+    const int tt = e / 32, r = e % 32;
+    const int t = t0 + tt;
+    const int i = t - r;
+    if (i < 0 || i >= g.ni || j0 + r >= g.nj) continue;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) es[k * CT + e] = fw[gaddr(sk, 5, s, t, k, r)];
+    for (int k = 0; k < ns; ++k) es[(5 + k) * CT + e] = sw[gaddr(sk, NSB, s, t, k, r)];
+  }
+  __syncthreads();
+  unsigned long long bad_count = 0, first1 = ~0ull, first2 = ~0ull;
+  for (int l = threadIdx.x; l < (C + 31) * C; l += blockDim.x) {
+    const int ip = -31 + l / C;
+    const int r = max(0, -ip) + l % C;
+    if (r > min(31, C - 1 - ip)) continue;
+    const int e = (ip + r) * 32 + r;
+    const int i = t0 + ip, j = j0 + r;
+    if (i < 0 || i >= g.ni || j >= g.nj) continue;
+    const long long c = (long long)i * g.nj + j;
+    const double* qc = q + c;
+    double* qo = qn + c;
+    const double* dd = es + e;
+    if (dq_std)
+      for (int k = 0; k < nv; ++k) dq_std[(long long)k * N + c] = dd[k * CT];
+    double o[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      o[k] = qc[k * N] + dd[k * CT];
+      qo[k * N] = o[k];
+    }
+    // pass 1: species sums
+    double tot = 0.0, dsum = 0.0, rawsum = 0.0, tail = 0.0;
+    for (int sp = 0; sp < ns; ++sp) {
+      const double qs = qc[(5 + sp) * N], ds = dd[(5 + sp) * CT];
+      tot += qs;
+      dsum += ds;
+      rawsum += qs + ds;
+      if (sp < ns - 1) tail += __dadd_rn(qs, ds);
+    }
+    const double defect = dd[0] - dsum, rnew = tot + dd[0];
+    const double lastv = o[0] - tail;
+    auto o_s = [&](int sp) {
+      if (scheme == SCH_CI && sp == ns - 1) return lastv;
+      return closure_species<NSB>(scheme, qc[(5 + sp) * N], dd[(5 + sp) * CT], tot, defect, rnew,
+                                  rawsum);
+    };
+    // pass 2: store
+    double osum = 0.0;
+    for (int sp = 0; sp < ns; ++sp) {
+      const double v = o_s(sp);
+      qo[(5 + sp) * N] = v;
+      osum += v;
+    }
+    bool ok1 = scheme == SCH_CI ? !(lastv < -1e-10 * o[0]) : !(osum <= 0.0);
+    // pass 3: gate (CS) and the clipped mass fractions of the decode
+    const double rho = o[0];
+    bool ok2 = (rho > 0.0) && finite(rho);
+    const double ir = 1.0 / rho;
+    double ysum = 0.0;
+    for (int sp = 0; sp < ns; ++sp) {
+      const double v = o_s(sp);
+      if (scheme != SCH_CI && v < -EPS_NEG * osum) ok1 = false;
+      double y = v * ir;
+      if (y < -EPS_NEG) ok2 = false;
+      if (y < 0.0) y = 0.0;
+      ysum += y;
+    }
+    // pass 4: renormalised mixture sums and temperature (decode_from)
+    const double isum = 1.0 / ysum;
+    double R = 0.0, cp = 0.0, yb = 0.0;
+    for (int sp = 0; sp < ns; ++sp) {
+      double y = o_s(sp) * ir;
+      if (y < 0.0) y = 0.0;
+      y = y * isum;
+      R += y * m.Rs[sp];
+      cp += y * m.cp[sp];
+      yb += y * m.bs[sp];
+    }
+    const double u0 = o[1] * ir, u1 = o[2] * ir, u2 = o[3] * ir;
+    const double Ek = 0.5 * ((u0 * u0 + u1 * u1) + u2 * u2);
+    const double T = ((o[4] * ir - Ek) - yb) * (1.0 / (cp - R));
+    if (!(T > 0.0) || !finite(T)) ok2 = false;
+    if (!ok1 && first1 == ~0ull) first1 = (unsigned long long)c;
+    if (!ok2 && first2 == ~0ull) first2 = (unsigned long long)c;
+    if (!(ok1 && ok2)) ++bad_count;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    bad_count += __shfl_xor_sync(0xffffffffu, bad_count, o);
+    first1 = min(first1, __shfl_xor_sync(0xffffffffu, first1, o));
+    first2 = min(first2, __shfl_xor_sync(0xffffffffu, first2, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (bad_count) atomicAdd(flags + FLAG_GATE_COUNT, bad_count);
+    if (first1 != ~0ull) raise_flag(flags, EB_GATE, (long long)first1);
+    if (first2 != ~0ull) raise_flag(flags, EB_GATE_DECODE, (long long)first2);
+  }
+}
+
 // ============================================================== launcher
 // epilogue tile length: the dq tile of (5 + ns) planes stays <= 48 KB so that
 // large species counts keep 4 CTAs per SM
@@ -1396,9 +1530,11 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     auto krec = ci ? k_records2d<NSB, true> : k_records2d<NSB, false>;
     cudaFuncSetAttribute(krec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
     const int nrec = sk.nstrip * (sk.T / C);
-    auto launch_records = [&](cudaStream_t s) {
+    auto launch_records = [&](cudaStream_t s, bool publish) {
+      WaveBufs wr = wb;
+      if (!publish) wr.rdy = nullptr;  // (no per-tile fence when nothing consumes the flags)
       krec<<<nrec, 256, rsm, s>>>(mp, g, sk, q, R, cfl, lamS, domd, dom_stride, ci ? 0 : per_species,
-                                  sp_scale, wb, C, flags);
+                                  sp_scale, wr, C, flags);
     };
     // ---------------- one sweep
     int only = -1;
@@ -1516,7 +1652,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       // cannot deadlock even where kernels are serialised (ncu replay,
       // CUDA_LAUNCH_BLOCKING) -- it then simply runs in the serial order
       cudaEventRecord(wb.e1, st);
-      launch_records(st);
+      launch_records(st, true);
       cudaStreamWaitEvent(wb.s2, wb.e1, 0);
       e = launch_pass(false, wb.s2, wb.rdy);
       if (e != cudaSuccess) return e;
@@ -1524,7 +1660,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       cudaStreamWaitEvent(st, wb.e2, 0);
     } else {
       if (ev) cudaEventRecord(ev[0], st);
-      launch_records(st);
+      launch_records(st, false);
       if (ev) cudaEventRecord(ev[1], st);
       e = launch_pass(false, st, nullptr);
       if (e != cudaSuccess) return e;
@@ -1536,9 +1672,12 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     // ---------------- epilogue
     const int CE = epilogue_steps(ns);
     const size_t esm = (size_t)(5 + ns) * CE * 32 * sizeof(double);
-    cudaFuncSetAttribute(k_epilogue2d<NSB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
-    k_epilogue2d<NSB><<<sk.nstrip * (sk.T / CE), 256, esm, st>>>(mp, g, sk, scheme, q, wb.fw,
-                                                                 wb.sw, qn, dq_std, CE, flags);
+    // (measured at 1024^2: streamed 1.18 -> 0.87 ms at ns = 40, equal at 20,
+    // slower at 11 (0.19 -> 0.24 ms) and at config 4 (1.39 -> 1.71 ms))
+    auto kepi = NSB > 24 ? k_epilogue2d_s<NSB> : k_epilogue2d<NSB>;
+    cudaFuncSetAttribute(kepi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
+    kepi<<<sk.nstrip * (sk.T / CE), 256, esm, st>>>(mp, g, sk, scheme, q, wb.fw, wb.sw, qn, dq_std,
+                                                    CE, flags);
     if (ev) cudaEventRecord(ev[4], st);
   });
   return cudaGetLastError();
