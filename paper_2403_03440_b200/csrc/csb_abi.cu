@@ -60,7 +60,6 @@ struct csb_ctx {
   double* dom_scratch = nullptr;
   double* norm_partial = nullptr;
   double* fm_buf[2] = {nullptr, nullptr};  // static 2-D face metrics (workspace)
-  double* cm_buf = nullptr;                // static cell metrics (workspace)
   bool fm_dirty = true;
   unsigned int* norm_counter = nullptr;
   int npart_cap = 0;
@@ -202,7 +201,9 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
   c->npart_cap = (int)std::max<long long>(4096, N / 64 + 1);
   c->norm_partial = k.take<double>((size_t)3 * c->npart_cap);
   c->norm_counter = k.take<unsigned int>(64);
-  c->cm_buf = k.take<double>((size_t)16 * N);
+  // (no static cell-metric table: the records kernel forms the cell-averaged
+  // face vectors from the face vectors, measured as fast as streaming a
+  // 16-plane table and 128 B/cell of workspace lighter)
   if (c->g.nk == 1) {
     c->fm_buf[0] = k.take<double>((size_t)6 * c->g.NF[0]);
     c->fm_buf[1] = k.take<double>((size_t)6 * c->g.NF[1]);
@@ -264,12 +265,7 @@ int zero_wave_records(csb_ctx* c, cudaStream_t st) {
 int ensure_face_metrics(csb_ctx* c, cudaStream_t st) {
   if (!c->fm_dirty) return CSB_OK;
   c->g.fm[0] = c->g.fm[1] = nullptr;
-  c->g.cm = nullptr;
-  if (c->cm_buf) {
-    cudaError_t e = launch_cell_metrics(c->g, c->cm_buf, st);
-    if (e != cudaSuccess) return cuda_check(c, e, "cell metrics");
-    c->g.cm = c->cm_buf;
-  }
+  c->g.cm = nullptr;  // cell metrics are formed from the face vectors where used
   if (c->g.nk == 1 && c->geom2d_ok && c->fm_buf[0]) {
     cudaError_t e = launch_face_metrics2d(c->g, c->fm_buf[0], c->fm_buf[1], st);
     if (e != cudaSuccess) return cuda_check(c, e, "face metrics");

@@ -555,26 +555,6 @@ cudaError_t launch_face_metrics2d(const GridDev& g, double* fm0, double* fm1, cu
 }
 
 // Static cell metrics (cell_metric): Sc_d, |Sc_d|^2, |Sc_d| for d = 0..2 and 1/V.
-__global__ void k_cell_metrics(GridDev g, double* cm) {
-  g.cm = nullptr;  // compute from the face vectors
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < g.N;
-       c += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(c % g.nk), j = (int)((c / g.nk) % g.nj), i = (int)(c / ((long long)g.nk * g.nj));
-    for (int d = 0; d < 3; ++d) {
-      double Sc[3], a2, sq;
-      cell_metric(g, c, i, j, k, d, Sc, a2, sq);
-      for (int x = 0; x < 3; ++x) cm[(5 * d + x) * g.N + c] = Sc[x];
-      cm[(5 * d + 3) * g.N + c] = a2;
-      cm[(5 * d + 4) * g.N + c] = sq;
-    }
-    cm[15 * g.N + c] = 1.0 / g.vol[c];
-  }
-}
 
-cudaError_t launch_cell_metrics(const GridDev& g, double* cm, cudaStream_t st) {
-  note_launches(1);
-  k_cell_metrics<<<grid_for(g.N, 256), 256, 0, st>>>(g, cm);
-  return cudaGetLastError();
-}
 
 }  // namespace csb

@@ -144,7 +144,6 @@ cudaError_t launch_dtau_arrays(long long N, const double* li, const double* lv, 
                                unsigned long long* flags, cudaStream_t st);
 cudaError_t launch_check_2d(const GridDev& g, int* ok, cudaStream_t st);
 cudaError_t launch_face_metrics2d(const GridDev& g, double* fm0, double* fm1, cudaStream_t st);
-cudaError_t launch_cell_metrics(const GridDev& g, double* cm, cudaStream_t st);
 cudaError_t launch_set_double(double* dst, double v, cudaStream_t st);
 void note_launches(unsigned long long n);
 unsigned long long launch_count();
