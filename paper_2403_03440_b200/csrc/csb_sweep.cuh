@@ -12,8 +12,8 @@
 
 namespace csb {
 
-// acc[0..n) += 0.5*(A(nb, S) + sgn*lam*I) x, block materialised in the
-// reference's fill order (lusgs.py:24-59); w, b of the neighbour rebuilt
+// acc[0..n) += 0.5*(A(nb, S) + sgn*lam*I) x in rank-2 form (below); the
+// reference materialises the block (lusgs.py:24-59); w, b of the neighbour rebuilt
 // from its stored state.  Returns U = u_nb . S.
 template <int NV>
 CSB_DEV double acc_block(int n, const OpDev& op, long long N, long long nb, const double S[3],
@@ -39,7 +39,7 @@ CSB_DEV double acc_block(int n, const OpDev& op, long long N, long long nb, cons
   b[4] = beta;
   if (n > 5) {
     const double T = st[ST_T * N + nb];
-#pragma unroll 1
+#pragma unroll
     for (int s = 0; s < NV - 5; ++s) {
       if (s < ns) {
         w[5 + s] = rho * op.Y[(long long)s * N + nb];
@@ -51,23 +51,21 @@ CSB_DEV double acc_block(int n, const OpDev& op, long long N, long long nb, cons
     }
   }
   const double dv = 0.5 * (U + sgn * lam);
-#pragma unroll (NV <= 8 ? NV : 1)
+  // rank-2 form of the half block (as the wavefront chains apply it):
+  // A x = w (a . x) + v (b . x) / 2 + dv x with a = (-U, S) / (2 rho),
+  // v = (0, S, U, 0..) -- O(nv) per neighbour instead of the O(nv^2)
+  // materialised block (lusgs.py:24-59; the same products, reassociated)
+  const double ax = ((a0 * x[0] + a1 * x[1]) + a2 * x[2]) + a3 * x[3];
+  double bx = 0.0;
+#pragma unroll
+  for (int c = 0; c < NV; ++c)
+    if (c < n) bx += b[c] * x[c];
+  bx *= 0.5;
+#pragma unroll
   for (int r = 0; r < NV; ++r) {
     if (r >= n) break;
-    double row = 0.0;
-#pragma unroll (NV <= 8 ? NV : 1)
-    for (int c = 0; c < NV; ++c) {
-      if (c >= n) break;
-      double A = 0.0;
-      if (c < 4) A += w[r] * (c == 0 ? a0 : (c == 1 ? a1 : (c == 2 ? a2 : a3)));
-      if (r >= 1 && r <= 4) {
-        const double v = r == 4 ? U : S[r - 1];
-        A += v * (0.5 * b[c]);
-      }
-      if (r == c) A += dv;
-      row += A * x[c];
-    }
-    acc[r] += row;
+    const double v = (r >= 1 && r <= 3) ? S[r - 1] : (r == 4 ? U : 0.0);
+    acc[r] += (w[r] * ax + v * bx) + dv * x[r];
   }
   return U;
 }

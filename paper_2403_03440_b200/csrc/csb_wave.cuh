@@ -1670,10 +1670,11 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[3], st);
     // ---------------- epilogue
+    // (measured at 1024^2: streamed 1.18 -> 0.87 ms at ns = 40, equal at 20,
+    // slower at 11 (0.19 -> 0.24 ms) and at config 4 (1.39 -> 1.71 ms); a
+    // variant staging q in shared memory was slower still at both ends)
     const int CE = epilogue_steps(ns);
     const size_t esm = (size_t)(5 + ns) * CE * 32 * sizeof(double);
-    // (measured at 1024^2: streamed 1.18 -> 0.87 ms at ns = 40, equal at 20,
-    // slower at 11 (0.19 -> 0.24 ms) and at config 4 (1.39 -> 1.71 ms))
     auto kepi = NSB > 24 ? k_epilogue2d_s<NSB> : k_epilogue2d<NSB>;
     cudaFuncSetAttribute(kepi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
     kepi<<<sk.nstrip * (sk.T / CE), 256, esm, st>>>(mp, g, sk, scheme, q, wb.fw, wb.sw, qn, dq_std,
