@@ -177,6 +177,15 @@ struct Carve {
   }
 };
 
+// planes of the FF / FB record groups: CS flow (30), CI coupled
+// (3 NV + 10), plus the ns x ns species block inverses of the coupled
+// operator with chemistry when the workspace carries blocks (NSB <= 16)
+int flow_planes(int nsb, bool with_block) {
+  int n = std::max(30, 3 * (5 + nsb) + 10);
+  if (with_block && nsb <= 16) n = std::max(n, 3 * (5 + nsb) + 10 + nsb * nsb);
+  return n;
+}
+
 size_t carve(csb_ctx* c, char* base, bool with_block) {
   Carve k{0, base};
   const long long N = c->g.N;
@@ -221,7 +230,7 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
     sk.Np = (long long)sk.nstrip * sk.T * 32;  // cells per plane (step-major groups)
     c->wb.sk = sk;
     const int nsb = bucket_of(ns);
-    const int nff = std::max(30, 3 * (5 + nsb) + 10);  // CS flow or CI coupled records
+    const int nff = flow_planes(nsb, with_block);  // CS flow or CI coupled records
     c->wb.ff = k.take<double>((size_t)nff * sk.Np);
     c->wb.fb = k.take<double>((size_t)nff * sk.Np);
     c->wb.fw = k.take<double>((size_t)5 * sk.Np);
@@ -245,7 +254,7 @@ size_t carve(csb_ctx* c, char* base, bool with_block) {
 int zero_wave_records(csb_ctx* c, cudaStream_t st) {
   const int nsb = bucket_of(c->ns);
   const WaveBufs& w = c->wb;
-  const int nff = std::max(30, 3 * (5 + nsb) + 10);
+  const int nff = flow_planes(nsb, c->ws_block);
   const std::pair<double*, int> groups[] = {{w.ff, nff},         {w.fb, nff},
                                             {w.fw, 5},           {w.sf, 2 * nsb + 2},
                                             {w.sb, 2 * nsb + 2}, {w.sw, nsb}};
@@ -770,9 +779,11 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
   const bool full = chem && scheme == SCH_CI;
   const bool dual = dt > 0.0 && std::isfinite(dt);
   if (full && !c->ws_block) return fail(c, CSB_E_STATE, "CI with chemistry needs block workspace");
-  // the coupled operator takes the wavefront path when frozen; dual-time
-  // steps (extra diagonal and rhs terms) take the generic hyperplane path
-  const bool ci_wave = scheme != SCH_CI || !chem;
+  // the coupled operator takes the wavefront path when frozen, and with
+  // chemistry up to 16 species (the ns x ns block inverses ride in the
+  // records); dual-time steps (extra diagonal and rhs terms) take the
+  // generic hyperplane path
+  const bool ci_wave = scheme != SCH_CI || !chem || (c->ws_block && bucket_of(c->ns) <= 16);
   const bool wave = path != 1 && c->wave_ok && !c->wave_disabled && ci_wave && c->geom2d_ok &&
                     rhs_is_R && !dual;
   if (path == 2 && !wave) return fail(c, CSB_E_STATE, "2-D wavefront path not applicable");
@@ -790,7 +801,9 @@ static int implicit_impl(csb_ctx* c, const double* q, const double* R, double cf
       domd = op.dom;
       dstride = op.dom_full ? c->ns + 1 : 1;
     }
-    const int nsI = scheme == SCH_CI ? -1 : chem ? c->ns : 1;  // record layout key
+    const int nsI = scheme == SCH_CI ? (chem ? -2 : -1) : chem ? c->ns : 1;  // record layout key
+    c->wb.ci_d = c->op.d;
+    c->wb.ci_dinv = c->op.dinv;
     if (e == cudaSuccess && c->wb.nsI != nsI) {
       // species record layout changes with nsI: re-zero the padding slots
       e = zero_wave_records(c, st) ? cudaErrorUnknown : cudaSuccess;

@@ -69,6 +69,11 @@ struct WaveBufs {
   cudaStream_t s2;
   cudaEvent_t e1, e2;
   int serial;     // no records / forward-sweep overlap (graph capture: single stream)
+  // coupled operator with chemistry on the wavefront: the scalar diagonal d
+  // written by the records kernel ([N]) and the species block inverses
+  // inv(d I - V dOmega) ([ns * ns][N]) scattered into the CF / CB records
+  double* ci_d;
+  double* ci_dinv;
 };
 
 cudaError_t launch_wave_step(const Model* mp, int ns, const GridDev& g, const WaveBufs& wb,

@@ -70,16 +70,20 @@ constexpr int WKF = CSB_WKF;  // flow slot: 8 steps x 30 planes = 60 KiB (measur
 //   CB (backward) invd, hr2, w[NV], b[NV], lower faces (e[3], sig) x 2, dq*[NV]
 template <int NSB>
 constexpr int ci_planes() { return 3 * (5 + NSB) + 10; }
-template <int NSB>
 #ifndef CSB_CI_SLOT_KB
 #define CSB_CI_SLOT_KB 100  // measured: 512^2 CI 0.842 -> 0.817 ms against 64 KB (8-step slots at ns = 5)
 #endif
+// With chemistry (CHEM) the coupled records also carry the species block
+// inverse dinv[NSB][NSB] (row-major) after those planes, in CF and CB.
+template <int NSB, bool CHEM>
+constexpr int ci_ng() { return ci_planes<NSB>() + (CHEM ? NSB * NSB : 0); }
+template <int NSB, bool CHEM = false>
 constexpr int ci_wk() {
   // (the larger slots only for the register chain: the smem-resident chain
   // above CI_MAXNSB also needs its state next to the ring)
   const int kb = NSB <= 16 ? CSB_CI_SLOT_KB : 64;
   int w = 8;
-  while (w > 1 && w * ci_planes<NSB>() * 256 > kb * 1024) w /= 2;
+  while (w > 1 && w * ci_ng<NSB, CHEM>() * 256 > kb * 1024) w /= 2;
   return w;
 }
 constexpr int CI_MAXNSB = 16;  // register-resident CI chain up to here; smem-resident above
@@ -328,6 +332,7 @@ __global__ void __launch_bounds__(256, NSB <= 8 ? 4 : 3) k_records2d(const Model
       }
       const double dci = base + rci;
       if (!(fabs(dci) >= 1e-300) || !isfinite(dci)) raise_flag(flags, EB_SINGULAR, c);
+      if (per_species && wb.ci_d) wb.ci_d[c] = dci;  // chemistry: the block inverse needs d
       const double beta = cs.gamma - 1.0;
       TC[0 * CT + e] = 1.0 / dci;
       TC[1 * CT + e] = 1.0 / cs.rho;
@@ -403,7 +408,7 @@ __global__ void __launch_bounds__(256, NSB <= 8 ? 4 : 3) k_records2d(const Model
     const int hc = (tt + 1) * HY + (r + 1);
     const double u = A[0 * NH + hc], v = A[1 * NH + hc], hr = A[7 * NH + hc];
     if constexpr (CI) {
-      constexpr int NG = ci_planes<NSB>();
+      const int NG = per_species ? ci_ng<NSB, true>() : ci_ng<NSB, false>();
       double* cf = wb.ff + gaddr(sk, NG, s, t, 0, r);
       double* cb = wb.fb + gaddr(sk, NG, s, t, 0, r);
       for (int p = 0; p < 2 + 2 * NV; ++p) {
@@ -507,6 +512,33 @@ __global__ void __launch_bounds__(256, NSB <= 8 ? 4 : 3) k_records2d(const Model
     }
   }
   publish_tile(wb, s, ib);
+}
+
+// Coupled operator with chemistry: the species block inverses dinv[r][c]
+// (natural layout [ns * ns][N], csb_batched_inverse) into the dinv planes of
+// the CF and CB records; one warp per (strip, step) row, so every store is a
+// 256-byte row of the step-major layout.  Padding rows / columns (>= ns)
+// keep their zeros.
+template <int NSB>
+__global__ void k_dinv2d(GridDev g, Skew sk, int ns, const double* __restrict__ dinv, WaveBufs wb) {
+  constexpr int NG = ci_ng<NSB, true>(), PD = ci_planes<NSB>();
+  const int lane = threadIdx.x & 31;
+  const long long rows = (long long)sk.nstrip * sk.T;
+  for (long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; w < rows;
+       w += ((long long)gridDim.x * blockDim.x) >> 5) {
+    const int s = (int)(w / sk.T), t = (int)(w % sk.T);
+    const int i = t - lane, j = s * 32 + lane;
+    if (i < 0 || i >= g.ni || j >= g.nj) continue;
+    const long long c = (long long)i * g.nj + j;
+    double* cf = wb.ff + gaddr(sk, NG, s, t, PD, lane);
+    double* cb = wb.fb + gaddr(sk, NG, s, t, PD, lane);
+    for (int r = 0; r < ns; ++r)
+      for (int cc = 0; cc < ns; ++cc) {
+        const double v = dinv[((long long)r * ns + cc) * g.N + c];
+        cf[(r * NSB + cc) * 32] = v;
+        cb[(r * NSB + cc) * 32] = v;
+      }
+  }
 }
 
 // ============================================================== wavefront
@@ -763,9 +795,10 @@ CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro, int grp) {
 // coupled (CI, frozen chemistry) chain: NV = 5 + NSB components per row with
 // the full rank-2 half blocks of lusgs.py:24-59 and the scalar diagonal
 // (lusgs.py:62-147); padding species carry zero records.
-template <int NSB, bool BWD>
+template <int NSB, bool BWD, bool CHEM>
 CSB_DEV void chain_ci(const ChainCtx& x, const WaveRole& ro) {
-  constexpr int NV = 5 + NSB, NG = ci_planes<NSB>(), WK = ci_wk<NSB>();
+  constexpr int NV = 5 + NSB, NG = ci_ng<NSB, CHEM>(), WK = ci_wk<NSB, CHEM>();
+  constexpr int PD = ci_planes<NSB>();  // CHEM: first dinv plane
   constexpr int PV = BWD ? 2 + 2 * NV + 8 : 2 + 2 * NV;  // dq* (backward) | rhs (forward)
   constexpr int FQ = BWD ? 2 + 2 * NV : 2 + 3 * NV;      // first face plane
   constexpr int NGO = BWD ? 5 : NG, PO = BWD ? 0 : 2 + 2 * NV + 8;
@@ -799,11 +832,32 @@ CSB_DEV void chain_ci(const ChainCtx& x, const WaveRole& ro) {
       }
       const double invd = p[0], hr2 = p[32];
       double dq[NV];
+      if constexpr (!CHEM) {
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+          const double v = p[(PV + c) * 32];
+          if (BWD) dq[c] = v - (oi[c] + ij[c]) * invd;
+          else dq[c] = ((v + oi[c]) + ij[c]) * invd;
+        }
+      } else {
+        // chemistry (lusgs.py:92-100, 136-144): flow rows / d, species rows
+        // dinv acc[5:] with dinv = inv(d I - V dOmega) from the records
+        double acc[NV];
+#pragma unroll
+        for (int c = 0; c < NV; ++c)
+          acc[c] = BWD ? oi[c] + ij[c] : (p[(PV + c) * 32] + oi[c]) + ij[c];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) dq[c] = BWD ? p[(PV + c) * 32] - acc[c] * invd : acc[c] * invd;
+#pragma unroll
+        for (int r = 0; r < NSB; ++r) {
+          double t = 0.0;
+#pragma unroll
+          for (int c = 0; c < NSB; ++c) t = fma(p[(PD + r * NSB + c) * 32], acc[5 + c], t);
+          dq[5 + r] = BWD ? p[(PV + 5 + r) * 32] - t : t;
+        }
+      }
 #pragma unroll
       for (int c = 0; c < NV; ++c) {
-        const double v = p[(PV + c) * 32];
-        if (BWD) dq[c] = v - (oi[c] + ij[c]) * invd;
-        else dq[c] = ((v + oi[c]) + ij[c]) * invd;
         if (!BWD) ob[(kk * NGO + c) * 32] = dq[c];
         else if (c < 5) ob[(kk * 5 + c) * 32] = dq[c];
         else ob2[(kk * NSB + c - 5) * 32] = dq[c];
@@ -951,7 +1005,8 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
                    : a.only == 5                  ? (blockIdx.x & 1)
                                                   : ((blockIdx.x >> 1) & 1);
   const WaveRole ro = kind == 1 ? a.role[1] : a.role[0];
-  const int WK = kind == 2 ? ci_wk<NSB>() : kind ? wave_wks<NSB, PER>() : WKF;
+  const int WK = kind == 2 ? (PER ? ci_wk<NSB, true>() : ci_wk<NSB, false>())
+                 : kind ? wave_wks<NSB, PER>() : WKF;
   const int nh = kind == 2 ? 5 + NSB : kind ? NSB : 5;
   const int nchain = kind == 1 ? sp_warps<NSB>() : 1;  // chain warps of this role
   const int D = ro.D, NG = ro.ng;
@@ -1182,8 +1237,10 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
     chain_species<NSB, BWD, PER>(x, ro, warp);
   } else {
     if constexpr (!PER) {
-      if constexpr (NSB <= CI_MAXNSB) chain_ci<NSB, BWD>(x, ro);
+      if constexpr (NSB <= CI_MAXNSB) chain_ci<NSB, BWD, false>(x, ro);
       else chain_ci_big<NSB, BWD>(x, ro, hin + (HRING + WK) * nh);
+    } else {  // coupled operator with chemistry (register chain only)
+      if constexpr (NSB <= CI_MAXNSB) chain_ci<NSB, BWD, true>(x, ro);
     }
   }
   if (a.dbg && lane == 0) {
@@ -1498,12 +1555,15 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
   CSB_NS_DISPATCH(ns, {
     const Skew& sk = wb.sk;
     const bool ci = scheme == SCH_CI;
-    if (ci && per_species) return cudaErrorInvalidConfiguration;
+    // coupled operator with chemistry: register chain + dinv records only
+    const bool ci_chem = ci && per_species;
+    if (ci_chem && (NSB > CI_MAXNSB || !wb.ci_d || !wb.ci_dinv)) return cudaErrorInvalidConfiguration;
     constexpr int NV = 5 + NSB;
     const int nsI = per_species ? NSB : 1;
     const int NSF = nsI + NSB + 2;
     const int WKS = per_species ? wave_wks<NSB, true>() : wave_wks<NSB, false>();
-    constexpr int NGC = ci_planes<NSB>(), WKC = ci_wk<NSB>();
+    const int NGC = ci_chem ? ci_ng<NSB, true>() : ci_ng<NSB, false>();
+    const int WKC = ci_chem ? ci_wk<NSB, true>() : ci_wk<NSB, false>();
     // large NSB (CI): + the smem-resident chain state (4 x NV x 32 doubles)
     const size_t ci_extra = NSB > CI_MAXNSB ? (size_t)4 * NV * 32 * sizeof(double) : 0;
     int Df = 0, Ds = 0, Dc = 0;
@@ -1533,8 +1593,15 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     auto launch_records = [&](cudaStream_t s, bool publish) {
       WaveBufs wr = wb;
       if (!publish) wr.rdy = nullptr;  // (no per-tile fence when nothing consumes the flags)
-      krec<<<nrec, 256, rsm, s>>>(mp, g, sk, q, R, cfl, lamS, domd, dom_stride, ci ? 0 : per_species,
+      krec<<<nrec, 256, rsm, s>>>(mp, g, sk, q, R, cfl, lamS, domd, dom_stride, per_species,
                                   sp_scale, wr, C, flags);
+      if (ci_chem) {
+        // dinv = inv(d I - V dOmega) per cell (implicit.py:362-368), into the records
+        launch_block_inverse(ns, g.N, domd, wb.ci_d, g.vol, wb.ci_dinv, flags, s);
+        note_launches(1);
+        k_dinv2d<NSB><<<grid_for((long long)sk.nstrip * sk.T * 32, 256), 256, 0, s>>>(
+            g, sk, ns, wb.ci_dinv, wb);
+      }
     };
     // ---------------- one sweep
     int only = -1;
@@ -1641,7 +1708,7 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     // (the threshold counts 2 CTAs per strip for CI too, as measured)
     const int sms = device_sms();
     const int nsweep = ci ? sk.nstrip : 2 * sk.nstrip;
-    const bool overlap = !ev && wb.s2 && !wb.serial && only == -1 &&
+    const bool overlap = !ev && wb.s2 && !wb.serial && !ci_chem && only == -1 &&
                          (2 * sk.nstrip <= sms * 48 / 148 ||
                           (getenv("CSB_FORCE_OVERLAP") && nsweep <= sms - 8)) &&
                          !getenv("CSB_NO_OVERLAP");

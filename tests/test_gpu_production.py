@@ -267,3 +267,30 @@ def test_wavefront_chemistry_ring_fits_at_buckets_24_48(ns):
     qw, fw, cw, _, dw = driver.implicit_step_raw(case, spec.q, R, spec.cfl, path=2, want_dq=True)
     assert comp_relerr(dw, dg) <= 1e-10
     assert (fw, cw) == (fg, cg)
+
+
+# ------------------------------------------------------- coupled operator with chemistry
+
+
+@pytest.mark.parametrize("ns,dims", [(5, (24, 40, 1)), (11, (24, 200, 1)), (16, (20, 70, 1)),
+                                     (5, (16, 832, 1))])
+def test_ci_chemistry_wavefront_vs_generic_and_oracle(ns, dims):
+    """The coupled operator with chemistry on the wavefront (the ns x ns
+    species block inverses ride in the CF / CB records and the chain applies
+    them, lusgs.py:92-100, 136-144): against the generic hyperplane sweeps of
+    the same step, and against the oracle with dOmega injected,
+    up to 16 species and at 26 strips."""
+    from paper_2403_03440_b200 import configs as C
+    from paper_2403_03440_b200 import driver, spatial
+    from paper_2403_03440_b200.configs import build_case
+    spec = C.config3(ns, seed=11, dims=dims, chemistry=True)
+    grid, model, bcs, mech = build_case(spec)
+    R = spatial.assemble_residual(spec.q, grid, bcs, mech, model)
+    case = driver.Case(grid=grid, model=model, bcs=bcs, freestream=None, mech=mech, scheme="CI",
+                       cfl=spec.cfl)
+    qg, fg, cg, _, dg = driver.implicit_step_raw(case, spec.q, R, spec.cfl, path=1, want_dq=True)
+    qw, fw, cw, _, dw = driver.implicit_step_raw(case, spec.q, R, spec.cfl, path=2, want_dq=True)
+    assert comp_relerr(dw, dg) <= 1e-10
+    assert comp_relerr(qw - spec.q, qg - spec.q) <= 1e-10
+    assert (fw, cw) == (fg, cg)
+    _iteration(spec, ("CI",), chemistry=True, path=2)
