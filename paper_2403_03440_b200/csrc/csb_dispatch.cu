@@ -104,7 +104,7 @@ cudaError_t launch_assemble_cell(const Model* mp, int ns, const GridDev& g, cons
 }
 cudaError_t launch_sweeps_generic(const Model* mdl, int ns, const GridDev& g, const OpDev& op,
                                   const double* rhs, double* dq, double* dq_star, cudaStream_t st) {
-  note_launches(2ull * ((g.ni - 1) + (g.nj - 1) + (g.nk - 1) + 1));
+  // (counted by launch_sweeps, which replays these launches as one graph)
   CSB_ROUTE(launch_sweeps_generic, mdl, ns, g, op, rhs, dq, dq_star, st)
 }
 cudaError_t launch_update(const Model* mp, int ns, const GridDev& g, int scheme, const double* q,
