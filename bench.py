@@ -497,7 +497,8 @@ def chemistry_scan(flush, nss=(5, 11, 20, 40), dims=(1024, 1024, 1), K=2, W=1):
     reactions, BASELINE config-3 recipe), CS1 vs CI per ns on the 1024^2 box.
     The iteration includes the FD source Jacobian (reference
     chemistry.py:76-104); CI with chemistry adds the species block inverse
-    inv(d I - V dOmega) per cell (implicit.py:362-368).  The synthetic
+    inv(d I - V dOmega) per cell (implicit.py:362-368) and runs on the
+    wavefront up to 16 species (generic hyperplane sweeps above).  The synthetic
     mechanisms are extremely stiff: the gate flags most cells,
     which does not change the work done."""
     import torch
@@ -516,6 +517,9 @@ def chemistry_scan(flush, nss=(5, 11, 20, 40), dims=(1024, 1024, 1), K=2, W=1):
                     "coupled_CI": N * K / (ci_ms * 1e-3),
                     "split_ms": cs_ms / K, "coupled_ms": ci_ms / K,
                     "split_srcjac_ms": st_cs["srcjac"],
+                    "coupled_path": ("wavefront (register CI chain, ns x ns block inverses in the "
+                                     "records)" if ns <= 16 else
+                                     "generic hyperplane sweeps (graph-replayed) + block inverse"),
                     "coupled_launches_per_step": launches / K})
         del run
         torch.cuda.empty_cache()
