@@ -138,12 +138,46 @@ CSB_DEV void mbar_wait(unsigned long long* b, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+CSB_DEV unsigned long long l2_evict_first() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+CSB_DEV unsigned long long l2_evict_last() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// Hand-off words (sentinel reset, chain stores, receiver polls) carry an
+// L2 evict-last hint and the sweeps' record streams an evict-first one: the
+// hand-off buffer (73 MB at config 4) then stays in L2 while the records
+// stream through it.  Without the hints the streams evicted the hand-off
+// lines, every poll became an HBM round trip under full load, and the
+// receiver (one poll in flight) set the pace of every strip with an upstream
+// strip (config 4: species strips 119 -> ~250 ns per step once ~25 strips ran;
+// sweeps 1.42 + 1.50 -> 1.23 + 1.25 ms).
+CSB_DEV void st_hand(double* p, double v) {
+#ifndef CSB_HAND_NORMAL
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(l2_evict_last())
+               : "memory");
+#else
+  *p = v;
+#endif
+}
 CSB_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+#ifndef CSB_TMA_NORMAL
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_evict_first())
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+#endif
 }
 CSB_DEV int ld_relaxed(const int* p) {
   int v;
@@ -198,7 +232,7 @@ static __global__ void k_hand_reset(double* __restrict__ hand, int nstrip, int T
     double* p = hand + sweep * per_sweep + (role ? (long long)nstrip * rows * nhf : 0) +
                 ((long long)strip * rows + r) * nh;
     const double v = (r < HPAD || r >= rows - HPAD) ? 0.0 : sent;
-    for (int c = 0; c < nh; ++c) p[c] = v;
+    for (int c = 0; c < nh; ++c) st_hand(p + c, v);
   }
 }
 
@@ -594,13 +628,57 @@ struct ChainCtx {
   double* hand_out;     // this strip's row of the hand-off buffer, at its step 0
   unsigned long long* full_bar;
   unsigned long long* empty_bar;
+  unsigned long long* pd;  // timing probe (CSB_PROBES): this CTA's stamp row, or null
 };
+
+// timing probe helpers (CSB_PROBES builds only): per-slot progress stamps and
+// the total time a chain waits for its ring slots
+CSB_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#ifdef CSB_PROBES
+#define CSB_PROBE_WAIT(bar, ph)                                       \
+  {                                                                   \
+    const unsigned long long tw0 = x.pd ? gtime() : 0ull;             \
+    mbar_wait(bar, ph);                                               \
+    if (x.pd) {                                                       \
+      const unsigned long long tw1 = gtime();                         \
+      pwait += tw1 - tw0;                                             \
+      if ((threadIdx.x & 31) == 0 && ks % 32 == 0 && ks / 32 < 56) x.pd[4 + ks / 32] = tw1; \
+    }                                                                 \
+  }
+#define CSB_PROBE_DECL unsigned long long pwait = 0ull;
+#define CSB_PROBE_END(slot_) \
+  if (x.pd && (threadIdx.x & 31) == 0) x.pd[slot_] = pwait;
+#else
+#define CSB_PROBE_WAIT(bar, ph) mbar_wait(bar, ph);
+#define CSB_PROBE_DECL
+#define CSB_PROBE_END(slot_)
+#endif
 
 // predicated store without a branch (a branch would end the scheduling region
 // of the unrolled step loop)
 CSB_DEV void st_pred_cg_f64(double* p, double v, bool pred) {
+#ifndef CSB_HAND_NORMAL
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.cg.L2::cache_hint.f64 [%0], %1, %3;\n}" ::"l"(p),
+      "d"(v), "r"((int)pred), "l"(l2_evict_last()));
+#else
   asm volatile("{\n.reg .pred q;\nsetp.ne.b32 q, %2, 0;\n@q st.global.cg.f64 [%0], %1;\n}" ::"l"(p),
                "d"(v), "r"((int)pred));
+#endif
+}
+// hand-off poll load (L2, bypassing L1)
+CSB_DEV unsigned long long ld_hand(const long long* p) {
+#ifndef CSB_HAND_NORMAL
+  unsigned long long v;
+  asm volatile("ld.global.cg.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(l2_evict_last()));
+  return v;
+#else
+  return (unsigned long long)__ldcg(p);
+#endif
 }
 
 // flow chain: 5 coupled components per row (rank-2 half blocks)
@@ -646,9 +724,10 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
   const long long slot = (long long)WK * NG * 32;
   double oi[5] = {0, 0, 0, 0, 0}, oj[5] = {0, 0, 0, 0, 0};
   int buf = 0, phase = 0;
+  CSB_PROBE_DECL
   for (int ks = 0; ks < x.nslots; ++ks) {
     const int k = BWD ? x.nslots - 1 - ks : ks;
-    mbar_wait(&x.full_bar[buf], phase);
+    CSB_PROBE_WAIT(&x.full_bar[buf], phase)
     const double* base = x.ring + buf * slot + lane;
     double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO) * 32 + lane;
     const double* hb = x.recv ? x.hin + ((k * WK) % HRING) * 5 : x.hin + HRING * 5;
@@ -715,6 +794,7 @@ CSB_DEV void chain_flow(const ChainCtx& x, const WaveRole& ro) {
       phase ^= 1;
     }
   }
+  CSB_PROBE_END(2)
 }
 
 // species chains: NSB independent scalar chains per row (padding species carry
@@ -750,9 +830,14 @@ CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro, int grp) {
 #pragma unroll
   for (int c = 0; c < SG; ++c) oi[c] = oj[c] = 0.0;
   int buf = 0, phase = 0;
+  CSB_PROBE_DECL
   for (int ks = 0; ks < x.nslots; ++ks) {
     const int k = BWD ? x.nslots - 1 - ks : ks;
-    mbar_wait(&x.full_bar[buf], phase);
+    if (grp == 0) {
+      CSB_PROBE_WAIT(&x.full_bar[buf], phase)
+    } else {
+      mbar_wait(&x.full_bar[buf], phase);
+    }
     const double* base = x.ring + buf * slot + lane;
     double* ob = ro.out + (((long long)x.s * a.sk.T + (long long)k * WK) * NGO + PO + c0) * 32 + lane;
     const double* hb = (x.recv ? x.hin + ((k * WK) % HRING) * NSB : x.hin + HRING * NSB) + c0;
@@ -790,6 +875,7 @@ CSB_DEV void chain_species(const ChainCtx& x, const WaveRole& ro, int grp) {
       phase ^= 1;
     }
   }
+  if (grp == 0) { CSB_PROBE_END(2) }
 }
 
 // coupled (CI, frozen chemistry) chain: NV = 5 + NSB components per row with
@@ -1040,6 +1126,7 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
   x.hand_out = ro.hand + ((long long)x.s * (T + 2 * HPAD) + HPAD) * nh;
   x.full_bar = full_bar;
   x.empty_bar = empty_bar;
+  x.pd = a.dbg ? a.dbg + 64 * (2 * s_strip + kind) : nullptr;
   if (threadIdx.x == 0) {
     for (int b = 0; b < D; ++b) {
       mbar_init(&full_bar[b], (x.has_up || a.fake_recv) ? 2 : 1);  // TMA producer (+ hand-off receiver)
@@ -1057,9 +1144,18 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
     if (lane == 0) {
       const int ep = a.rdy ? *a.epoch : 0;
       int buf = 0, phase = 0;
+#ifdef CSB_PROBES
+      unsigned long long pw = 0ull;
+#endif
       for (int ks = 0; ks < x.nslots; ++ks) {
         const int k = BWD ? x.nslots - 1 - ks : ks;
+#ifdef CSB_PROBES
+        const unsigned long long tw0 = x.pd ? gtime() : 0ull;
         if (ks >= D) mbar_wait(&empty_bar[buf], phase ^ 1);
+        if (x.pd) pw += gtime() - tw0;
+#else
+        if (ks >= D) mbar_wait(&empty_bar[buf], phase ^ 1);
+#endif
         if (a.rdy) {
           // records tiles of this slot's steps stored (records kernel running
           // concurrently): acquire their flags, then order the bulk copy
@@ -1081,6 +1177,9 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
           phase ^= 1;
         }
       }
+#ifdef CSB_PROBES
+      if (x.pd) x.pd[60] = pw;
+#endif
     }
     return;
   }
@@ -1123,12 +1222,21 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
     // Q is rounded down to a power of two; WK is one already)
     int Q = max(1, min(WK >= 8 ? 1 : 8 / WK, 512 / nw));
     while (Q & (Q - 1)) Q &= Q - 1;
+#ifdef CSB_PROBES
+    unsigned long long rpoll = 0ull;
+#endif
     if (Q == 1) {
     // one slot per poll (slots of >= 8 steps)
     int buf = 0, phase = 0;
     for (int ks = 0; ks < x.nslots; ++ks) {
       const int k = BWD ? x.nslots - 1 - ks : ks;
       if (ks >= D) mbar_wait(&empty_bar[buf], phase ^ 1);  // slot free: hin rows too
+#ifdef CSB_RECV_LAG
+      {  // probe: poll only once the chain has released slot ks - D + LAG
+        const int j = ks - D + CSB_RECV_LAG;
+        if (j >= 0 && CSB_RECV_LAG > 0) mbar_wait(&empty_bar[j % D], (j / D) & 1);
+      }
+#endif
       const long long u0 = (long long)k * WK + (BWD ? -31 : 31);  // upstream step of kk = 0
       const long long* sw = reinterpret_cast<const long long*>(src) + u0 * nh;
       double* dst = hin + ((k * WK) % HRING) * nh;
@@ -1136,6 +1244,9 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
       unsigned have = 0u;  // bit r: word lane + 32 r loaded and final
       const int cnt = nw > lane ? (nw - lane + 31) / 32 : 0;
       const unsigned need = (1u << cnt) - 1u;
+#ifdef CSB_PROBES
+      const unsigned long long tp0 = x.pd ? gtime() : 0ull;
+#endif
       while (true) {
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -1145,7 +1256,7 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
               w[r] = 0ull;
               have |= 1u << r;
             } else {
-              w[r] = (unsigned long long)__ldcg(sw + e);
+              w[r] = ld_hand(sw + e);
               if (w[r] != HAND_SENTINEL) have |= 1u << r;
             }
           }
@@ -1153,6 +1264,9 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
         if (__all_sync(0xffffffffu, (have & need) == need)) break;
         __nanosleep(a.poll_ns);
       }
+#ifdef CSB_PROBES
+      if (x.pd) rpoll += gtime() - tp0;
+#endif
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
         const int e = lane + 32 * r;
@@ -1193,7 +1307,7 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
               w[r] = 0ull;
               have |= 1u << r;
             } else {
-              w[r] = (unsigned long long)__ldcg(sw + e);
+              w[r] = ld_hand(sw + e);
               if (w[r] != HAND_SENTINEL) have |= 1u << r;
             }
           }
@@ -1218,6 +1332,9 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
       }
     }
     }
+#ifdef CSB_PROBES
+    if (x.pd && lane == 0) x.pd[3] = rpoll;
+#endif
     return;
   }
 
@@ -1246,7 +1363,7 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
   if (a.dbg && lane == 0) {
     unsigned long long t1;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    unsigned long long* d = a.dbg + 16 * (2 * s + kind);
+    unsigned long long* d = a.dbg + 64 * (2 * s + kind);
     d[0] = t0;
     d[1] = t1;
   }
@@ -1625,8 +1742,8 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       wa.dbg = nullptr;
       static unsigned long long* dbg = nullptr;
       if (probe_env("CSB_WAVE_DBG")) {
-        if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 16 * 2 * 4096);
-        cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 16 * 2 * sk.nstrip, s);
+        if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 64 * 2 * 4096);
+        cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 64 * 2 * sk.nstrip, s);
         wa.dbg = dbg;
       }
       size_t smem;
@@ -1678,16 +1795,23 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
       cudaMemsetAsync(wb.prog, 0, sizeof(int) * 2, s);
       kfn<<<nblk, wave_threads<NSB>(), smem, s>>>(wa);
       if (wa.dbg) {
-        std::vector<unsigned long long> h(16 * 2 * sk.nstrip);
+        std::vector<unsigned long long> h(64 * 2 * sk.nstrip);
         cudaMemcpyAsync(h.data(), wa.dbg, h.size() * 8, cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
         unsigned long long tmin = ~0ull;
         for (int e = 0; e < 2 * sk.nstrip; ++e)
-          if (h[16 * e]) tmin = std::min(tmin, h[16 * e]);
+          if (h[64 * e]) tmin = std::min(tmin, h[64 * e]);
         for (int e = 0; e < 2 * sk.nstrip; ++e)
-          if (h[16 * e])
-            fprintf(stderr, "wave%s strip %d kind %d: start %.2f end %.2f\n", bwd ? "B" : "F",
-                    e / 2, e % 2, (h[16 * e] - tmin) * 1e-3, (h[16 * e + 1] - tmin) * 1e-3);
+          if (h[64 * e]) {
+            const unsigned long long* d = &h[64 * e];
+            fprintf(stderr,
+                    "wave%s strip %d kind %d: start %.2f end %.2f chain_wait %.2f recv_poll %.2f "
+                    "prod_wait %.2f stamps",
+                    bwd ? "B" : "F", e / 2, e % 2, (d[0] - tmin) * 1e-3, (d[1] - tmin) * 1e-3,
+                    d[2] * 1e-3, d[3] * 1e-3, d[60] * 1e-3);
+            for (int q = 4; q < 60 && d[q]; ++q) fprintf(stderr, " %.1f", (d[q] - tmin) * 1e-3);
+            fprintf(stderr, "\n");
+          }
       }
       return cudaGetLastError();
     };
