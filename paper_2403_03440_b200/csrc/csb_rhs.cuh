@@ -16,6 +16,7 @@
 #pragma once
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "csb_common.cuh"
 #include "csb_kernels.cuh"
@@ -894,8 +895,12 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
   const int strideX = K2D ? BY : BY * BZ, strideY = K2D ? 1 : BZ, strideZ = 1;
   const int ndir = K2D ? 2 : 3;
 
-#pragma unroll 1
-  for (int d = 0; d < ndir; ++d) {
+  // One direction: convective + viscous face passes into sF, then the flux
+  // difference into the cells.  dtag is std::integral_constant<int, D> on the
+  // 2-D path (every grid-array index static: no local copy of the kernel
+  // parameters) and a plain int on the 3-D path.
+  auto dir_pass = [&](auto dtag) {
+    const int d = dtag;
     // faces of direction d inside the tile: dims (ci+1, cj, ck) etc.  2-D:
     // enumerated over the full tile (FY columns; constant with a fixed tile),
     // faces beyond a partial edge tile skipped; the flux buffer uses the
@@ -996,9 +1001,13 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
     }
     }
     __syncthreads();
-    // difference into R (R = 0 + dR_0 + dR_1 + dR_2, spatial.py:258-259);
+    // difference into R (R = 0 + dR_0 + dR_1 + dR_2, spatial.py:258-259).
+    // The last direction also applies the chemistry source (261-267), the
+    // finite check (269-271) and, when requested, the residual-norm terms
+    // (driver.py:85-90), so R is read back once per direction at most.
     // 2-D: cells over the full tile (index ii * TJ + jj, also the sR index)
     const int ncell = K2D ? TI * TJ : ci * cj * ck;
+    const bool last = d == ndir - 1;
     for (int l = threadIdx.x; l < ncell; l += blockDim.x) {
       const int kk = K2D ? 0 : l % ck;
       const int jj = K2D ? l % TJ : (l / ck) % cj;
@@ -1016,53 +1025,46 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
         flo = (ii * FY + jj) * fz + kk;
         fhi = flo + 1;
       }
-      for (int c = 0; c < nv; ++c) {
-        const double dR = sF[c * maxf + fhi] - sF[c * maxf + flo];
-        double* r = sr_on ? sR + c * ncell + l : R + (long long)c * g.N + cell;
-        if (d == 0) *r = dR;
-        else *r = *r + dR;
+      const long long N = g.N;
+      double* __restrict__ Rc = R + cell;
+      double* __restrict__ sRc = sR + l;
+      if (!last) {
+        // first / middle direction: partial sums, loads of a group of 8
+        // components issued before their stores
+        for (int c0 = 0; c0 < nv; c0 += 8) {
+          double pv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            pv[k] = (d == 0 || c0 + k >= nv) ? 0.0 : (sr_on ? sRc[(c0 + k) * ncell] : Rc[(c0 + k) * N]);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int c = c0 + k;
+            if (c >= nv) break;
+            const double dR = sF[c * maxf + fhi] - sF[c * maxf + flo];
+            const double v = d == 0 ? dR : pv[k] + dR;
+            if (sr_on) sRc[c * ncell] = v;
+            else Rc[c * N] = v;
+          }
+        }
+        continue;
       }
-    }
-    __syncthreads();
-  }
-
-  // chemistry source (spatial.py:261-267), the finite check (269-271) and,
-  // when requested, the residual norms (driver.py:85-90)
-  const int ncell = K2D ? TI * TJ : ci * cj * ck;
-  for (int l = threadIdx.x; l < ncell; l += blockDim.x) {
-    const int kk = K2D ? 0 : l % ck;
-    const int jj = K2D ? l % TJ : (l / ck) % cj;
-    const int ii = K2D ? l / TJ : l / (ck * cj);
-    if (K2D && (ii >= ci || jj >= cj)) continue;
-    const long long cell = cell_index(g, i0 + ii, j0 + jj, k0 + kk);
-    if (mech.nrx > 0) {
-      const int ls = lidx(ii + NG, jj + NG, K2D ? 0 : kk + NG);
-      double rs[NSB], om[NSB];
-      const double rho = sP[ls];
+      // last direction
+      double om[NSB];
+      double V = 0.0;
+      const bool chem = mech.nrx > 0;
+      if (chem) {
+        const int ls = lidx(ii + NG, jj + NG, K2D ? 0 : kk + NG);
+        double rs[NSB];
+        const double rho = sP[ls];
 #pragma unroll
-      for (int s = 0; s < NSB; ++s)
-        if (s < ns) rs[s] = rho * sP[(5 + s) * ldP + ls];
-      omega_cell<NSB>(m, mech, sP[(5 + ns) * ldP + ls], rs, om);
-      const double V = __ldg(g.vol + cell);
-#pragma unroll
-      for (int s = 0; s < NSB; ++s)
-        if (s < ns) {
-          double* r = sr_on ? sR + (5 + s) * ncell + l : R + (long long)(5 + s) * g.N + cell;
-          *r = *r - om[s] * V;
-        }
-    }
-    bool fin = true;
-    if constexpr (stream_species<NSB>()) {
-      // large species counts: one component at a time (same sums, same order)
+        for (int s = 0; s < NSB; ++s)
+          if (s < ns) rs[s] = rho * sP[(5 + s) * ldP + ls];
+        omega_cell<NSB>(m, mech, sP[(5 + ns) * ldP + ls], rs, om);
+        V = __ldg(g.vol + cell);
+      }
+      bool fin = true;
       double f = 0.0, sp = 0.0, r0 = 0.0;
-      for (int c = 0; c < nv; ++c) {
-        double v;
-        if (sr_on) {
-          v = sR[c * ncell + l];
-          R[(long long)c * g.N + cell] = v;
-        } else {
-          v = R[(long long)c * g.N + cell];
-        }
+      auto fold = [&](int c, double v) {
         fin &= finite(v);
         if (c == 0) {
           r0 = v;
@@ -1072,6 +1074,36 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
         } else {
           sp += v;
         }
+      };
+      if constexpr (stream_species<NSB>()) {
+        for (int c0 = 0; c0 < nv; c0 += 8) {
+          double pv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            pv[k] = (c0 + k >= nv) ? 0.0 : (sr_on ? sRc[(c0 + k) * ncell] : Rc[(c0 + k) * N]);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int c = c0 + k;
+            if (c >= nv) break;
+            double v = pv[k] + (sF[c * maxf + fhi] - sF[c * maxf + flo]);
+            if (chem && c >= 5) v = v - om[c - 5] * V;
+            Rc[c * N] = v;
+            fold(c, v);
+          }
+        }
+      } else {
+        double rv[5 + NSB];
+#pragma unroll
+        for (int c = 0; c < 5 + NSB; ++c)
+          if (c < nv) rv[c] = sr_on ? sRc[c * ncell] : Rc[c * N];
+#pragma unroll
+        for (int c = 0; c < 5 + NSB; ++c)
+          if (c < nv) {
+            double v = rv[c] + (sF[c * maxf + fhi] - sF[c * maxf + flo]);
+            if (chem && c >= 5) v = v - om[c - 5] * V;
+            Rc[c * N] = v;
+            fold(c, v);
+          }
       }
       if (!fin) raise_flag(flags, EB_RES_NONFINITE, cell);
       if (nrm.out) {
@@ -1079,36 +1111,16 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
         n_sp += sp * sp;
         n_rho += r0 * r0;
       }
-      continue;
     }
-    double rv[5 + NSB];
-#pragma unroll
-    for (int c = 0; c < 5 + NSB; ++c)
-      if (c < nv) {
-        if (sr_on) {
-          rv[c] = sR[c * ncell + l];
-          R[(long long)c * g.N + cell] = rv[c];
-        } else {
-          rv[c] = R[(long long)c * g.N + cell];
-        }
-        fin &= finite(rv[c]);
-      }
-    if (!fin) raise_flag(flags, EB_RES_NONFINITE, cell);
-    if (nrm.out) {
-      // residual_norms terms (driver.py:85-90), as k_norms_partial
-      double f = rv[0] * rv[0];
-#pragma unroll
-      for (int c = 1; c < 5; ++c) f += rv[c] * rv[c];
-      double sp = 0.0;
-#pragma unroll
-      for (int c = 0; c < NSB; ++c)
-        if (c < ns) sp += rv[5 + c];
-      n_flow += f;
-      n_sp += sp * sp;
-      n_rho += rv[0] * rv[0];
-    }
+    __syncthreads();  // next direction rewrites sF; next tile restages sP
+  };
+  if constexpr (K2D) {
+    dir_pass(std::integral_constant<int, 0>{});
+    dir_pass(std::integral_constant<int, 1>{});
+  } else {
+#pragma unroll 1
+    for (int d = 0; d < 3; ++d) dir_pass(d);
   }
-  __syncthreads();  // next tile restages sP / sF / sR
   }  // tile loop
   if (nrm.out) {
     // block partials, then the last block reduces all partials in fixed order
@@ -1242,23 +1254,23 @@ cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, c
   if (sr_on) smem = smem_sr;
   const long long ntiles = (long long)((g.ni + TI - 1) / TI) * ((g.nj + TJ - 1) / TJ) *
                            (k2d ? 1 : (g.nk + TK - 1) / TK);
-  // guarded fallback: a persistent grid (exits at once when not needed)
-  const long long nblk = guard ? std::min<long long>(ntiles, 2LL * device_sms()) : ntiles;
-  if (!(nrm.out && nblk <= nrm.cap)) nrm.out = nullptr;
-  if (fused) *fused = nrm.out != nullptr;
+  // persistent grid: every resident CTA loops over the tiles (the model
+  // table, the kernel setup and the block's norms reduction are paid once
+  // per CTA instead of once per tile)
   cudaError_t err = cudaSuccess;
   CSB_NS_DISPATCH(ns, {
-    if (k2d) {
-      auto kfn = TI == 15 && TJ == 16 ? k_residual<NSB, true, 15, 16> : k_residual<NSB, true>;
-      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kfn<<<(unsigned)nblk, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
-                                             nrm, sr_on, guard);
-    } else {
-      auto kfn = k_residual<NSB, false>;
-      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kfn<<<(unsigned)nblk, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
-                                             nrm, sr_on, guard);
-    }
+    auto kfn = k2d ? (TI == 15 && TJ == 16 ? k_residual<NSB, true, 15, 16> : k_residual<NSB, true>)
+                   : k_residual<NSB, false>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    const long long nblk = std::min<long long>(ntiles, (long long)per_sm * device_sms());
+    if (!(nrm.out && nblk <= nrm.cap)) nrm.out = nullptr;
+    if (fused) *fused = nrm.out != nullptr;
+    kfn<<<(unsigned)nblk, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
+                                           nrm, sr_on, guard);
     err = cudaGetLastError();
   });
   return err;
