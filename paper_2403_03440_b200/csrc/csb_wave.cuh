@@ -1370,134 +1370,114 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
 }
 
 // ============================================================== epilogue
-// Tile = one strip x C steps (a parallelogram in (i, j), as in k_records2d).
-// Phase A: the step-major dq rows -> smem (a warp reads one contiguous row);
-// phase B: closure + gate column by column, so the q / q_new accesses of a
-// warp are contiguous runs of up to C cells.
-template <int NSB>
-__global__ void __launch_bounds__(256, NSB <= 8 ? 3 : 2) k_epilogue2d(const Model* __restrict__ mp, GridDev g, Skew sk,
-                                                    int scheme, const double* __restrict__ q,
-                                                    const double* __restrict__ fw,
-                                                    const double* __restrict__ sw,
-                                                    double* __restrict__ qn,
-                                                    double* __restrict__ dq_std, int C,
-                                                    unsigned long long* flags) {
-  extern __shared__ double es[];
-  const Model& m = *mp;
-  const int ns = m.ns, nv = 5 + ns;
-  const int ncb = sk.T / C;
-  const int s = blockIdx.x / ncb, ib = blockIdx.x % ncb;
-  const int t0 = ib * C, j0 = s * 32;
-  const int CT = C * 32;
-  const long long N = g.N;
-  for (int e = threadIdx.x; e < CT; e += blockDim.x) {
-    const int tt = e / 32, r = e % 32;
-    const int t = t0 + tt;
-    const int i = t - r;
-    if (i < 0 || i >= g.ni || j0 + r >= g.nj) continue;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) es[k * CT + e] = fw[gaddr(sk, 5, s, t, k, r)];
-    for (int k = 0; k < ns; ++k) es[(5 + k) * CT + e] = sw[gaddr(sk, NSB, s, t, k, r)];
-  }
-  __syncthreads();
+// Tile = one strip (32 rows j) x CI columns i, CI = warps per CTA: a rectangle
+// in (i, j), so every q / q_new access of a warp is one aligned 256-byte row
+// (warp = column, lane = row).  The step-major dq rows of the tile (steps
+// i0 .. i0 + CI + 30; each row is shared with the neighbouring column tiles)
+// are gathered into shared memory by 8-byte cp.async, row by row (a warp
+// reads the contiguous lanes of one step that fall into the tile), into
+// element (plane k, column ii, row r) at (k * CI + ii) * 32 + r.  The grid is
+// persistent and the tiles are double-buffered: the gather of the next tile
+// is in flight while this one is closed and gated.
+CSB_DEV void cp_async8(double* dst_smem, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src)
+               : "memory");
+}
+CSB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int PENDING>
+CSB_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(PENDING) : "memory");
+}
+
+struct GateAcc {
   unsigned long long bad_count = 0, first1 = ~0ull, first2 = ~0ull;
-  // i' = tt - r in [-31, C - 1], r in [max(0, -i'), min(31, C - 1 - i')]
-  for (int l = threadIdx.x; l < (C + 31) * C; l += blockDim.x) {
-    const int ip = -31 + l / C;
-    const int r = max(0, -ip) + l % C;
-    if (r > min(31, C - 1 - ip)) continue;
-    const int e = (ip + r) * 32 + r;
-    const int i = t0 + ip, j = j0 + r;
-    if (i < 0 || i >= g.ni || j >= g.nj) continue;
-    const long long c = (long long)i * g.nj + j;
-    double d[5 + NSB];
+};
+
+// Closure + gate of one cell, register form: all q loads first (memory-level
+// parallelism), the closure in place in those registers (dq is read from
+// shared memory where it is used: 5 + NSB live doubles instead of three such
+// arrays), the gate decodes the new state from registers (no read-back of
+// q_new).  dd: the cell's dq planes, stride DS.
+template <int NSB>
+CSB_DEV void epilogue_cell(const Model& m, int scheme, const double* __restrict__ qc,
+                           double* __restrict__ qo, const double* dd, int DS, long long N,
+                           long long c, double* __restrict__ dq_std, GateAcc& ga) {
+  const int ns = m.ns, nv = 5 + ns;
+  if (dq_std) {
 #pragma unroll
     for (int k = 0; k < 5 + NSB; ++k)
-      if (k < nv) d[k] = es[k * CT + e];
-    if (dq_std) {
+      if (k < nv) dq_std[(long long)k * N + c] = dd[k * DS];
+  }
+  double o[5 + NSB];  // q, then q_new in place
 #pragma unroll
-      for (int k = 0; k < 5 + NSB; ++k)
-        if (k < nv) dq_std[(long long)k * N + c] = d[k];
+  for (int k = 0; k < 5 + NSB; ++k) o[k] = k < nv ? qc[k * N] : 0.0;
+  const double d0 = dd[0];
+  bool ok1 = true;
+  if (scheme == SCH_CI) {
+    o[0] = o[0] + d0;
+    double tail = 0.0;
+#pragma unroll
+    for (int sp = 0; sp < NSB; ++sp)
+      if (sp < ns - 1) {
+        o[5 + sp] = o[5 + sp] + dd[(5 + sp) * DS];
+        tail += o[5 + sp];
+      }
+    const double lastv = o[0] - tail;
+    // bitwise select (a guarded store here becomes one dynamically indexed
+    // store, which moves o[] to local memory)
+#pragma unroll
+    for (int sp = 0; sp < NSB; ++sp) {
+      const unsigned long long msk = 0ull - (unsigned long long)(sp == ns - 1);
+      o[5 + sp] = __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(o[5 + sp]) & ~msk) |
+                                                   ((unsigned long long)__double_as_longlong(lastv) & msk)));
     }
-    // all q loads first (memory-level parallelism), closure in registers, the
-    // gate decodes the new state from registers (no read-back of q_new)
-    const double* qc = q + c;
-    double* qo = qn + c;
-    double qv[5 + NSB], o[5 + NSB];
+    ok1 = !(lastv < -1e-10 * o[0]);
+  } else {
+    double tot = 0.0, dsum = 0.0;
 #pragma unroll
-    for (int k = 0; k < 5 + NSB; ++k) qv[k] = k < nv ? qc[k * N] : 0.0;
-#pragma unroll
-    for (int k = 0; k < 5; ++k) o[k] = qv[k] + d[k];
-    bool ok1 = true;
-    if (scheme == SCH_CI) {
-      double tail = 0.0;
+    for (int sp = 0; sp < NSB; ++sp)
+      if (sp < ns) {
+        tot += o[5 + sp];
+        dsum += dd[(5 + sp) * DS];
+      }
+    double osum = 0.0;
+    if (scheme == SCH_CS1) {
+      const double defect = d0 - dsum;
 #pragma unroll
       for (int sp = 0; sp < NSB; ++sp)
-        if (sp < ns - 1) {
-          o[5 + sp] = qv[5 + sp] + d[5 + sp];
-          tail += o[5 + sp];
-        }
-      const double lastv = o[0] - tail;
-      // bitwise select (a guarded store here becomes one dynamically indexed
-      // store, which moves o[] to local memory)
-#pragma unroll
-      for (int sp = 0; sp < NSB; ++sp) {
-        const unsigned long long msk = 0ull - (unsigned long long)(sp == ns - 1);
-        o[5 + sp] = __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(o[5 + sp]) & ~msk) |
-                                                     ((unsigned long long)__double_as_longlong(lastv) & msk)));
-      }
-      ok1 = !(lastv < -1e-10 * o[0]);
+        if (sp < ns) o[5 + sp] = o[5 + sp] + dd[(5 + sp) * DS] + (o[5 + sp] / tot) * defect;
     } else {
-      double tot = 0.0, dsum = 0.0;
+      const double rnew = tot + d0;
+      double rawsum = 0.0;
 #pragma unroll
       for (int sp = 0; sp < NSB; ++sp)
         if (sp < ns) {
-          tot += qv[5 + sp];
-          dsum += d[5 + sp];
+          o[5 + sp] = o[5 + sp] + dd[(5 + sp) * DS];
+          rawsum += o[5 + sp];
         }
-      double osum = 0.0;
-      if (scheme == SCH_CS1) {
-        const double defect = d[0] - dsum;
-#pragma unroll
-        for (int sp = 0; sp < NSB; ++sp)
-          if (sp < ns) o[5 + sp] = qv[5 + sp] + d[5 + sp] + (qv[5 + sp] / tot) * defect;
-      } else {
-        const double rnew = tot + d[0];
-        double rawsum = 0.0;
-#pragma unroll
-        for (int sp = 0; sp < NSB; ++sp)
-          if (sp < ns) rawsum += qv[5 + sp] + d[5 + sp];
-#pragma unroll
-        for (int sp = 0; sp < NSB; ++sp)
-          if (sp < ns) o[5 + sp] = rnew * (qv[5 + sp] + d[5 + sp]) / rawsum;
-      }
 #pragma unroll
       for (int sp = 0; sp < NSB; ++sp)
-        if (sp < ns) osum += o[5 + sp];
-      ok1 = !(osum <= 0.0);
-#pragma unroll
-      for (int sp = 0; sp < NSB; ++sp)
-        if (sp < ns && o[5 + sp] < -EPS_NEG * osum) ok1 = false;
+        if (sp < ns) o[5 + sp] = rnew * o[5 + sp] / rawsum;
     }
+    o[0] = o[0] + d0;
 #pragma unroll
-    for (int k = 0; k < 5 + NSB; ++k)
-      if (k < nv) qo[k * N] = o[k];
-    Cell<NSB> cs;
-    const bool ok2 = decode_from<NSB>(m, [&](int k) { return o[k]; }, cs);
-    if (!ok1 && first1 == ~0ull) first1 = (unsigned long long)c;
-    if (!ok2 && first2 == ~0ull) first2 = (unsigned long long)c;
-    if (!(ok1 && ok2)) ++bad_count;
+    for (int sp = 0; sp < NSB; ++sp)
+      if (sp < ns) osum += o[5 + sp];
+    ok1 = !(osum <= 0.0);
+#pragma unroll
+    for (int sp = 0; sp < NSB; ++sp)
+      if (sp < ns && o[5 + sp] < -EPS_NEG * osum) ok1 = false;
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    bad_count += __shfl_xor_sync(0xffffffffu, bad_count, o);
-    first1 = min(first1, __shfl_xor_sync(0xffffffffu, first1, o));
-    first2 = min(first2, __shfl_xor_sync(0xffffffffu, first2, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (bad_count) atomicAdd(flags + FLAG_GATE_COUNT, bad_count);
-    if (first1 != ~0ull) raise_flag(flags, EB_GATE, (long long)first1);
-    if (first2 != ~0ull) raise_flag(flags, EB_GATE_DECODE, (long long)first2);
-  }
+#pragma unroll
+  for (int k = 1; k < 5; ++k) o[k] = o[k] + dd[k * DS];
+#pragma unroll
+  for (int k = 0; k < 5 + NSB; ++k)
+    if (k < nv) qo[k * N] = o[k];
+  Cell<NSB> cs;
+  const bool ok2 = decode_from<NSB>(m, [&](int k) { return o[k]; }, cs);
+  if (!ok1 && ga.first1 == ~0ull) ga.first1 = (unsigned long long)c;
+  if (!ok2 && ga.first2 == ~0ull) ga.first2 = (unsigned long long)c;
+  if (!(ok1 && ok2)) ++ga.bad_count;
 }
 
 // Large species counts (NSB > 24): the same closure + gate with the species
@@ -1505,7 +1485,6 @@ __global__ void __launch_bounds__(256, NSB <= 8 ? 3 : 2) k_epilogue2d(const Mode
 // capped the kernel at 2 CTAs per SM with spills): every species pass
 // recomputes o_s from q (L1) and dq (shared memory) with pinned rounding
 // (__d*_rn), so every pass sees the value that was stored.
-template <int NSB>
 CSB_DEV double closure_species(int scheme, double qs, double ds, double tot, double defect,
                                double rnew, double rawsum) {
   if (scheme == SCH_CS1)  // rho_s + drho_s + (rho_s / sum rho_s)(drho - sum drho_s)
@@ -1515,135 +1494,167 @@ CSB_DEV double closure_species(int scheme, double qs, double ds, double tot, dou
   return __dadd_rn(qs, ds);  // CI (the last species is reconstructed)
 }
 
+CSB_DEV void epilogue_cell_streamed(const Model& m, int scheme, const double* __restrict__ qc,
+                                    double* __restrict__ qo, const double* dd, int DS, long long N,
+                                    long long c, double* __restrict__ dq_std, GateAcc& ga) {
+  const int ns = m.ns, nv = 5 + ns;
+  if (dq_std)
+    for (int k = 0; k < nv; ++k) dq_std[(long long)k * N + c] = dd[k * DS];
+  double o[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    o[k] = qc[k * N] + dd[k * DS];
+    qo[k * N] = o[k];
+  }
+  // pass 1: species sums
+  double tot = 0.0, dsum = 0.0, rawsum = 0.0, tail = 0.0;
+  for (int sp = 0; sp < ns; ++sp) {
+    const double qs = qc[(5 + sp) * N], ds = dd[(5 + sp) * DS];
+    tot += qs;
+    dsum += ds;
+    rawsum += qs + ds;
+    if (sp < ns - 1) tail += __dadd_rn(qs, ds);
+  }
+  const double defect = dd[0] - dsum, rnew = tot + dd[0];
+  const double lastv = o[0] - tail;
+  auto o_s = [&](int sp) {
+    if (scheme == SCH_CI && sp == ns - 1) return lastv;
+    return closure_species(scheme, qc[(5 + sp) * N], dd[(5 + sp) * DS], tot, defect, rnew, rawsum);
+  };
+  // pass 2: store
+  double osum = 0.0;
+  for (int sp = 0; sp < ns; ++sp) {
+    const double v = o_s(sp);
+    qo[(5 + sp) * N] = v;
+    osum += v;
+  }
+  bool ok1 = scheme == SCH_CI ? !(lastv < -1e-10 * o[0]) : !(osum <= 0.0);
+  // pass 3: gate (CS) and the clipped mass fractions of the decode
+  const double rho = o[0];
+  bool ok2 = (rho > 0.0) && finite(rho);
+  const double ir = 1.0 / rho;
+  double ysum = 0.0;
+  for (int sp = 0; sp < ns; ++sp) {
+    const double v = o_s(sp);
+    if (scheme != SCH_CI && v < -EPS_NEG * osum) ok1 = false;
+    double y = v * ir;
+    if (y < -EPS_NEG) ok2 = false;
+    if (y < 0.0) y = 0.0;
+    ysum += y;
+  }
+  // pass 4: renormalised mixture sums and temperature (decode_from)
+  const double isum = 1.0 / ysum;
+  double R = 0.0, cp = 0.0, yb = 0.0;
+  for (int sp = 0; sp < ns; ++sp) {
+    double y = o_s(sp) * ir;
+    if (y < 0.0) y = 0.0;
+    y = y * isum;
+    R += y * m.Rs[sp];
+    cp += y * m.cp[sp];
+    yb += y * m.bs[sp];
+  }
+  const double u0 = o[1] * ir, u1 = o[2] * ir, u2 = o[3] * ir;
+  const double Ek = 0.5 * ((u0 * u0 + u1 * u1) + u2 * u2);
+  const double T = ((o[4] * ir - Ek) - yb) * (1.0 / (cp - R));
+  if (!(T > 0.0) || !finite(T)) ok2 = false;
+  if (!ok1 && ga.first1 == ~0ull) ga.first1 = (unsigned long long)c;
+  if (!ok2 && ga.first2 == ~0ull) ga.first2 = (unsigned long long)c;
+  if (!(ok1 && ok2)) ++ga.bad_count;
+}
+
 #ifndef CSB_EPI_MINB
 #define CSB_EPI_MINB 4
 #endif
 template <int NSB>
-__global__ void __launch_bounds__(256, CSB_EPI_MINB) k_epilogue2d_s(const Model* __restrict__ mp, GridDev g,
-                                                      Skew sk, int scheme,
-                                                      const double* __restrict__ q,
-                                                      const double* __restrict__ fw,
-                                                      const double* __restrict__ sw,
-                                                      double* __restrict__ qn,
-                                                      double* __restrict__ dq_std, int C,
-                                                      unsigned long long* flags) {
+constexpr int epilogue_minb() {
+#ifdef CSB_EPI_MINB_REG
+  return NSB > 24 ? CSB_EPI_MINB : CSB_EPI_MINB_REG;
+#else
+  // measured (config 4 / 512^2 ns = 5): 2 CTAs per SM 0.875 / 0.027 ms, 3-4 CTAs
+  // (80 / 64 registers, spills) 0.947 / 0.035 ms
+  return NSB > 24 ? CSB_EPI_MINB : 2;
+#endif
+}
+
+template <int NSB>
+__global__ void __launch_bounds__(256, epilogue_minb<NSB>())
+    k_epilogue2d(const Model* __restrict__ mp, GridDev g, Skew sk, int scheme,
+                 const double* __restrict__ q, const double* __restrict__ fw,
+                 const double* __restrict__ sw, double* __restrict__ qn,
+                 double* __restrict__ dq_std, int nbuf, unsigned long long* flags) {
   extern __shared__ double es[];
   const Model& m = *mp;
   const int ns = m.ns, nv = 5 + ns;
-  const int ncb = sk.T / C;
-  const int s = blockIdx.x / ncb, ib = blockIdx.x % ncb;
-  const int t0 = ib * C, j0 = s * 32;
-  const int CT = C * 32;
+  const int CI = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int DS = CI * 32;            // plane stride inside a tile
+  const int tile_doubles = nv * DS;  // one buffer
+  const int ncol = (g.ni + CI - 1) / CI;
+  const long long ntiles = (long long)ncol * sk.nstrip;
   const long long N = g.N;
-  for (int e = threadIdx.x; e < CT; e += blockDim.x) {
-    const int tt = e / 32, r = e % 32;
-    const int t = t0 + tt;
-    const int i = t - r;
-    if (i < 0 || i >= g.ni || j0 + r >= g.nj) continue;
+  // tile -> (column block, strip), strips fastest: concurrently running CTAs
+  // cover whole rows of q
+  auto gather = [&](long long tile, double* buf) {
+    const int s = (int)(tile % sk.nstrip), i0 = (int)(tile / sk.nstrip) * CI;
+    const bool row_in = s * 32 + lane < g.nj;
+    for (int rr = warp; rr < CI + 31; rr += CI) {
+      const int ii = rr - lane;
+      if (ii < 0 || ii >= CI || i0 + ii >= g.ni || !row_in) continue;
+      const int t = i0 + rr;
+      double* dst = buf + ii * 32 + lane;
+      const double* f = fw + gaddr(sk, 5, s, t, 0, lane);
+      const double* sp = sw + gaddr(sk, NSB, s, t, 0, lane);
 #pragma unroll
-    for (int k = 0; k < 5; ++k) es[k * CT + e] = fw[gaddr(sk, 5, s, t, k, r)];
-    for (int k = 0; k < ns; ++k) es[(5 + k) * CT + e] = sw[gaddr(sk, NSB, s, t, k, r)];
+      for (int k = 0; k < 5; ++k) cp_async8(dst + k * DS, f + k * 32);
+      for (int k = 0; k < ns; ++k) cp_async8(dst + (5 + k) * DS, sp + k * 32);
+    }
+  };
+  GateAcc ga;
+  long long tile = blockIdx.x;
+  int cur = 0;
+  if (tile < ntiles) gather(tile, es);
+  cp_async_commit();
+  for (; tile < ntiles; tile += gridDim.x) {
+    const long long next = tile + gridDim.x;
+    if (nbuf > 1) {
+      if (next < ntiles) gather(next, es + (cur ^ 1) * tile_doubles);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    {
+      const int s = (int)(tile % sk.nstrip), i = (int)(tile / sk.nstrip) * CI + warp;
+      const int j = s * 32 + lane;
+      if (i < g.ni && j < g.nj) {
+        const long long c = (long long)i * g.nj + j;
+        const double* dd = es + cur * tile_doubles + warp * 32 + lane;
+        if constexpr (NSB > 24) epilogue_cell_streamed(m, scheme, q + c, qn + c, dd, DS, N, c, dq_std, ga);
+        else epilogue_cell<NSB>(m, scheme, q + c, qn + c, dd, DS, N, c, dq_std, ga);
+      }
+    }
+    __syncthreads();
+    if (nbuf > 1) {
+      cur ^= 1;
+    } else {
+      if (next < ntiles) gather(next, es);
+      cp_async_commit();
+    }
   }
-  __syncthreads();
-  unsigned long long bad_count = 0, first1 = ~0ull, first2 = ~0ull;
-  for (int l = threadIdx.x; l < (C + 31) * C; l += blockDim.x) {
-    const int ip = -31 + l / C;
-    const int r = max(0, -ip) + l % C;
-    if (r > min(31, C - 1 - ip)) continue;
-    const int e = (ip + r) * 32 + r;
-    const int i = t0 + ip, j = j0 + r;
-    if (i < 0 || i >= g.ni || j >= g.nj) continue;
-    const long long c = (long long)i * g.nj + j;
-    const double* qc = q + c;
-    double* qo = qn + c;
-    const double* dd = es + e;
-    if (dq_std)
-      for (int k = 0; k < nv; ++k) dq_std[(long long)k * N + c] = dd[k * CT];
-    double o[5];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) {
-      o[k] = qc[k * N] + dd[k * CT];
-      qo[k * N] = o[k];
-    }
-    // pass 1: species sums
-    double tot = 0.0, dsum = 0.0, rawsum = 0.0, tail = 0.0;
-    for (int sp = 0; sp < ns; ++sp) {
-      const double qs = qc[(5 + sp) * N], ds = dd[(5 + sp) * CT];
-      tot += qs;
-      dsum += ds;
-      rawsum += qs + ds;
-      if (sp < ns - 1) tail += __dadd_rn(qs, ds);
-    }
-    const double defect = dd[0] - dsum, rnew = tot + dd[0];
-    const double lastv = o[0] - tail;
-    auto o_s = [&](int sp) {
-      if (scheme == SCH_CI && sp == ns - 1) return lastv;
-      return closure_species<NSB>(scheme, qc[(5 + sp) * N], dd[(5 + sp) * CT], tot, defect, rnew,
-                                  rawsum);
-    };
-    // pass 2: store
-    double osum = 0.0;
-    for (int sp = 0; sp < ns; ++sp) {
-      const double v = o_s(sp);
-      qo[(5 + sp) * N] = v;
-      osum += v;
-    }
-    bool ok1 = scheme == SCH_CI ? !(lastv < -1e-10 * o[0]) : !(osum <= 0.0);
-    // pass 3: gate (CS) and the clipped mass fractions of the decode
-    const double rho = o[0];
-    bool ok2 = (rho > 0.0) && finite(rho);
-    const double ir = 1.0 / rho;
-    double ysum = 0.0;
-    for (int sp = 0; sp < ns; ++sp) {
-      const double v = o_s(sp);
-      if (scheme != SCH_CI && v < -EPS_NEG * osum) ok1 = false;
-      double y = v * ir;
-      if (y < -EPS_NEG) ok2 = false;
-      if (y < 0.0) y = 0.0;
-      ysum += y;
-    }
-    // pass 4: renormalised mixture sums and temperature (decode_from)
-    const double isum = 1.0 / ysum;
-    double R = 0.0, cp = 0.0, yb = 0.0;
-    for (int sp = 0; sp < ns; ++sp) {
-      double y = o_s(sp) * ir;
-      if (y < 0.0) y = 0.0;
-      y = y * isum;
-      R += y * m.Rs[sp];
-      cp += y * m.cp[sp];
-      yb += y * m.bs[sp];
-    }
-    const double u0 = o[1] * ir, u1 = o[2] * ir, u2 = o[3] * ir;
-    const double Ek = 0.5 * ((u0 * u0 + u1 * u1) + u2 * u2);
-    const double T = ((o[4] * ir - Ek) - yb) * (1.0 / (cp - R));
-    if (!(T > 0.0) || !finite(T)) ok2 = false;
-    if (!ok1 && first1 == ~0ull) first1 = (unsigned long long)c;
-    if (!ok2 && first2 == ~0ull) first2 = (unsigned long long)c;
-    if (!(ok1 && ok2)) ++bad_count;
-  }
+  cp_async_wait<0>();
   for (int o = 16; o > 0; o >>= 1) {
-    bad_count += __shfl_xor_sync(0xffffffffu, bad_count, o);
-    first1 = min(first1, __shfl_xor_sync(0xffffffffu, first1, o));
-    first2 = min(first2, __shfl_xor_sync(0xffffffffu, first2, o));
+    ga.bad_count += __shfl_xor_sync(0xffffffffu, ga.bad_count, o);
+    ga.first1 = min(ga.first1, __shfl_xor_sync(0xffffffffu, ga.first1, o));
+    ga.first2 = min(ga.first2, __shfl_xor_sync(0xffffffffu, ga.first2, o));
   }
-  if ((threadIdx.x & 31) == 0) {
-    if (bad_count) atomicAdd(flags + FLAG_GATE_COUNT, bad_count);
-    if (first1 != ~0ull) raise_flag(flags, EB_GATE, (long long)first1);
-    if (first2 != ~0ull) raise_flag(flags, EB_GATE_DECODE, (long long)first2);
+  if (lane == 0) {
+    if (ga.bad_count) atomicAdd(flags + FLAG_GATE_COUNT, ga.bad_count);
+    if (ga.first1 != ~0ull) raise_flag(flags, EB_GATE, (long long)ga.first1);
+    if (ga.first2 != ~0ull) raise_flag(flags, EB_GATE_DECODE, (long long)ga.first2);
   }
 }
 
 // ============================================================== launcher
-// epilogue tile length: the dq tile of (5 + ns) planes stays <= 48 KB so that
-// large species counts keep 4 CTAs per SM
-inline int epilogue_steps(int ns) {
-  int ce = 16;
-  if (const char* e = probe_env("CSB_EPI_C")) ce = atoi(e);  // tuning probe
-  if (ce < 2 || TQ % ce) ce = 16;  // must divide T
-  while (ce > 2 && (size_t)(5 + ns) * ce * 32 * sizeof(double) > 48 * 1024) ce /= 2;
-  return ce;
-}
-
 inline size_t wave_role_smem(int D, int WK, int NG, int nh) {
   return ((size_t)D * WK * NG * 32 + (size_t)(HRING + WK) * nh) * sizeof(double);
 }
@@ -1860,16 +1871,28 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     e = launch_pass(true, st, nullptr);
     if (e != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[3], st);
-    // ---------------- epilogue
-    // (measured at 1024^2: streamed 1.18 -> 0.87 ms at ns = 40, equal at 20,
-    // slower at 11 (0.19 -> 0.24 ms) and at config 4 (1.39 -> 1.71 ms); a
-    // variant staging q in shared memory was slower still at both ends)
-    const int CE = epilogue_steps(ns);
-    const size_t esm = (size_t)(5 + ns) * CE * 32 * sizeof(double);
-    auto kepi = NSB > 24 ? k_epilogue2d_s<NSB> : k_epilogue2d<NSB>;
-    cudaFuncSetAttribute(kepi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
-    kepi<<<sk.nstrip * (sk.T / CE), 256, esm, st>>>(mp, g, sk, scheme, q, wb.fw, wb.sw, qn, dq_std,
-                                                    CE, flags);
+    // ---------------- epilogue (persistent grid over strip x column tiles)
+    {
+      // warps per CTA = columns per tile: 8 with two tile buffers while they
+      // stay within ~100 KB (2 CTAs per SM), one buffer above (ns > 19),
+      // fewer columns as the last resort (ns > 45)
+      int CE = 8, nbuf = 2;
+      auto esm_of = [&](int ce, int nb) { return (size_t)nb * (5 + ns) * ce * 32 * sizeof(double); };
+      if (esm_of(CE, 2) > 100 * 1024) nbuf = 1;
+      while (CE > 2 && esm_of(CE, nbuf) > 100 * 1024) CE /= 2;
+      const size_t esm = esm_of(CE, nbuf);
+      auto kepi = k_epilogue2d<NSB>;
+      cudaFuncSetAttribute(kepi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esm);
+      static int per_sm = 0;  // (per bucket instantiation; CE and esm depend on ns only)
+      static int per_sm_ns = -1;
+      if (per_sm_ns != ns) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kepi, CE * 32, esm);
+        per_sm_ns = ns;
+      }
+      const long long ntile = (long long)sk.nstrip * ((g.ni + CE - 1) / CE);
+      const int nblk = (int)std::min<long long>(ntile, (long long)sms * std::max(per_sm, 1));
+      kepi<<<nblk, CE * 32, esm, st>>>(mp, g, sk, scheme, q, wb.fw, wb.sw, qn, dq_std, nbuf, flags);
+    }
     if (ev) cudaEventRecord(ev[4], st);
   });
   return cudaGetLastError();
