@@ -193,6 +193,16 @@ CSB_DEV void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 CSB_DEV int ld_volatile_s(const int* p) { return *(volatile const int*)p; }
+// 8-byte asynchronous global -> shared copies (records staging, epilogue gather)
+CSB_DEV void cp_async8(double* dst_smem, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src)
+               : "memory");
+}
+CSB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int PENDING>
+CSB_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(PENDING) : "memory");
+}
 
 // step-major group address of (strip s, step t, plane p, row r)
 CSB_DEV long long gaddr(const Skew& k, int NG, int s, int t, int p, int r) {
@@ -546,6 +556,272 @@ __global__ void __launch_bounds__(256, NSB <= 8 ? 4 : 3) k_records2d(const Model
     }
   }
   publish_tile(wb, s, ib);
+}
+
+// ============================================================== records, sliding window
+// The CS records of the serial launch order (no concurrent forward sweep).
+// A persistent CTA walks along one strip in blocks of C wavefront steps and
+// keeps the per-cell quantities of the last C + 2 steps in shared-memory rings
+// indexed by step, so every cell is decoded once per strip it touches (34 / 32
+// of the cells) instead of once per tile halo ((C + 2) x 34 / (C x 32) = 1.6
+// at the 4-step tiles of k_records2d), and the natural-layout loads come in
+// runs of C consecutive rows of one grid column (k_records2d: runs of C + 2 on
+// a 4-step tile; measured at config 4: 10.8 GB through L2 for 2.7 GB of
+// input).
+//   phase A (item = cell of steps t0 + 1 .. t0 + C, rows -1 .. 32): decode +
+//     transport into the A ring (what the face radii of the neighbours need);
+//     the pass-through inputs of the cell itself (-R, V, S_k, lam_S, dOmega
+//     diagonal) and the face vectors go to shared memory by cp.async.
+//   phase B (warp = step t0 .. t0 + C - 1, lane = row): local time step,
+//     diagonals, the four faces, and all record stores (256-byte rows).
+// Work unit = (chunk of L steps, strip), chunks outermost, so the strips of a
+// chunk run side by side (their halo rows hit L2).
+template <int C>
+constexpr int rec_s_threads() { return (34 * C + 31) / 32 * 32; }
+constexpr int REC_S_NA = 11;  // A ring planes: u v w c nf nsp 1/V | lower-i Sx Sy, lower-j Sx Sy
+// T ring planes (cell itself): rho h beta hr V Sz | -R source [5 + NSB] | lamS | dOmega diag [NSB]
+template <int NSB>
+constexpr int rec_s_ntp(bool per_species) { return 6 + 5 + NSB + 1 + (per_species ? NSB : 0); }
+template <int NSB, int C>
+constexpr size_t rec_s_smem(bool per_species) {
+  return ((size_t)REC_S_NA * (C + 2) * 34 + (size_t)rec_s_ntp<NSB>(per_species) * (C + 1) * 32) *
+         sizeof(double);
+}
+
+template <int NSB, int C>
+__global__ void __launch_bounds__(rec_s_threads<C>(), C >= 16 ? 1 : (C >= 8 ? 2 : 4))
+    k_records2d_s(const Model* __restrict__ mp, GridDev g, Skew sk, const double* __restrict__ q,
+                  const double* __restrict__ R, const double* __restrict__ cfl_p,
+                  const double* __restrict__ lamS, const double* __restrict__ domd, int dom_stride,
+                  int per_species, double sp_scale, WaveBufs wb, int L, unsigned long long* flags) {
+  extern __shared__ double sm[];
+  const Model& m = *mp;
+  const int ns = m.ns, nv = 5 + ns;
+  const int nsI = per_species ? NSB : 1;
+  const int NSF = nsI + NSB + 2;
+  constexpr int RA = C + 2, RT = C + 1, HY = 34;
+  constexpr int SA = RA * HY, ST = RT * 32;  // plane strides of the rings
+  double* A = sm;
+  double* TP = sm + REC_S_NA * SA;
+  constexpr int T_RHS = 6, T_LAMS = 6 + 5 + NSB, T_DOM = T_LAMS + 1;
+  const long long N = g.N;
+  const double cfl = *cfl_p;
+  const int nchunk = (sk.T + L - 1) / L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto slot_a = [](int step) { return (step + 1) % RA; };  // step >= -1
+  auto slot_t = [](int step) { return step % RT; };
+
+  for (int unit = blockIdx.x; unit < nchunk * sk.nstrip; unit += gridDim.x) {
+    const int s = unit % sk.nstrip, tb = (unit / sk.nstrip) * L, te = min(tb + L, sk.T);
+    const int j0 = s * 32;
+    // ---------------- phase A: n steps from tf
+    auto phase_a = [&](int tf, int n, int tin) {  // T ring (cell itself) from step tin on
+      const int l = threadIdx.x;
+      if (l >= 34 * C) return;
+      const int rr = l % 34, tt = (l / 34 + rr) % C;  // a run of C lanes shares one grid column
+      if (tt >= n) return;
+      const int step = tf + tt, r = rr - 1;
+      const int i = step - r, j = j0 + r;
+      if (i < 0 || j < 0 || i > g.ni || j > g.nj) return;
+      double* a = A + slot_a(step) * HY + rr;
+      if (j < g.nj) {  // lower-i face (includes the boundary face i = ni)
+        const long long f = face_index(g, 0, i, j, 0);
+        a[7 * SA] = __ldg(g.S[0] + f);
+        a[8 * SA] = __ldg(g.S[0] + g.NF[0] + f);
+      }
+      if (i < g.ni) {  // lower-j face (includes j = nj)
+        const long long f = face_index(g, 1, i, j, 0);
+        a[9 * SA] = __ldg(g.S[1] + f);
+        a[10 * SA] = __ldg(g.S[1] + g.NF[1] + f);
+      }
+      if (i >= g.ni || j >= g.nj) return;
+      const long long c = (long long)i * g.nj + j;
+      const bool inner = r >= 0 && r < 32 && step >= tin;
+      double* tp = TP + slot_t(inner ? step : 0) * 32 + (inner ? r : 0);
+      if (inner) {
+        // (plain loads: a warp's 8-byte cp.async requests reach L2 one sector
+        // per lane, measured 291 M L2 read sectors for 157 M requested)
+        tp[5 * ST] = __ldg(g.S[2] + 2 * g.NF[2] + 2 * c);  // k-face z component (nk == 1)
+#pragma unroll
+        for (int k0 = 0; k0 < 5 + NSB; k0 += 8) {
+          double rv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) rv[k] = k0 + k < nv ? __ldg(R + (long long)(k0 + k) * N + c) : 0.0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (k0 + k < 5 + NSB) tp[(T_RHS + k0 + k) * ST] = rv[k];
+        }
+        if (lamS) tp[T_LAMS * ST] = lamS[c];
+        if (per_species)
+          for (int sp = 0; sp < ns; ++sp)
+            tp[(T_DOM + sp) * ST] = domd[(long long)sp * dom_stride * N + c];
+      }
+      Cell<NSB> cs;
+      const bool ok = decode_from<NSB>(m, [&](int kq) { return __ldg(q + c + kq * N); }, cs);
+      double mu, kc, D, nf, nsp, nu;
+      transport<NSB>(m, cs.T, cs.Y, cs.rho, mu, kc, D);
+      diffusivities(mu, kc, D, cs.rho, cs.cp - cs.R, nf, nsp, nu);
+      a[0 * SA] = cs.u[0];
+      a[1 * SA] = cs.u[1];
+      a[2 * SA] = cs.u[2];
+      a[3 * SA] = cs.c;
+      a[4 * SA] = nf;
+      a[5 * SA] = nsp;
+      const double V = __ldg(g.vol + c);
+      a[6 * SA] = 1.0 / V;
+      if (inner) {
+        if (!ok) raise_flag(flags, EB_DECODE, c);
+        tp[4 * ST] = V;
+        tp[0 * ST] = cs.rho;
+        tp[1 * ST] = cs.h;
+        tp[2 * ST] = cs.gamma - 1.0;
+        tp[3 * ST] = 0.5 / cs.rho;
+      }
+    };
+    // ---------------- phase B: step t0 + warp, row = lane
+    auto phase_b = [&](int t0) {
+      if (warp >= C) return;
+      const int t = t0 + warp, r = lane;
+      const int i = t - r, j = j0 + r;
+      // cells outside the grid are padding slots: zeroed once at workspace
+      // setup, never written
+      if (i < 0 || i >= g.ni || j >= g.nj) return;
+      const long long c = (long long)i * g.nj + j;
+      const int hc = slot_a(t) * HY + r + 1;
+      const int up = slot_a(t + 1) * HY + r + 1;  // (i + 1, j); (i, j + 1) at up + 1
+      const int lo = slot_a(t - 1) * HY + r + 1;  // (i - 1, j); (i, j - 1) at lo - 1
+      const double* tp = TP + slot_t(t) * 32 + r;
+      const double u = A[0 * SA + hc], v = A[1 * SA + hc], w = A[2 * SA + hc], cc = A[3 * SA + hc];
+      const double nf = A[4 * SA + hc], nsp = A[5 * SA + hc], iV = A[6 * SA + hc];
+      const double rho = tp[0 * ST], h = tp[1 * ST], beta = tp[2 * ST], hr = tp[3 * ST];
+      const double V = tp[4 * ST], Sz = tp[5 * ST];
+      const double nu = npmax(nf, nsp);
+      // cell radii at the cell-averaged metric, dtau (implicit.py:152-163, 33-44)
+      double li[3], lv[3], rf = 0.0, rsp = 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        double U, a2, sq;
+        if (d < 2) {
+          const int hu = d == 0 ? up : up + 1;
+          const double s0 = 0.5 * (A[(7 + 2 * d) * SA + hc] + A[(7 + 2 * d) * SA + hu]);
+          const double s1 = 0.5 * (A[(8 + 2 * d) * SA + hc] + A[(8 + 2 * d) * SA + hu]);
+          U = fabs(u * s0 + v * s1);
+          a2 = s0 * s0 + s1 * s1;
+          sq = sqrt(a2);
+        } else {
+          U = fabs(w * Sz);
+          a2 = Sz * Sz;
+          sq = fabs(Sz);
+        }
+        li[d] = U + cc * sq;
+        lv[d] = nu * a2 * iV;
+        const double lf = (U + cc * sq) + 2.0 * nf * a2 * iV;
+        const double ls = U + 2.0 * nsp * a2 * iV;
+        rf = d == 0 ? lf : rf + lf;
+        rsp = d == 0 ? ls : rsp + ls;
+      }
+      const double den = iV * (((li[0] + li[1]) + li[2]) + ((lv[0] + lv[1]) + lv[2])) +
+                         (lamS ? tp[T_LAMS * ST] : 0.0);
+      if (!(den > 0.0)) raise_flag(flags, EB_ZERO_WAVE, c);
+      const double dtau = cfl / den;
+      const double base = V / dtau;
+      const double dflow = base + rf;
+      bool bad = !(fabs(dflow) >= 1e-300) || !isfinite(dflow);
+      const double dsp0 = base + rsp;
+      double* ff = wb.ff + gaddr(sk, NFF, s, t, 0, r);
+      double* fb = wb.fb + gaddr(sk, NFB, s, t, 0, r);
+      double* sf = wb.sf + gaddr(sk, NSF, s, t, 0, r);
+      double* sb = wb.sb + gaddr(sk, NSF, s, t, 0, r);
+      if (per_species) {
+        for (int sp = 0; sp < ns; ++sp) {
+          const double x = dsp0 - tp[(T_DOM + sp) * ST] * V;
+          bad |= !(fabs(x) >= 1e-300) || !isfinite(x);
+          const double ix = 1.0 / x;
+          __stcs(&sf[sp * 32], ix);
+          __stcs(&sb[sp * 32], ix);
+        }
+        for (int sp = ns; sp < NSB; ++sp) {  // padding species
+          __stcs(&sf[sp * 32], 0.0);
+          __stcs(&sb[sp * 32], 0.0);
+        }
+      } else {
+        bad |= !(fabs(dsp0) >= 1e-300) || !isfinite(dsp0);
+        const double ix = 1.0 / dsp0;
+        __stcs(&sf[0], ix);
+        __stcs(&sb[0], ix);
+      }
+      if (bad) raise_flag(flags, EB_SINGULAR, c);
+#pragma unroll
+      for (int k = 0; k < NSB; ++k) __stcs(&sf[(nsI + k) * 32], k < ns ? -tp[(T_RHS + 5 + k) * ST] : 0.0);
+      {
+        const double Ek = 0.5 * ((u * u + v * v) + w * w);
+        double cell[11];
+        cell[0] = 1.0 / dflow;
+        cell[1] = rho;
+        cell[2] = rho * u;
+        cell[3] = rho * v;
+        cell[4] = rho * w;
+        cell[5] = rho * h;
+        cell[6] = beta * Ek;
+        cell[7] = -beta * u;
+        cell[8] = -beta * v;
+        cell[9] = -beta * w;
+        cell[10] = beta;
+#pragma unroll
+        for (int p = 0; p < 11; ++p) {
+          __stcs(&ff[p * 32], cell[p]);
+          __stcs(&fb[p * 32], cell[p]);
+        }
+#pragma unroll
+        for (int k = 0; k < 5; ++k) __stcs(&ff[(11 + k) * 32], -tp[(T_RHS + k) * ST]);
+      }
+      // faces: 0 upper-i (i+1), 1 upper-j (j+1), 2 lower-i (i), 3 lower-j (j)
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const int d = f & 1;
+        const bool upper = f < 2;
+        // face metric: upper-i = lower-i face of (i + 1, j), upper-j = lower-j
+        // face of (i, j + 1); S_z = 0 on i/j faces of a 2-D grid (k_check_2d)
+        const int nb = upper ? (d == 0 ? up : up + 1) : (d == 0 ? lo : lo - 1);
+        const int hf = upper ? nb : hc;
+        const double S0 = A[(7 + 2 * d) * SA + hf], S1 = A[(8 + 2 * d) * SA + hf];
+        const double a2 = S0 * S0 + S1 * S1;
+        const double ar = sqrt(a2);
+        const bool nb_in = upper ? (d == 0 ? i + 1 < g.ni : j + 1 < g.nj) : (d == 0 ? i > 0 : j > 0);
+        auto lam = [&](int hh, bool sp) {
+          const double U = fabs(A[0 * SA + hh] * S0 + A[1 * SA + hh] * S1);
+          if (sp) return U + 2.0 * A[5 * SA + hh] * a2 * A[6 * SA + hh];
+          return (U + A[3 * SA + hh] * ar) + 2.0 * A[4 * SA + hh] * a2 * A[6 * SA + hh];
+        };
+        double lf = lam(hc, false), ls = lam(hc, true);
+        if (nb_in) {
+          lf = npmax(lf, lam(nb, false));
+          ls = npmax(ls, lam(nb, true));
+        }
+        const double sgn_lf = upper ? lf : -lf, sgn_ls = upper ? ls : -ls;
+        const double U = u * S0 + v * S1;
+        double* fd = upper ? ff + (16 + 7 * d) * 32 : fb + (11 + 7 * d) * 32;
+        __stcs(&fd[0 * 32], -U * hr);
+        __stcs(&fd[1 * 32], S0 * hr);
+        __stcs(&fd[2 * 32], S1 * hr);
+        __stcs(&fd[3 * 32], 0.5 * S0);
+        __stcs(&fd[4 * 32], 0.5 * S1);
+        __stcs(&fd[5 * 32], 0.5 * U);
+        __stcs(&fd[6 * 32], 0.5 * (U + sgn_lf));
+        const double csp = sp_scale * (U + sgn_ls);
+        if (upper) __stcs(&sf[(nsI + NSB + d) * 32], csp);
+        else __stcs(&sb[(nsI + d) * 32], csp);
+      }
+    };
+    __syncthreads();  // the previous unit's phase B is done with the rings
+    phase_a(tb - 1, 2, tb);
+    for (int t0 = tb; t0 < te; t0 += C) {
+      phase_a(t0 + 1, C, tb);
+      __syncthreads();
+      phase_b(t0);
+      __syncthreads();
+    }
+  }
 }
 
 // Coupled operator with chemistry: the species block inverses dinv[r][c]
@@ -1379,15 +1655,6 @@ __global__ void __launch_bounds__(wave_threads<NSB>(), 1) k_wave2d(WaveArgs a) {
 // element (plane k, column ii, row r) at (k * CI + ii) * 32 + r.  The grid is
 // persistent and the tiles are double-buffered: the gather of the next tile
 // is in flight while this one is closed and gated.
-CSB_DEV void cp_async8(double* dst_smem, const double* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src)
-               : "memory");
-}
-CSB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int PENDING>
-CSB_DEV void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(PENDING) : "memory");
-}
 
 struct GateAcc {
   unsigned long long bad_count = 0, first1 = ~0ull, first2 = ~0ull;
@@ -1718,9 +1985,64 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     auto krec = ci ? k_records2d<NSB, true> : k_records2d<NSB, false>;
     cudaFuncSetAttribute(krec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
     const int nrec = sk.nstrip * (sk.T / C);
+    // serial order, CS: the sliding-window kernel with the longest blocks whose
+    // rings fit (measured at config 4, ns = 11: 16-step blocks at 1 CTA/SM
+    // 2.48 ms with 4.6 GB of DRAM reads, 8-step blocks at 2 CTAs/SM 2.60 ms
+    // with 7.7 GB, 4-step blocks 3.33 ms; tile kernel 3.16 ms), else the tile
+    // kernel.  CSB_REC_S = 0 | 4 | 8 | 16 picks one (all parity-tested).
+    int CS_ = 0;
+    auto ssm_of = [&](int c) -> size_t {
+      return c == 16  ? (per_species ? rec_s_smem<NSB, 16>(true) : rec_s_smem<NSB, 16>(false))
+             : c == 8 ? (per_species ? rec_s_smem<NSB, 8>(true) : rec_s_smem<NSB, 8>(false))
+                      : (per_species ? rec_s_smem<NSB, 4>(true) : rec_s_smem<NSB, 4>(false));
+    };
+    if (!ci) {
+      const size_t cap = 200 * 1024;
+      // (1024^2: ns = 5 0.249 ms with 8-step blocks at 2 CTAs/SM, 0.271 with 16; ns = 11 0.35 /
+      // 0.36; ns = 40 1.34 with 8-step blocks at 1 CTA/SM; tile kernel 0.263 / 0.39 / 1.43)
+      CS_ = NSB > 8 && ssm_of(16) <= cap ? 16 : (ssm_of(8) <= cap ? 8 : (ssm_of(4) <= cap ? 4 : 0));
+      if (const char* ev_s = getenv("CSB_REC_S")) {
+        const int c = atoi(ev_s);
+        if (c == 0 || ((c == 4 || c == 8 || c == 16) && ssm_of(c) <= cap)) CS_ = c;
+      }
+    }
+    auto launch_records_s = [&](cudaStream_t s) {
+      const int Cs = CS_;
+      const size_t ssm = ssm_of(Cs);
+      auto ks = Cs == 16 ? k_records2d_s<NSB, 16> : Cs == 8 ? k_records2d_s<NSB, 8> : k_records2d_s<NSB, 4>;
+      const int nt = Cs == 16 ? rec_s_threads<16>() : Cs == 8 ? rec_s_threads<8>() : rec_s_threads<4>();
+      cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ks, nt, ssm) != cudaSuccess ||
+          per_sm < 1)
+        per_sm = 1;
+      const int G = per_sm * device_sms();
+      // chunk count: fewest scheduling rounds x (chunk length + the 2-step prologue)
+      int best_nc = 1;
+      long long best_cost = -1;
+      const int max_nc = sk.T / Cs;
+      for (int nc = 1; nc <= max_nc; ++nc) {
+        const int Lc = ((sk.T + nc - 1) / nc + Cs - 1) / Cs * Cs;
+        if ((long long)Lc * (nc - 1) >= sk.T) continue;  // fewer chunks already cover T
+        const long long rounds = ((long long)nc * sk.nstrip + G - 1) / G;
+        const long long cost = rounds * (Lc + 2);
+        if (best_cost < 0 || cost < best_cost) {
+          best_cost = cost;
+          best_nc = nc;
+        }
+      }
+      const int Lc = ((sk.T + best_nc - 1) / best_nc + Cs - 1) / Cs * Cs;
+      const int nunit = ((sk.T + Lc - 1) / Lc) * sk.nstrip;
+      WaveBufs wr = wb;
+      wr.rdy = nullptr;
+      ks<<<std::min(nunit, G), nt, ssm, s>>>(mp, g, sk, q, R, cfl, lamS, domd, dom_stride,
+                                             per_species, sp_scale, wr, Lc, flags);
+    };
     auto launch_records = [&](cudaStream_t s, bool publish) {
       WaveBufs wr = wb;
       if (!publish) wr.rdy = nullptr;  // (no per-tile fence when nothing consumes the flags)
+      if (!publish && CS_) launch_records_s(s);
+      else
       krec<<<nrec, 256, rsm, s>>>(mp, g, sk, q, R, cfl, lamS, domd, dom_stride, per_species,
                                   sp_scale, wr, C, flags);
       if (ci_chem) {

@@ -26,6 +26,14 @@ from paper_2403_03440_b200.device import SCHEMES, get_engine  # noqa: E402
 
 
 def main():
+    if os.environ.get("CSB_L2_FETCH"):  # experiment: cudaLimitMaxL2FetchGranularity (0x05)
+        torch.cuda.init()
+        torch.zeros(1, device="cuda")
+        rt = ctypes.CDLL("libcudart.so")
+        rc = rt.cudaDeviceSetLimit(5, ctypes.c_size_t(int(os.environ["CSB_L2_FETCH"])))
+        v = ctypes.c_size_t(0)
+        rt.cudaDeviceGetLimit(ctypes.byref(v), 5)
+        print("L2 fetch granularity", rc, v.value)
     a = sys.argv[1:]
     cfg = int(a[0]) if a else 1
     ns = int(a[1]) if len(a) > 1 else 11

@@ -33,6 +33,14 @@ def spec_of(name):
 
 
 def main():
+    if os.environ.get("CSB_L2_FETCH"):  # experiment: cudaLimitMaxL2FetchGranularity (0x05)
+        torch.cuda.init()
+        torch.zeros(1, device="cuda")
+        rt = ctypes.CDLL("libcudart.so")
+        rc = rt.cudaDeviceSetLimit(5, ctypes.c_size_t(int(os.environ["CSB_L2_FETCH"])))
+        v = ctypes.c_size_t(0)
+        rt.cudaDeviceGetLimit(ctypes.byref(v), 5)
+        print("L2 fetch granularity", rc, v.value)
     names = sys.argv[1:] or ["c4"]
     out = {"lib": os.environ.get("CSB_LIB_PATH", "default")}
     for name in names:

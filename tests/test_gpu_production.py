@@ -200,6 +200,27 @@ def test_config3_synthetic_chemistry_vs_oracle(ns):
     _iteration(spec, ("CS1", "CI"), chemistry=True)
 
 
+@pytest.mark.parametrize("ns,rec", [(11, None), (11, "4"), (20, None), (40, None)])
+def test_serial_order_chemistry_sliding_records_vs_oracle(ns, rec):
+    """Serial launch order (what every grid above 24 strips runs): the
+    sliding-window records kernel with per-species diagonals (dOmega) and
+    lam_S, at the block length the launcher picks and at a forced one."""
+    from paper_2403_03440_b200 import configs as C
+    spec = C.config3(ns, seed=5, dims=(40, 72, 1), chemistry=True)
+    with _env(CSB_NO_OVERLAP="1", CSB_REC_S=rec):
+        _iteration(spec, ("CS1",), chemistry=True, path=2)
+
+
+@pytest.mark.parametrize("rec", ["0", "4", "8", "16"])
+def test_serial_order_records_block_lengths_vs_oracle(rec):
+    """Every records variant of the serial order (tile kernel, 4- / 8- /
+    16-step sliding blocks) on a grid with partial strips and partial chunks."""
+    from paper_2403_03440_b200 import configs as C
+    spec = C.config0(seed=25, dims=(150, 75, 1))
+    with _env(CSB_NO_OVERLAP="1", CSB_REC_S=rec):
+        _iteration(spec, ("CS1", "CS2"), path=2)
+
+
 # ------------------------------------------------------- (f) paper species off-diagonal
 
 
