@@ -38,6 +38,7 @@ struct csb_ctx {
   GridDev g{};
   int geom2d_ok = 0;
   int k2d_disabled = 0;
+  int planar_disabled = 0;  // a step found w != 0: skip the planar residual variant
   int bc_kind[6] = {-1, -1, -1, -1, -1, -1};
   int bc_axis[6] = {-1, -1, -1, -1, -1, -1};
   double bc_Tw[6] = {0, 0, 0, 0, 0, 0};
@@ -458,6 +459,7 @@ int csb_set_grid(csb_ctx* c, int ni, int nj, int nk, const double* Si, const dou
   if (changed) c->has_ws = false;
   c->geom2d_ok = 0;
   c->k2d_disabled = 0;
+  c->planar_disabled = 0;
   if (nk == 1) {
     int* d_ok = nullptr;
     if (cudaMalloc(&d_ok, sizeof(int)) != cudaSuccess) return fail(c, CSB_E_CUDA, "cudaMalloc");
@@ -487,6 +489,7 @@ int csb_set_bc(csb_ctx* c, int face, int kind, double T_wall, int axis, const do
   for (int k = 0; k < nc; ++k) c->fs[(size_t)face * nc + k] = fs_prim ? fs_prim[k] : NAN;
   c->fs_dirty = true;
   c->k2d_disabled = 0;
+  c->planar_disabled = 0;
   return CSB_OK;
 }
 
@@ -530,17 +533,18 @@ int csb_status(csb_ctx* c, unsigned long long* flags, long long* first_cell, lon
   cudaError_t e = cudaMemcpyAsync(h, c->flags, sizeof(h), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_check(c, e, "read status");
-  if (flags) *flags = h[0];
+  if (flags) *flags = h[0] & ~(1ull << EB_NONPLANAR);
   if (first_cell) {
     *first_cell = -1;  // smallest offending cell over all raised bits
     for (int b = 0; b < EB_COUNT; ++b)
-      if ((h[0] & (1ull << b)) && b != EB_KSKIP) {
+      if ((h[0] & (1ull << b)) && b != EB_KSKIP && b != EB_NONPLANAR) {
         const long long cb = (long long)h[1 + b];
         if (*first_cell < 0 || cb < *first_cell) *first_cell = cb;
       }
   }
   if (gate_count) *gate_count = (long long)h[FLAG_GATE_COUNT];
   if (h[0] & (1ull << EB_KSKIP)) c->k2d_disabled = 1;
+  if (h[0] & (1ull << EB_NONPLANAR)) c->planar_disabled = 1;
   return reset_flags(c, st);
 }
 
@@ -552,14 +556,20 @@ int csb_residual(csb_ctx* c, const double* q, double* R, double* P, int first_or
   if ((r = sync_fs(c))) return r;
   cudaStream_t st = S(stream);
   if ((r = ensure_face_metrics(c, st))) return r;
-  const bool k2d = use_k2d(c);
+  const bool k2d = use_k2d(c), planar = k2d && !c->planar_disabled;
   cudaError_t e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
-                                  k2d, c->flags, st);
-  // K2D precondition (w == 0 under symmetry k-faces) checked by that launch:
-  // the general path re-runs on the device when it raised EB_KSKIP
+                                  planar ? RES_K2D_PLANAR : (k2d ? RES_K2D : RES_GENERAL), c->flags, st);
+  // preconditions checked by the launches themselves; the slower variants
+  // re-run on the device when the faster one raised its flag (no-ops
+  // otherwise): planar (w == 0 everywhere, EB_NONPLANAR) -> K2D (w == 0
+  // under symmetry k-faces, EB_KSKIP) -> general
+  const NormsOut none{nullptr, 0, nullptr, nullptr};
+  if (e == cudaSuccess && planar)
+    e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order, RES_K2D,
+                        c->flags, st, none, nullptr, c->flags, EB_NONPLANAR);
   if (e == cudaSuccess && k2d)
-    e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order, false,
-                        c->flags, st, NormsOut{nullptr, 0, nullptr, nullptr}, nullptr, c->flags);
+    e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
+                        RES_GENERAL, c->flags, st, none, nullptr, c->flags, EB_KSKIP);
   if (e == cudaSuccess && P) e = launch_padded(c->d_model, c->ns, c->g, bc_of(c), q, P, c->flags, st);
   return cuda_check(c, e, "residual");
 }
@@ -749,15 +759,20 @@ int csb_residual_norms(csb_ctx* c, long long N, const double* R, double* out3, v
 // launch otherwise), and the standalone norms when they could not be fused.
 static cudaError_t residual_norms_impl(csb_ctx* c, const double* q, double* R, int first_order,
                                        double* norms3, cudaStream_t st) {
-  bool fused = false, fused2 = true;
-  const bool k2d = use_k2d(c);
+  bool fused = false, fused2 = true, fused3 = true;
+  const bool k2d = use_k2d(c), planar = k2d && !c->planar_disabled;
   const NormsOut nrm{c->norm_partial, c->npart_cap, c->norm_counter, norms3};
+  const NormsOut none{nullptr, 0, nullptr, nullptr};
   cudaError_t e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
-                                  k2d, c->flags, st, nrm, &fused);
+                                  planar ? RES_K2D_PLANAR : (k2d ? RES_K2D : RES_GENERAL), c->flags,
+                                  st, nrm, &fused);
+  if (e == cudaSuccess && planar)
+    e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order, RES_K2D,
+                        c->flags, st, fused ? nrm : none, &fused3, c->flags, EB_NONPLANAR);
   if (e == cudaSuccess && k2d)
-    e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order, false,
-                        c->flags, st, fused ? nrm : NormsOut{nullptr, 0, nullptr, nullptr}, &fused2,
-                        c->flags);
+    e = launch_residual(c->d_model, c->ns, c->g, bc_of(c), mech_of(c), q, R, first_order,
+                        RES_GENERAL, c->flags, st, fused ? nrm : none, &fused2, c->flags, EB_KSKIP);
+  if (!fused3) fused2 = false;
   if (e == cudaSuccess && (!fused || !fused2))
     e = launch_norms(c->ns, c->g.N, R, c->partial, norms3, st);
   return e;

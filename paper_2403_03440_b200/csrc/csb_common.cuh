@@ -32,7 +32,9 @@ enum ErrBit : int {
   EB_KSKIP = 6,        // 2-D fast-path precondition violated (internal)
   EB_BLOCK = 7,        // CI species block not invertible (implicit.py:365-368)
   EB_GATE_DECODE = 8,  // post-update cons_to_prim gate (driver.py:250)
-  EB_COUNT = 9
+  EB_NONPLANAR = 9,    // planar 2-D residual found w != 0 (internal: the K2D kernel re-runs;
+                       // never reported, csb_status masks it)
+  EB_COUNT = 10
 };
 // flag buffer layout (unsigned long long): [0] bits, [1+b] first cell of bit b,
 // [15] gate-failure count

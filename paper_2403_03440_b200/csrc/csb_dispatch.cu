@@ -12,8 +12,8 @@ unsigned long long launch_count() { return g_launches.load(std::memory_order_rel
 
 #define CSB_DECL(b)                                                                               \
   cudaError_t launch_residual_b##b(const Model*, int, const GridDev&, const BCDev&, const Mech&,   \
-                                   const double*, double*, int, bool, unsigned long long*,         \
-                                   cudaStream_t, NormsOut, bool*, const unsigned long long*);      \
+                                   const double*, double*, int, int, unsigned long long*,          \
+                                   cudaStream_t, NormsOut, bool*, const unsigned long long*, int); \
   cudaError_t launch_padded_b##b(const Model*, int, const GridDev&, const BCDev&, const double*,   \
                                  double*, unsigned long long*, cudaStream_t);                      \
   cudaError_t launch_decode_b##b(const Model*, int, const GridDev&, const double*, double*,        \
@@ -60,12 +60,13 @@ CSB_BUCKET_LIST(CSB_DECL)
   }
 
 cudaError_t launch_residual(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
-                            const Mech& mech, const double* q, double* R, int first_order, bool k2d,
+                            const Mech& mech, const double* q, double* R, int first_order, int mode,
                             unsigned long long* flags, cudaStream_t st, NormsOut nrm, bool* fused,
-                            const unsigned long long* guard) {
+                            const unsigned long long* guard, int guard_bit) {
   note_launches(1);
   if (fused) *fused = false;
-  CSB_ROUTE(launch_residual, mp, ns, g, bc, mech, q, R, first_order, k2d, flags, st, nrm, fused, guard)
+  CSB_ROUTE(launch_residual, mp, ns, g, bc, mech, q, R, first_order, mode, flags, st, nrm, fused, guard,
+            guard_bit)
 }
 cudaError_t launch_padded(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                           const double* q, double* P, unsigned long long* flags, cudaStream_t st) {

@@ -94,11 +94,16 @@ struct NormsOut {
 
 // launch_residual returns with *fused = true when the norms were computed
 // in the same launch (nrm.out set and the tile count fits nrm.cap).
+// mode: RES_GENERAL, RES_K2D (nk == 1 fast path) or RES_K2D_PLANAR (K2D with
+// w == 0 everywhere: raises EB_NONPLANAR otherwise).  guard: run only when
+// bit guard_bit of *guard is set (device-side fallback behind a faster mode).
+enum ResidualMode : int { RES_GENERAL = 0, RES_K2D = 1, RES_K2D_PLANAR = 2 };
 cudaError_t launch_residual(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
-                            const Mech& mech, const double* q, double* R, int first_order, bool k2d,
+                            const Mech& mech, const double* q, double* R, int first_order, int mode,
                             unsigned long long* flags, cudaStream_t st,
                             NormsOut nrm = NormsOut{nullptr, 0, nullptr, nullptr},
-                            bool* fused = nullptr, const unsigned long long* guard = nullptr);
+                            bool* fused = nullptr, const unsigned long long* guard = nullptr,
+                            int guard_bit = 6 /* EB_KSKIP */);
 cudaError_t launch_padded(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
                           const double* q, double* P, unsigned long long* flags, cudaStream_t st);
 

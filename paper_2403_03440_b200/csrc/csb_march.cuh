@@ -130,7 +130,7 @@ __global__ void k_march_pre(MarchCfg k, cudaGraphConditionalHandle step) {
 // after an implicit-step attempt: accept, retry at half the CFL, or stop
 __global__ void k_march_after(MarchCfg k, cudaGraphConditionalHandle retry) {
   MarchState& s = *k.st;
-  const unsigned long long f = k.flags[0] & ~(1ull << EB_KSKIP);
+  const unsigned long long f = k.flags[0] & ~((1ull << EB_KSKIP) | (1ull << EB_NONPLANAR));
   bool nonphys;
   if (f & (1ull << EB_DECODE)) {
     nonphys = true;

@@ -630,6 +630,191 @@ CSB_DEV bool face_visc2d(const Model& m, const double* sP, int ldP, int im, int 
   return ok;
 }
 
+// 2-D (K2D) face flux, convective + viscous in one evaluation (the same
+// formulas as face_conv + face_visc2d, spatial.py:217-256 and 143-204, with
+// the species sums factored so that every species is visited twice instead
+// of five times):
+//   pass 1 per species: MUSCL states y_L, y_R, face average y_f, normal and
+//     tangential differences dn, dP (the gradient is g = dn xn + dP xt), and
+//     the sums the face states, the viscosity and the diffusion correction
+//     need (sum y R_s, sum y cp_s, sum y b_s on L / R / f, sum y_f mu_ref,
+//     sum dn, sum dP, sum b_s dn, ...);
+//   pass 2 per species: F_s = y_L C_L + y_R C_R + (-rho D)(g_s . S) - y_f (j . S)
+//     with C_L = rho_L (U_L / 2 + lam / 2), C_R = rho_R (U_R / 2 - lam / 2).
+// Sums are reassociated against the reference (differences of a few ulp of the
+// flux; the parity tests bound R at 1e-10 relative).  PL: planar flow (w == 0
+// in every staged cell, checked by the caller): the z components, which are
+// exactly zero on a K2D grid (k_check_2d), are not evaluated.
+template <int NSB, int D, bool PL>
+CSB_DEV bool face_flux2d(const Model& m, const double* sP, int ldP, int im, int ip, int sd, int st,
+                         const double* S, const double* xn, const double* xt, bool first_order,
+                         double* F, int ldF) {
+  constexpr int NX = PL ? 2 : 3;
+  const int ns = m.ns;
+  const int imm = im - sd, ipp = ip + sd;
+  double XNS = 0.0, XTS = 0.0, a2 = 0.0;
+#pragma unroll
+  for (int x = 0; x < NX; ++x) {
+    XNS += xn[x] * S[x];
+    XTS += xt[x] * S[x];
+    a2 += S[x] * S[x];
+  }
+  // tangential central difference of component c, face-averaged (spatial.py:241-248)
+  auto tang = [&](int c) {
+    const double* p = sP + c * ldP;
+    return 0.5 * (0.5 * (p[im + st] - p[im - st]) + 0.5 * (p[ip + st] - p[ip - st]));
+  };
+  // ---- flow components: MUSCL states, face averages, velocity gradients
+  double WL[5], WR[5], Wf[5];
+  double tSm[NX];  // (tau . S) / mu
+  {
+    double gu[NX][NX];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      if (PL && c == 3) {
+        WL[c] = WR[c] = Wf[c] = 0.0;
+        continue;
+      }
+      const double* p = sP + c * ldP;
+      const double vm = p[im], vp = p[ip];
+      const double dc = vp - vm;
+      if (first_order) {
+        WL[c] = vm;
+        WR[c] = vp;
+      } else {
+        WL[c] = vm + 0.5 * minmod(vm - p[imm], dc);
+        WR[c] = vp - 0.5 * minmod(dc, p[ipp] - vp);
+      }
+      Wf[c] = 0.5 * (vm + vp);
+      if (c >= 1 && c <= NX) {
+        const double dP = tang(c);
+#pragma unroll
+        for (int x = 0; x < NX; ++x) gu[c - 1][x] = dc * xn[x] + dP * xt[x];
+      }
+    }
+    double div = 0.0;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) div += gu[i][i];
+    const double td = 2.0 / 3.0 * div;
+#pragma unroll
+    for (int i = 0; i < NX; ++i) {
+      double acc = -td * S[i];
+#pragma unroll
+      for (int x = 0; x < NX; ++x) acc += (gu[i][x] + gu[x][i]) * S[x];
+      tSm[i] = acc;
+    }
+  }
+  double GTS;  // grad T . S
+  {
+    const double* p = sP + (5 + ns) * ldP;
+    GTS = (p[ip] - p[im]) * XNS + tang(5 + ns) * XTS;
+  }
+  // ---- species pass 1
+  double RL = 0.0, cpL = 0.0, ybL = 0.0, RR = 0.0, cpR = 0.0, ybR = 0.0;
+  double Rf = 0.0, cpf = 0.0, ybf = 0.0, mua = 0.0;
+  double Sdn = 0.0, SdP = 0.0, Bdn = 0.0, BdP = 0.0, Cdn = 0.0, CdP = 0.0;
+  for (int sp = 0; sp < ns; ++sp) {
+    const double* p = sP + (5 + sp) * ldP;
+    const double vm = p[im], vp = p[ip];
+    const double dc = vp - vm;
+    double yl = vm, yr = vp;
+    if (!first_order) {
+      yl = vm + 0.5 * minmod(vm - p[imm], dc);
+      yr = vp - 0.5 * minmod(dc, p[ipp] - vp);
+    }
+    const double yf = 0.5 * (vm + vp);
+    const double dP = 0.5 * (0.5 * (p[im + st] - p[im - st]) + 0.5 * (p[ip + st] - p[ip - st]));
+    const double Rs = m.Rs[sp], cps = m.cp[sp], bs = m.bs[sp];
+    RL += yl * Rs;
+    cpL += yl * cps;
+    ybL += yl * bs;
+    RR += yr * Rs;
+    cpR += yr * cps;
+    ybR += yr * bs;
+    Rf += yf * Rs;
+    cpf += yf * cps;
+    ybf += yf * bs;
+    if (m.suth_shared) mua += yf * m.mu_ref[sp];
+    Sdn += dc;
+    SdP += dP;
+    Bdn += bs * dc;
+    BdP += bs * dP;
+    Cdn += cps * dc;
+    CdP += cps * dP;
+  }
+  // ---- face states
+  double TL, cL, eL, TR, cR, eR;
+  bool ok = face_state_sums(WL[0], WL[1], WL[2], WL[3], WL[4], RL, cpL, ybL, TL, cL, eL);
+  ok &= face_state_sums(WR[0], WR[1], WR[2], WR[3], WR[4], RR, cpR, ybR, TR, cR, eR);
+  const double rho = Wf[0];
+  const double Tf = Wf[4] / (rho * Rf);
+  ok &= (Tf > 0.0) && finite(Tf);
+  double mu;
+  if (m.suth_shared) {
+    const double xx = Tf * m.inv_T_mu[0];
+    mu = mua * ((xx * sqrt(xx)) * m.TS[0] / (Tf + m.S_mu[0]));
+  } else {
+    mu = 0.0;
+    for (int sp = 0; sp < ns; ++sp) {
+      const double* p = sP + (5 + sp) * ldP;
+      mu += (0.5 * (p[im] + p[ip])) * mu_species(m, sp, Tf);
+    }
+  }
+  const double kc = mu * cpf / m.Pr;
+  const double nrd = -(mu / m.Sc);  // -(rho D), D = mu / (rho Sc)
+  double UL = 0.0, UR = 0.0;
+#pragma unroll
+  for (int x = 0; x < NX; ++x) {
+    UL += WL[1 + x] * S[x];
+    UR += WR[1 + x] * S[x];
+  }
+  const double area = sqrt(a2);
+  const double hl = 0.5 * npmax(fabs(UL) + cL * area, fabs(UR) + cR * area);
+  const double JS = nrd * (Sdn * XNS + SdP * XTS);  // (sum_s j_s) . S
+  // ---- flow fluxes
+  F[0] = 0.5 * (UL * WL[0] + UR * WR[0]) - hl * (WR[0] - WL[0]);
+  double utS = 0.0;
+#pragma unroll
+  for (int x = 0; x < 3; ++x) {
+    if (x >= NX) {
+      F[(1 + x) * ldF] = 0.0;
+      continue;
+    }
+    const double qL = WL[0] * WL[1 + x], qR = WR[0] * WR[1 + x];
+    const double fl = UL * qL + WL[4] * S[x];
+    const double fr = UR * qR + WR[4] * S[x];
+    const double tS = mu * tSm[x];
+    utS += Wf[1 + x] * tS;
+    F[(1 + x) * ldF] = (0.5 * (fl + fr) - hl * (qR - qL)) - tS;
+  }
+  {
+    const double qL = WL[0] * eL, qR = WR[0] * eR;
+    const double fl = UL * qL + WL[4] * UL;
+    const double fr = UR * qR + WR[4] * UR;
+    // sum_s h_s (j_s . S), h_s = b_s + cp_s T_f
+    const double hsjS = nrd * ((Bdn + Tf * Cdn) * XNS + (BdP + Tf * CdP) * XTS) - JS * (ybf + Tf * cpf);
+    const double qS = hsjS - kc * GTS;
+    F[4 * ldF] = (0.5 * (fl + fr) - hl * (qR - qL)) + (qS - utS);
+  }
+  // ---- species pass 2
+  const double CL = WL[0] * (0.5 * UL + hl), CR = WR[0] * (0.5 * UR - hl);
+  const double nXNS = nrd * XNS, nXTS = nrd * XTS;
+  for (int sp = 0; sp < ns; ++sp) {
+    const double* p = sP + (5 + sp) * ldP;
+    const double vm = p[im], vp = p[ip];
+    const double dc = vp - vm;
+    double yl = vm, yr = vp;
+    if (!first_order) {
+      yl = vm + 0.5 * minmod(vm - p[imm], dc);
+      yr = vp - 0.5 * minmod(dc, p[ipp] - vp);
+    }
+    const double yf = 0.5 * (vm + vp);
+    const double dP = 0.5 * (0.5 * (p[im + st] - p[im - st]) + 0.5 * (p[ip + st] - p[ip - st]));
+    F[(5 + sp) * ldF] = (yl * CL + yr * CR) + ((dc * nXNS + dP * nXTS) - yf * JS);
+  }
+  return ok;
+}
+
 // 2-D face enumeration of a tile: thread index f -> face (fi, fj) and its
 // flux-buffer slot fi * FY + fj (FY = TJ + (D == 1)).  j-faces enumerate the
 // TI x TJ faces in rows of TJ first and the tile's last face column (fj = TJ)
@@ -694,6 +879,57 @@ CSB_DEV void visc_pass2d(const Model& m, const GridDev& g, const double* sP, int
   }
 }
 
+// K2D faces of direction D of one tile through face_flux2d (convective +
+// viscous in one evaluation); same face enumeration as visc_pass2d.
+template <int NSB, int D, bool PL>
+CSB_DEV void flux_pass2d(const Model& m, const GridDev& g, const double* sP, int ldP, double* sF,
+                         int maxf, int i0, int j0, int ci, int cj, int BY, int TIc, int TJc,
+                         bool first_order, unsigned long long* flags) {
+  const int FX = TIc + (D == 0), FY = TJc + (D == 1);
+  const int fx = ci + (D == 0), fy = cj + (D == 1);
+  const int nf = FX * FY;
+  const int sd = D == 0 ? BY : 1, st = D == 0 ? 1 : BY;
+  for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+    int fi, fj;
+    face_of2d<D>(f, TIc, TJc, fi, fj);
+    if (fi >= fx || fj >= fy) continue;
+    const int fs = fi * FY + fj;  // flux-buffer slot
+    const int ip = (fi + NG) * BY + (fj + NG);
+    const int im = ip - sd;
+    const int gi = i0 + fi, gj = j0 + fj;
+    double S[3], xn[3], xt[3];
+    const long long fidx = face_index(g, D, gi, gj, 0);
+    constexpr int NX = PL ? 2 : 3;
+    {
+      const double* p = g.S[D];
+      const long long nfa = g.NF[D];
+#pragma unroll
+      for (int x = 0; x < 3; ++x) S[x] = x < NX ? __ldg(p + x * nfa + fidx) : 0.0;
+    }
+    if (g.fm[D]) {
+      // static metric terms, precomputed once per grid (k_face_metrics2d)
+      const double* fm = g.fm[D] + fidx;
+      const long long nfa = g.NF[D];
+#pragma unroll
+      for (int x = 0; x < 3; ++x) {
+        xn[x] = x < NX ? __ldg(fm + x * nfa) : 0.0;
+        xt[x] = x < NX ? __ldg(fm + (3 + x) * nfa) : 0.0;
+      }
+    } else {
+      bool hasm, hasp;
+      long long cellm, cellp;
+      load_S(g, D, fidx, S);
+      face_metric2d<D>(g, gi, gj, S, xn, xt, hasm, hasp, cellm, cellp);
+    }
+    if (!face_flux2d<NSB, D, PL>(m, sP, ldP, im, ip, sd, st, S, xn, xt, first_order, sF + fs, maxf)) {
+      const int nd = D == 0 ? g.ni : g.nj, pos = D == 0 ? gi : gj;
+      raise_flag(flags, EB_FACE_T,
+                 pos < nd ? cell_index(g, gi, gj, 0)
+                          : cell_index(g, D == 0 ? gi - 1 : gi, D == 0 ? gj : gj - 1, 0));
+    }
+  }
+}
+
 // Net chemical production of one cell (chemistry.py:46-65).
 template <int NSB>
 CSB_DEV void omega_cell(const Model& m, const Mech& mech, double T, const double* rho_s,
@@ -741,7 +977,10 @@ CSB_DEV void omega_cell(const Model& m, const Mech& mech, double T, const double
 // FTI, FTJ: compile-time 2-D tile (0: runtime TI_, TJ_).  With a fixed tile
 // every shared-memory plane stride and face / cell index divisor is a
 // constant, which removes most of the integer address arithmetic.
-template <int NSB, bool K2D, int FTI = 0, int FTJ = 0>
+#ifndef CSB_RES_FUSED
+#define CSB_RES_FUSED 1  // K2D faces through face_flux2d (0: face_conv + face_visc2d)
+#endif
+template <int NSB, bool K2D, int FTI = 0, int FTJ = 0, bool PL = false>
 #ifndef CSB_RES_MINB
 #define CSB_RES_MINB 2  // measured: 3 CTAs/SM (80 registers, spills) is 12-29% slower
 #endif
@@ -750,11 +989,12 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
                                                   double* __restrict__ R, int first_order, int TI_,
                                                   int TJ_, int TK, unsigned long long* flags,
                                                   NormsOut nrm, int sr_on,
-                                                  const unsigned long long* __restrict__ guard) {
+                                                  const unsigned long long* __restrict__ guard,
+                                                  int guard_bit) {
   // guarded launch (the general-path fallback queued behind a K2D launch):
   // runs only when that launch raised EB_KSKIP (w != 0 under symmetry
   // k-faces), as a persistent grid over the tiles; otherwise exits at once
-  if (guard && !((__ldcg(guard) >> EB_KSKIP) & 1ull)) return;
+  if (guard && !((__ldcg(guard) >> guard_bit) & 1ull)) return;
   const int TI = FTI ? FTI : TI_, TJ = FTJ ? FTJ : TJ_;
   extern __shared__ double smem[];
   __shared__ Model sm;
@@ -855,6 +1095,7 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
       if (!(T > 0.0) || !finite(T)) ok = false;
       if (!ok) raise_flag(flags, EB_DECODE, cell);
       if (K2D && bc.kind[4] == BC_SYMMETRY && qc[3 * N] != 0.0) raise_flag(flags, EB_KSKIP, cell);
+      if (PL && !(qc[3 * N] == 0.0)) raise_flag(flags, EB_NONPLANAR, cell);
       sP[0 * ldP + l] = rho;
       sP[1 * ldP + l] = u[0];
       sP[2 * ldP + l] = u[1];
@@ -867,6 +1108,7 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
       if (!decode<NSB>(m, q + cell, g.N, cs)) raise_flag(flags, EB_DECODE, cell);
       if (K2D && bc.kind[4] == BC_SYMMETRY && q[cell + 3 * g.N] != 0.0)
         raise_flag(flags, EB_KSKIP, cell);
+      if (PL && !(q[cell + 3 * g.N] == 0.0)) raise_flag(flags, EB_NONPLANAR, cell);
       sP[0 * ldP + l] = cs.rho;
       sP[1 * ldP + l] = cs.u[0];
       sP[2 * ldP + l] = cs.u[1];
@@ -883,6 +1125,8 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
         for (int c = 0; c < 6 + NSB; ++c) v[c] = 0.0;
       } else {
         padded_value<NSB>(m, g, bc, q, pi, pj, pk, v, flags);
+        // (ghosts the reference never fills are NaN and never read)
+        if (PL && v[3] != 0.0 && v[3] == v[3]) raise_flag(flags, EB_NONPLANAR, 0);
       }
 #pragma unroll
       for (int c = 0; c < 6 + NSB; ++c)
@@ -908,6 +1152,12 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
     const int fx = ci + (d == 0), fy = cj + (d == 1), fz = ck + (d == 2);
     const int FY = K2D ? TJ + (d == 1) : fy;
     const int nf = K2D ? (TI + (d == 0)) * FY : fx * fy * fz;
+    if constexpr (K2D && CSB_RES_FUSED) {
+      if (d == 0)
+        flux_pass2d<NSB, 0, PL>(m, g, sP, ldP, sF, maxf, i0, j0, ci, cj, BY, TI, TJ, first_order != 0, flags);
+      else
+        flux_pass2d<NSB, 1, PL>(m, g, sP, ldP, sF, maxf, i0, j0, ci, cj, BY, TI, TJ, first_order != 0, flags);
+    } else {
     for (int f = threadIdx.x; f < nf; f += blockDim.x) {
       // (d == 1 ? ... : ...) keeps both divisors compile-time with a fixed tile
       const int fk = K2D ? 0 : f % fz;
@@ -1000,6 +1250,7 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
         raise_flag(flags, EB_FACE_T, hasp ? cellp : cellm);
     }
     }
+    }  // !(K2D && CSB_RES_FUSED)
     __syncthreads();
     // difference into R (R = 0 + dR_0 + dR_1 + dR_2, spatial.py:258-259).
     // The last direction also applies the chemistry source (261-267), the
@@ -1243,9 +1494,10 @@ static inline bool residual_in_smem(size_t smem, int cells, int nv, size_t& tota
 }
 
 cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, const BCDev& bc,
-                            const Mech& mech, const double* q, double* R, int first_order, bool k2d,
+                            const Mech& mech, const double* q, double* R, int first_order, int mode,
                             unsigned long long* flags, cudaStream_t st, NormsOut nrm, bool* fused,
-                            const unsigned long long* guard) {
+                            const unsigned long long* guard, int guard_bit) {
+  const bool k2d = mode != RES_GENERAL, planar = mode == RES_K2D_PLANAR;
   int TI, TJ, TK;
   size_t smem;
   pick_tile(ns, k2d, g.nk, TI, TJ, TK, smem);
@@ -1259,8 +1511,10 @@ cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, c
   // per CTA instead of once per tile)
   cudaError_t err = cudaSuccess;
   CSB_NS_DISPATCH(ns, {
-    auto kfn = k2d ? (TI == 15 && TJ == 16 ? k_residual<NSB, true, 15, 16> : k_residual<NSB, true>)
-                   : k_residual<NSB, false>;
+    const bool fixed = TI == 15 && TJ == 16;
+    auto kfn = !k2d    ? k_residual<NSB, false>
+               : planar ? (fixed ? k_residual<NSB, true, 15, 16, true> : k_residual<NSB, true, 0, 0, true>)
+                        : (fixed ? k_residual<NSB, true, 15, 16> : k_residual<NSB, true>);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem) != cudaSuccess ||
@@ -1270,7 +1524,7 @@ cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, c
     if (!(nrm.out && nblk <= nrm.cap)) nrm.out = nullptr;
     if (fused) *fused = nrm.out != nullptr;
     kfn<<<(unsigned)nblk, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
-                                           nrm, sr_on, guard);
+                                           nrm, sr_on, guard, guard_bit);
     err = cudaGetLastError();
   });
   return err;
