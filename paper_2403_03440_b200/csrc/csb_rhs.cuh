@@ -652,6 +652,10 @@ CSB_DEV bool face_flux2d(const Model& m, const double* sP, int ldP, int im, int 
   constexpr int NX = PL ? 2 : 3;
   const int ns = m.ns;
   const int imm = im - sd, ipp = ip + sd;
+  // PL: the caller's staged planes and flux planes have no w component
+  // (plane 3 dropped): planes >= 4 sit one plane lower
+  const double* sQ = PL ? sP - ldP : sP;
+  double* Fq = PL ? F - ldF : F;
   double XNS = 0.0, XTS = 0.0, a2 = 0.0;
 #pragma unroll
   for (int x = 0; x < NX; ++x) {
@@ -661,7 +665,7 @@ CSB_DEV bool face_flux2d(const Model& m, const double* sP, int ldP, int im, int 
   }
   // tangential central difference of component c, face-averaged (spatial.py:241-248)
   auto tang = [&](int c) {
-    const double* p = sP + c * ldP;
+    const double* p = (c >= 4 ? sQ : sP) + c * ldP;
     return 0.5 * (0.5 * (p[im + st] - p[im - st]) + 0.5 * (p[ip + st] - p[ip - st]));
   };
   // ---- flow components: MUSCL states, face averages, velocity gradients
@@ -675,7 +679,7 @@ CSB_DEV bool face_flux2d(const Model& m, const double* sP, int ldP, int im, int 
         WL[c] = WR[c] = Wf[c] = 0.0;
         continue;
       }
-      const double* p = sP + c * ldP;
+      const double* p = (c >= 4 ? sQ : sP) + c * ldP;
       const double vm = p[im], vp = p[ip];
       const double dc = vp - vm;
       if (first_order) {
@@ -706,7 +710,7 @@ CSB_DEV bool face_flux2d(const Model& m, const double* sP, int ldP, int im, int 
   }
   double GTS;  // grad T . S
   {
-    const double* p = sP + (5 + ns) * ldP;
+    const double* p = sQ + (5 + ns) * ldP;
     GTS = (p[ip] - p[im]) * XNS + tang(5 + ns) * XTS;
   }
   // ---- species pass 1
@@ -714,7 +718,7 @@ CSB_DEV bool face_flux2d(const Model& m, const double* sP, int ldP, int im, int 
   double Rf = 0.0, cpf = 0.0, ybf = 0.0, mua = 0.0;
   double Sdn = 0.0, SdP = 0.0, Bdn = 0.0, BdP = 0.0, Cdn = 0.0, CdP = 0.0;
   for (int sp = 0; sp < ns; ++sp) {
-    const double* p = sP + (5 + sp) * ldP;
+    const double* p = sQ + (5 + sp) * ldP;
     const double vm = p[im], vp = p[ip];
     const double dc = vp - vm;
     double yl = vm, yr = vp;
@@ -756,7 +760,7 @@ CSB_DEV bool face_flux2d(const Model& m, const double* sP, int ldP, int im, int 
   } else {
     mu = 0.0;
     for (int sp = 0; sp < ns; ++sp) {
-      const double* p = sP + (5 + sp) * ldP;
+      const double* p = sQ + (5 + sp) * ldP;
       mu += (0.5 * (p[im] + p[ip])) * mu_species(m, sp, Tf);
     }
   }
@@ -776,10 +780,7 @@ CSB_DEV bool face_flux2d(const Model& m, const double* sP, int ldP, int im, int 
   double utS = 0.0;
 #pragma unroll
   for (int x = 0; x < 3; ++x) {
-    if (x >= NX) {
-      F[(1 + x) * ldF] = 0.0;
-      continue;
-    }
+    if (x >= NX) continue;  // (PL: no w-momentum flux plane)
     const double qL = WL[0] * WL[1 + x], qR = WR[0] * WR[1 + x];
     const double fl = UL * qL + WL[4] * S[x];
     const double fr = UR * qR + WR[4] * S[x];
@@ -794,13 +795,13 @@ CSB_DEV bool face_flux2d(const Model& m, const double* sP, int ldP, int im, int 
     // sum_s h_s (j_s . S), h_s = b_s + cp_s T_f
     const double hsjS = nrd * ((Bdn + Tf * Cdn) * XNS + (BdP + Tf * CdP) * XTS) - JS * (ybf + Tf * cpf);
     const double qS = hsjS - kc * GTS;
-    F[4 * ldF] = (0.5 * (fl + fr) - hl * (qR - qL)) + (qS - utS);
+    Fq[4 * ldF] = (0.5 * (fl + fr) - hl * (qR - qL)) + (qS - utS);
   }
   // ---- species pass 2
   const double CL = WL[0] * (0.5 * UL + hl), CR = WR[0] * (0.5 * UR - hl);
   const double nXNS = nrd * XNS, nXTS = nrd * XTS;
   for (int sp = 0; sp < ns; ++sp) {
-    const double* p = sP + (5 + sp) * ldP;
+    const double* p = sQ + (5 + sp) * ldP;
     const double vm = p[im], vp = p[ip];
     const double dc = vp - vm;
     double yl = vm, yr = vp;
@@ -810,7 +811,7 @@ CSB_DEV bool face_flux2d(const Model& m, const double* sP, int ldP, int im, int 
     }
     const double yf = 0.5 * (vm + vp);
     const double dP = 0.5 * (0.5 * (p[im + st] - p[im - st]) + 0.5 * (p[ip + st] - p[ip - st]));
-    F[(5 + sp) * ldF] = (yl * CL + yr * CR) + ((dc * nXNS + dP * nXTS) - yf * JS);
+    Fq[(5 + sp) * ldF] = (yl * CL + yr * CR) + ((dc * nXNS + dP * nXTS) - yf * JS);
   }
   return ok;
 }
@@ -990,7 +991,7 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
                                                   int TJ_, int TK, unsigned long long* flags,
                                                   NormsOut nrm, int sr_on,
                                                   const unsigned long long* __restrict__ guard,
-                                                  int guard_bit) {
+                                                  int guard_bit, int twobuf) {
   // guarded launch (the general-path fallback queued behind a K2D launch):
   // runs only when that launch raised EB_KSKIP (w != 0 under symmetry
   // k-faces), as a persistent grid over the tiles; otherwise exits at once
@@ -1033,9 +1034,18 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
   const int ci = min(TI, g.ni - i0), cj = min(TJ, g.nj - j0), ck = K2D ? 1 : min(TK, g.nk - k0);
   double* sP = smem;
   const int maxf = max(max((TI + 1) * TJ * TK, TI * (TJ + 1) * TK), TI * TJ * (K2D ? 1 : TK + 1));
-  double* sF = smem + (long long)nc * ldP;
+  // PL (planar, w == 0): the w plane of the staged primitives and the
+  // w-momentum flux plane are not stored; PP maps a component to its plane
+  constexpr int NPD = PL ? 1 : 0;
+  auto PP = [](int c) { return PL && c > 3 ? c - 1 : c; };
+  double* sQ = sP - NPD * ldP;  // planes >= 4
+  double* sF = smem + (long long)(nc - NPD) * ldP;
+  // twobuf: the two directions' fluxes in separate buffers, one difference
+  // pass for both (no partial R between the directions, 3 barriers per tile
+  // instead of 5)
+  double* sF1 = twobuf ? sF + (long long)(nv - NPD) * maxf : sF;
   // partial residual of the tile, sum over directions in order (0 + dR_0 + ...)
-  double* sR = sF + (long long)nv * maxf;
+  double* sR = sF + (long long)(twobuf ? 2 : 1) * (nv - NPD) * maxf;
 
   // ---- stage decoded primitives + halo (padded coordinates = interior + NG)
   for (int l = threadIdx.x; l < ldP; l += blockDim.x) {
@@ -1075,15 +1085,15 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
           double y = v[k] * ir;
           if (y < -EPS_NEG) ok = false;
           if (y < 0.0) y = 0.0;
-          sP[(5 + s0 + k) * ldP + l] = y;
+          sQ[(5 + s0 + k) * ldP + l] = y;
           sum += y;
         }
       }
       double R = 0.0, cp = 0.0, yb = 0.0;
       const double isum = 1.0 / sum;
       for (int sp = 0; sp < ns; ++sp) {
-        const double y = sP[(5 + sp) * ldP + l] * isum;
-        sP[(5 + sp) * ldP + l] = y;
+        const double y = sQ[(5 + sp) * ldP + l] * isum;
+        sQ[(5 + sp) * ldP + l] = y;
         R += y * m.Rs[sp];
         cp += y * m.cp[sp];
         yb += y * m.bs[sp];
@@ -1099,9 +1109,9 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
       sP[0 * ldP + l] = rho;
       sP[1 * ldP + l] = u[0];
       sP[2 * ldP + l] = u[1];
-      sP[3 * ldP + l] = u[2];
-      sP[4 * ldP + l] = rho * R * T;
-      sP[(5 + ns) * ldP + l] = T;
+      if (!PL) sP[3 * ldP + l] = u[2];
+      sQ[4 * ldP + l] = rho * R * T;
+      sQ[(5 + ns) * ldP + l] = T;
     } else if (interior) {
       const long long cell = cell_index(g, pi - NG, pj - NG, pk - NG);
       Cell<NSB> cs;
@@ -1112,12 +1122,12 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
       sP[0 * ldP + l] = cs.rho;
       sP[1 * ldP + l] = cs.u[0];
       sP[2 * ldP + l] = cs.u[1];
-      sP[3 * ldP + l] = cs.u[2];
-      sP[4 * ldP + l] = cs.p;
+      if (!PL) sP[3 * ldP + l] = cs.u[2];
+      sQ[4 * ldP + l] = cs.p;
 #pragma unroll
       for (int s = 0; s < NSB; ++s)
-        if (s < ns) sP[(5 + s) * ldP + l] = cs.Y[s];
-      sP[(5 + ns) * ldP + l] = cs.T;
+        if (s < ns) sQ[(5 + s) * ldP + l] = cs.Y[s];
+      sQ[(5 + ns) * ldP + l] = cs.T;
     } else {
       double v[6 + NSB];
       if (!inside_pad) {
@@ -1130,7 +1140,7 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
       }
 #pragma unroll
       for (int c = 0; c < 6 + NSB; ++c)
-        if (c < nc) sP[c * ldP + l] = v[c];
+        if (c < nc && !(PL && c == 3)) sP[PP(c) * ldP + l] = v[c];
     }
   }
   __syncthreads();
@@ -1152,11 +1162,12 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
     const int fx = ci + (d == 0), fy = cj + (d == 1), fz = ck + (d == 2);
     const int FY = K2D ? TJ + (d == 1) : fy;
     const int nf = K2D ? (TI + (d == 0)) * FY : fx * fy * fz;
-    if constexpr (K2D && CSB_RES_FUSED) {
+    if constexpr (K2D && (CSB_RES_FUSED || PL)) {
       if (d == 0)
         flux_pass2d<NSB, 0, PL>(m, g, sP, ldP, sF, maxf, i0, j0, ci, cj, BY, TI, TJ, first_order != 0, flags);
       else
-        flux_pass2d<NSB, 1, PL>(m, g, sP, ldP, sF, maxf, i0, j0, ci, cj, BY, TI, TJ, first_order != 0, flags);
+        flux_pass2d<NSB, 1, PL>(m, g, sP, ldP, sF1, maxf, i0, j0, ci, cj, BY, TI, TJ, first_order != 0, flags);
+      if (twobuf && d == 0) return;  // differenced together with direction 1
     } else {
     for (int f = threadIdx.x; f < nf; f += blockDim.x) {
       // (d == 1 ? ... : ...) keeps both divisors compile-time with a fixed tile
@@ -1250,7 +1261,7 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
         raise_flag(flags, EB_FACE_T, hasp ? cellp : cellm);
     }
     }
-    }  // !(K2D && CSB_RES_FUSED)
+    }  // !(K2D && (CSB_RES_FUSED || PL))
     __syncthreads();
     // difference into R (R = 0 + dR_0 + dR_1 + dR_2, spatial.py:258-259).
     // The last direction also applies the chemistry source (261-267), the
@@ -1279,6 +1290,13 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
       const long long N = g.N;
       double* __restrict__ Rc = R + cell;
       double* __restrict__ sRc = sR + l;
+      const double* sFd = (twobuf && d == 1) ? sF1 : sF;  // this direction's fluxes
+      // twobuf: direction 0's flux difference of component plane pc
+      const int flo0 = ii * TJ + jj, fhi0 = flo0 + TJ;
+      auto prev = [&](int c, int pc) {
+        return twobuf ? sF[pc * maxf + fhi0] - sF[pc * maxf + flo0]
+                      : (sr_on ? sRc[c * ncell] : Rc[c * N]);
+      };
       if (!last) {
         // first / middle direction: partial sums, loads of a group of 8
         // components issued before their stores
@@ -1291,7 +1309,8 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
           for (int k = 0; k < 8; ++k) {
             const int c = c0 + k;
             if (c >= nv) break;
-            const double dR = sF[c * maxf + fhi] - sF[c * maxf + flo];
+            if (PL && c == 3) continue;  // (R_3 = 0 is written by the last direction)
+            const double dR = sFd[PP(c) * maxf + fhi] - sFd[PP(c) * maxf + flo];
             const double v = d == 0 ? dR : pv[k] + dR;
             if (sr_on) sRc[c * ncell] = v;
             else Rc[c * N] = v;
@@ -1309,8 +1328,8 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
         const double rho = sP[ls];
 #pragma unroll
         for (int s = 0; s < NSB; ++s)
-          if (s < ns) rs[s] = rho * sP[(5 + s) * ldP + ls];
-        omega_cell<NSB>(m, mech, sP[(5 + ns) * ldP + ls], rs, om);
+          if (s < ns) rs[s] = rho * sQ[(5 + s) * ldP + ls];
+        omega_cell<NSB>(m, mech, sQ[(5 + ns) * ldP + ls], rs, om);
         V = __ldg(g.vol + cell);
       }
       bool fin = true;
@@ -1331,12 +1350,12 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
           double pv[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            pv[k] = (c0 + k >= nv) ? 0.0 : (sr_on ? sRc[(c0 + k) * ncell] : Rc[(c0 + k) * N]);
+            pv[k] = (c0 + k >= nv || (PL && c0 + k == 3)) ? 0.0 : prev(c0 + k, PP(c0 + k));
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const int c = c0 + k;
             if (c >= nv) break;
-            double v = pv[k] + (sF[c * maxf + fhi] - sF[c * maxf + flo]);
+            double v = (PL && c == 3) ? 0.0 : pv[k] + (sFd[PP(c) * maxf + fhi] - sFd[PP(c) * maxf + flo]);
             if (chem && c >= 5) v = v - om[c - 5] * V;
             Rc[c * N] = v;
             fold(c, v);
@@ -1346,11 +1365,11 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
         double rv[5 + NSB];
 #pragma unroll
         for (int c = 0; c < 5 + NSB; ++c)
-          if (c < nv) rv[c] = sr_on ? sRc[c * ncell] : Rc[c * N];
+          if (c < nv) rv[c] = (PL && c == 3) ? 0.0 : prev(c, PP(c));
 #pragma unroll
         for (int c = 0; c < 5 + NSB; ++c)
           if (c < nv) {
-            double v = rv[c] + (sF[c * maxf + fhi] - sF[c * maxf + flo]);
+            double v = (PL && c == 3) ? 0.0 : rv[c] + (sFd[PP(c) * maxf + fhi] - sFd[PP(c) * maxf + flo]);
             if (chem && c >= 5) v = v - om[c - 5] * V;
             Rc[c * N] = v;
             fold(c, v);
@@ -1445,8 +1464,10 @@ __global__ void k_padded(const Model* __restrict__ mp, GridDev g, BCDev bc,
 // host launchers
 // ----------------------------------------------------------------------------
 
-static inline void pick_tile(int ns, bool k2d, int nk, int& TI, int& TJ, int& TK, size_t& smem) {
-  const int nc = 6 + ns, nv = 5 + ns;
+// drop: planes not stored (1 for the planar 2-D variant: w and its flux)
+static inline void pick_tile(int ns, bool k2d, int nk, int& TI, int& TJ, int& TK, size_t& smem,
+                             int drop = 0) {
+  const int nc = 6 + ns - drop, nv = 5 + ns - drop;
   const size_t budget = 200 * 1024;
   if (k2d) {
     // the largest tile that keeps 2 CTAs per SM (<= 104 KB), else the largest
@@ -1500,9 +1521,26 @@ cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, c
   const bool k2d = mode != RES_GENERAL, planar = mode == RES_K2D_PLANAR;
   int TI, TJ, TK;
   size_t smem;
-  pick_tile(ns, k2d, g.nk, TI, TJ, TK, smem);
+  pick_tile(ns, k2d, g.nk, TI, TJ, TK, smem, planar ? 1 : 0);
+  // planar: both directions' fluxes resident (one difference pass) when the
+  // second buffer keeps the tile's CTAs per SM (static shared memory ~4.9 KB
+  // and the 1 KB system reservation per CTA come on top)
+#ifndef CSB_RES_TWOBUF
+#define CSB_RES_TWOBUF 1
+#endif
+  int twobuf = 0;
+  if (planar && CSB_RES_TWOBUF) {
+    const size_t maxf = std::max((size_t)(TI + 1) * TJ, (size_t)TI * (TJ + 1));
+    const size_t smem2 = smem + maxf * (4 + ns) * sizeof(double);
+    const size_t two = (227 * 1024) / 2 - 1024 - 5 * 1024, one = 200 * 1024;
+    if (smem2 <= (smem <= (size_t)104 * 1024 ? two : one)) {
+      twobuf = 1;
+      smem = smem2;
+    }
+  }
   size_t smem_sr;
-  const int sr_on = residual_in_smem(smem, TI * TJ * TK, 5 + ns, smem_sr) ? 1 : 0;
+  const int sr_on =
+      !twobuf && residual_in_smem(smem, TI * TJ * TK, 5 + ns, smem_sr) ? 1 : 0;
   if (sr_on) smem = smem_sr;
   const long long ntiles = (long long)((g.ni + TI - 1) / TI) * ((g.nj + TJ - 1) / TJ) *
                            (k2d ? 1 : (g.nk + TK - 1) / TK);
@@ -1524,7 +1562,7 @@ cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, c
     if (!(nrm.out && nblk <= nrm.cap)) nrm.out = nullptr;
     if (fused) *fused = nrm.out != nullptr;
     kfn<<<(unsigned)nblk, 256, smem, st>>>(mp, g, bc, mech, q, R, first_order, TI, TJ, TK, flags,
-                                           nrm, sr_on, guard, guard_bit);
+                                           nrm, sr_on, guard, guard_bit, twobuf);
     err = cudaGetLastError();
   });
   return err;
