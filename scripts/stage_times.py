@@ -53,8 +53,9 @@ def main():
         qn, R, norms = eng.empty(eng.nv, eng.N), eng.empty(eng.nv, eng.N), eng.empty(4)
         st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
         lib = eng.lib
+        sch = int(os.environ.get("CSB_SCHEME", "1"))  # 1 CS1, 2 CS2, 0 CI
         for _ in range(3):
-            assert lib.csb_iteration(eng.ctx, q.data_ptr(), float(spec.cfl), 1, 0, 0, qn.data_ptr(),
+            assert lib.csb_iteration(eng.ctx, q.data_ptr(), float(spec.cfl), sch, 0, 0, qn.data_ptr(),
                                      R.data_ptr(), norms.data_ptr(), st) == 0
         torch.cuda.synchronize()
         K = 5
@@ -64,13 +65,13 @@ def main():
             lib.csb_residual(eng.ctx, q.data_ptr(), R.data_ptr(), None, 0, st)
         b.record()
         for _ in range(K):
-            lib.csb_iteration(eng.ctx, q.data_ptr(), float(spec.cfl), 1, 0, 0, qn.data_ptr(),
+            lib.csb_iteration(eng.ctx, q.data_ptr(), float(spec.cfl), sch, 0, 0, qn.data_ptr(),
                               R.data_ptr(), norms.data_ptr(), st)
         c.record()
         torch.cuda.synchronize()
         ms5 = (ctypes.c_float * 5)()
         for _ in range(2):
-            lib.csb_profile_step(eng.ctx, q.data_ptr(), R.data_ptr(), float(spec.cfl), 1,
+            lib.csb_profile_step(eng.ctx, q.data_ptr(), R.data_ptr(), float(spec.cfl), sch,
                                  qn.data_ptr(), ms5, st)
         eng.status()
         out[name] = {"residual_ms": a.elapsed_time(b) / K, "iteration_ms": b.elapsed_time(c) / K,
