@@ -579,16 +579,19 @@ __global__ void __launch_bounds__(256, NSB <= 8 ? 4 : 3) k_records2d(const Model
 template <int C>
 constexpr int rec_s_threads() { return (34 * C + 31) / 32 * 32; }
 constexpr int REC_S_NA = 11;  // A ring planes: u v w c nf nsp 1/V | lower-i Sx Sy, lower-j Sx Sy
-// T ring planes (cell itself): rho h beta hr V Sz | -R source [5 + NSB] | lamS | dOmega diag [NSB]
+// T ring planes (cell itself): rho h beta hr V Sz | -R source [5 + NSB] | lamS |
+// CS with chemistry: dOmega diag [NSB];  CI: T, rho Y [NSB]
 template <int NSB>
-constexpr int rec_s_ntp(bool per_species) { return 6 + 5 + NSB + 1 + (per_species ? NSB : 0); }
+constexpr int rec_s_ntp(bool per_species, bool ci = false) {
+  return 6 + 5 + NSB + 1 + (ci ? 1 + NSB : (per_species ? NSB : 0));
+}
 template <int NSB, int C>
-constexpr size_t rec_s_smem(bool per_species) {
-  return ((size_t)REC_S_NA * (C + 2) * 34 + (size_t)rec_s_ntp<NSB>(per_species) * (C + 1) * 32) *
+constexpr size_t rec_s_smem(bool per_species, bool ci = false) {
+  return ((size_t)REC_S_NA * (C + 2) * 34 + (size_t)rec_s_ntp<NSB>(per_species, ci) * (C + 1) * 32) *
          sizeof(double);
 }
 
-template <int NSB, int C>
+template <int NSB, int C, bool CI>
 __global__ void __launch_bounds__(rec_s_threads<C>(), C >= 16 ? 1 : (C >= 8 ? 2 : 4))
     k_records2d_s(const Model* __restrict__ mp, GridDev g, Skew sk, const double* __restrict__ q,
                   const double* __restrict__ R, const double* __restrict__ cfl_p,
@@ -604,6 +607,8 @@ __global__ void __launch_bounds__(rec_s_threads<C>(), C >= 16 ? 1 : (C >= 8 ? 2 
   double* A = sm;
   double* TP = sm + REC_S_NA * SA;
   constexpr int T_RHS = 6, T_LAMS = 6 + 5 + NSB, T_DOM = T_LAMS + 1;
+  constexpr int T_TEMP = T_LAMS + 1, T_RY = T_TEMP + 1;  // CI
+  constexpr int NV = 5 + NSB;
   const long long N = g.N;
   const double cfl = *cfl_p;
   const int nchunk = (sk.T + L - 1) / L;
@@ -652,7 +657,7 @@ __global__ void __launch_bounds__(rec_s_threads<C>(), C >= 16 ? 1 : (C >= 8 ? 2 
             if (k0 + k < 5 + NSB) tp[(T_RHS + k0 + k) * ST] = rv[k];
         }
         if (lamS) tp[T_LAMS * ST] = lamS[c];
-        if (per_species)
+        if (!CI && per_species)
           for (int sp = 0; sp < ns; ++sp)
             tp[(T_DOM + sp) * ST] = domd[(long long)sp * dom_stride * N + c];
       }
@@ -675,7 +680,12 @@ __global__ void __launch_bounds__(rec_s_threads<C>(), C >= 16 ? 1 : (C >= 8 ? 2 
         tp[0 * ST] = cs.rho;
         tp[1 * ST] = cs.h;
         tp[2 * ST] = cs.gamma - 1.0;
-        tp[3 * ST] = 0.5 / cs.rho;
+        tp[3 * ST] = CI ? 1.0 / cs.rho : 0.5 / cs.rho;
+        if constexpr (CI) {
+          tp[T_TEMP * ST] = cs.T;
+#pragma unroll
+          for (int sp = 0; sp < NSB; ++sp) tp[(T_RY + sp) * ST] = sp < ns ? cs.rho * cs.Y[sp] : 0.0;
+        }
       }
     };
     // ---------------- phase B: step t0 + warp, row = lane
@@ -725,6 +735,77 @@ __global__ void __launch_bounds__(rec_s_threads<C>(), C >= 16 ? 1 : (C >= 8 ? 2 
       if (!(den > 0.0)) raise_flag(flags, EB_ZERO_WAVE, c);
       const double dtau = cfl / den;
       const double base = V / dtau;
+      if constexpr (CI) {
+        // one scalar diagonal with the unified radius (implicit.py:362-373)
+        double rci = 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          // (U + c |Sc|) + 2 nu a2 / V from the terms formed above
+          rci = d == 0 ? li[d] + 2.0 * lv[d] : rci + (li[d] + 2.0 * lv[d]);
+        }
+        const double dci = base + rci;
+        if (!(fabs(dci) >= 1e-300) || !isfinite(dci)) raise_flag(flags, EB_SINGULAR, c);
+        if (per_species && wb.ci_d) wb.ci_d[c] = dci;  // chemistry: the block inverse needs d
+        const int NGc = per_species ? ci_ng<NSB, true>() : ci_ng<NSB, false>();
+        double* cf = wb.ff + gaddr(sk, NGc, s, t, 0, r);
+        double* cb = wb.fb + gaddr(sk, NGc, s, t, 0, r);
+        const double Ek = 0.5 * ((u * u + v * v) + w * w);
+        const double Tc = tp[T_TEMP * ST];
+        auto both = [&](int p, double x) {
+          __stcs(&cf[p * 32], x);
+          __stcs(&cb[p * 32], x);
+        };
+        both(0, 1.0 / dci);
+        both(1, hr);  // 1 / rho
+        both(2, rho);
+        both(3, rho * u);
+        both(4, rho * v);
+        both(5, rho * w);
+        both(6, rho * h);
+        both(2 + NV + 0, beta * Ek);
+        both(2 + NV + 1, -beta * u);
+        both(2 + NV + 2, -beta * v);
+        both(2 + NV + 3, -beta * w);
+        both(2 + NV + 4, beta);
+#pragma unroll
+        for (int sp = 0; sp < NSB; ++sp) {
+          // _w_column / _grad_p_row species entries (implicit.py:59-81)
+          const bool real = sp < ns;
+          const double RsT = real ? m.Rs[sp] * Tc : 0.0;
+          const double hs = real ? m.bs[sp] + m.cp[sp] * Tc : 0.0;
+          both(2 + 5 + sp, tp[(T_RY + sp) * ST]);
+          both(2 + NV + 5 + sp, real ? RsT - beta * (hs - RsT) : 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < NV; ++k)
+          __stcs(&cf[(2 + 2 * NV + k) * 32], k < nv ? -tp[(T_RHS + k) * ST] : 0.0);
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const int d = f & 1;
+          const bool upper = f < 2;
+          const int nb = upper ? (d == 0 ? up : up + 1) : (d == 0 ? lo : lo - 1);
+          const int hf = upper ? nb : hc;
+          const double S0 = A[(7 + 2 * d) * SA + hf], S1 = A[(8 + 2 * d) * SA + hf];
+          const double a2 = S0 * S0 + S1 * S1;
+          const double ar = sqrt(a2);
+          const bool nb_in = upper ? (d == 0 ? i + 1 < g.ni : j + 1 < g.nj) : (d == 0 ? i > 0 : j > 0);
+          // unified face radius (implicit.py:176-197 with nu = max(nu_flow, nu_sp))
+          auto lam = [&](int hh) {
+            const double Uh = fabs(A[0 * SA + hh] * S0 + A[1 * SA + hh] * S1);
+            const double nuh = npmax(A[4 * SA + hh], A[5 * SA + hh]);
+            return (Uh + A[3 * SA + hh] * ar) + 2.0 * nuh * a2 * A[6 * SA + hh];
+          };
+          double lu = lam(hc);
+          if (nb_in) lu = npmax(lu, lam(nb));
+          const double U = u * S0 + v * S1;
+          double* fd = upper ? cf + (2 + 3 * NV + 4 * d) * 32 : cb + (2 + 2 * NV + 4 * d) * 32;
+          __stcs(&fd[0 * 32], 0.5 * S0);
+          __stcs(&fd[1 * 32], 0.5 * S1);
+          __stcs(&fd[2 * 32], 0.5 * U);
+          __stcs(&fd[3 * 32], 0.5 * (U + (upper ? lu : -lu)));
+        }
+        return;
+      }
       const double dflow = base + rf;
       bool bad = !(fabs(dflow) >= 1e-300) || !isfinite(dflow);
       const double dsp0 = base + rsp;
@@ -1985,19 +2066,20 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     auto krec = ci ? k_records2d<NSB, true> : k_records2d<NSB, false>;
     cudaFuncSetAttribute(krec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
     const int nrec = sk.nstrip * (sk.T / C);
-    // serial order, CS: the sliding-window kernel with the longest blocks whose
+    // serial order (CS and CI): the sliding-window kernel with the longest blocks whose
     // rings fit (measured at config 4, ns = 11: 16-step blocks at 1 CTA/SM
     // 2.48 ms with 4.6 GB of DRAM reads, 8-step blocks at 2 CTAs/SM 2.60 ms
     // with 7.7 GB, 4-step blocks 3.33 ms; tile kernel 3.16 ms), else the tile
     // kernel.  CSB_REC_S = 0 | 4 | 8 | 16 picks one (all parity-tested).
     int CS_ = 0;
     auto ssm_of = [&](int c) -> size_t {
-      return c == 16  ? (per_species ? rec_s_smem<NSB, 16>(true) : rec_s_smem<NSB, 16>(false))
-             : c == 8 ? (per_species ? rec_s_smem<NSB, 8>(true) : rec_s_smem<NSB, 8>(false))
-                      : (per_species ? rec_s_smem<NSB, 4>(true) : rec_s_smem<NSB, 4>(false));
+      const bool ps = per_species != 0;
+      return c == 16  ? rec_s_smem<NSB, 16>(ps, ci)
+             : c == 8 ? rec_s_smem<NSB, 8>(ps, ci)
+                      : rec_s_smem<NSB, 4>(ps, ci);
     };
-    if (!ci) {
-      const size_t cap = 200 * 1024;
+    {
+      const size_t cap = 224 * 1024;  // (227 KB per CTA on sm_100)
       // (1024^2: ns = 5 0.249 ms with 8-step blocks at 2 CTAs/SM, 0.271 with 16; ns = 11 0.35 /
       // 0.36; ns = 40 1.34 with 8-step blocks at 1 CTA/SM; tile kernel 0.263 / 0.39 / 1.43)
       CS_ = NSB > 8 && ssm_of(16) <= cap ? 16 : (ssm_of(8) <= cap ? 8 : (ssm_of(4) <= cap ? 4 : 0));
@@ -2009,7 +2091,12 @@ cudaError_t CSB_BK(launch_wave_step)(const Model* mp, int ns, const GridDev& g, 
     auto launch_records_s = [&](cudaStream_t s) {
       const int Cs = CS_;
       const size_t ssm = ssm_of(Cs);
-      auto ks = Cs == 16 ? k_records2d_s<NSB, 16> : Cs == 8 ? k_records2d_s<NSB, 8> : k_records2d_s<NSB, 4>;
+      auto ks = ci ? (Cs == 16  ? k_records2d_s<NSB, 16, true>
+                      : Cs == 8 ? k_records2d_s<NSB, 8, true>
+                                : k_records2d_s<NSB, 4, true>)
+                   : (Cs == 16  ? k_records2d_s<NSB, 16, false>
+                      : Cs == 8 ? k_records2d_s<NSB, 8, false>
+                                : k_records2d_s<NSB, 4, false>);
       const int nt = Cs == 16 ? rec_s_threads<16>() : Cs == 8 ? rec_s_threads<8>() : rec_s_threads<4>();
       cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
       int per_sm = 0;
