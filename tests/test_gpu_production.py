@@ -221,6 +221,52 @@ def test_serial_order_records_block_lengths_vs_oracle(rec):
         _iteration(spec, ("CS1", "CS2", "CI"), path=2)
 
 
+@pytest.mark.parametrize("kbc", ["supersonic_outflow", "symmetry"])
+def test_residual_fallback_chain_w_nonzero_vs_oracle(kbc):
+    """The planar 2-D residual (w == 0) finds w != 0: the K2D kernel re-runs on
+    the device (outflow k boundaries), and under symmetry k boundaries the
+    general path after it; R, the fused norms of csb_iteration and a second
+    call (the context then skips the planar variant) all match the oracle."""
+    import ctypes
+
+    from paper_2403_03440_b200 import configs as C
+    from paper_2403_03440_b200 import spatial
+    from paper_2403_03440_b200.configs import build_case
+    from paper_2403_03440_b200.device import SCHEMES, get_engine
+    spec = C.config0(seed=31, dims=(45, 52, 1))
+    spec.bcs["kmin"] = C.BCSpec(kbc)
+    spec.bcs["kmax"] = C.BCSpec(kbc)
+    rng = np.random.default_rng(7)
+    rho = spec.q[..., 0]
+    w = rng.uniform(-300.0, 300.0, rho.shape)
+    spec.q[..., 3] = rho * w
+    spec.q[..., 4] += 0.5 * rho * w * w
+    grid, model, bcs, mech = spec_product(spec)
+    th, og, obcs, omech = spec_oracle(spec)
+    Ro = O.residual(spec.q, og, obcs, omech, th)
+    for _ in range(2):
+        R = spatial.assemble_residual(spec.q, grid, bcs, mech, model)
+        assert comp_relerr(R, Ro) <= TOL
+    # fused iteration entry (residual + norms + implicit step) on a fresh context
+    grid2, model2, bcs2, mech2 = build_case(spec)
+    eng = get_engine(grid2, model2)
+    eng.set_bcs(bcs2)
+    eng.set_mechanism(mech2)
+    q = eng.to_soa(spec.q, eng.nv)
+    qn, Rd, norms = eng.empty(eng.nv, eng.N), eng.empty(eng.nv, eng.N), eng.empty(4)
+    st = ctypes.c_void_p(eng.stream)
+    on = np.array(O.norms(Ro))
+    for _ in range(2):  # (the second call runs with the planar variant disabled)
+        rc = eng.lib.csb_iteration(eng.ctx, q.data_ptr(), float(spec.cfl), SCHEMES["CS1"], 0, 0,
+                                   qn.data_ptr(), Rd.data_ptr(), norms.data_ptr(), st)
+        assert rc == 0, eng.lib.csb_last_error(eng.ctx)
+        eng.status()
+        Rg = eng.from_soa(Rd, spec.q, spec.q.shape)
+        assert comp_relerr(np.asarray(Rg), Ro) <= TOL
+        got = norms.cpu().numpy()[:3]
+        assert np.max(np.abs(got - on) / np.abs(on)) <= 1e-10
+
+
 # ------------------------------------------------------- (f) paper species off-diagonal
 
 
