@@ -115,7 +115,13 @@ int csb_status(csb_ctx* ctx, unsigned long long* flags, long long* first_cell,
 /* ---------------------------------------------------------------- stages */
 
 /* assemble_residual (spatial.py:207-274): q [nv][N] -> R [nv][N].
- * P (nullable): padded primitives [6+ns][(ni+4)(nj+4)(nk+4)] (return_padded). */
+ * P (nullable): padded primitives [6+ns][(ni+4)(nj+4)(nk+4)] (return_padded).
+ * On an nk == 1 grid the library runs the fastest variant whose precondition
+ * holds and checks the precondition on the device: planar (w == 0 in every
+ * cell), then the 2-D form (k-face fluxes cancel; w == 0 under symmetry
+ * k-faces, CSB_F_KSKIP), then the general 3-D form.  The slower variants are
+ * queued behind the faster one as guarded launches that exit at once unless
+ * it raised its flag, so R is always the general path's result. */
 int csb_residual(csb_ctx* ctx, const double* q, double* R, double* P, int first_order,
                  void* stream);
 
