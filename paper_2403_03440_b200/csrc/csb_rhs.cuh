@@ -1498,25 +1498,35 @@ static inline void pick_tile(int ns, bool k2d, int nk, int& TI, int& TJ, int& TK
   const int nc = 6 + ns - drop, nv = 5 + ns - drop;
   const size_t budget = 200 * 1024;
   if (k2d) {
-    // the largest tile that keeps 2 CTAs per SM (<= 104 KB), else the largest
-    // that fits (measured: ns = 20 on a 15 x 16 tile at 1 CTA/SM is 3x slower
-    // per cell than ns = 11)
-    // (tiles below 7 x 16 cells lose more to the halo than they gain:
-    // ns = 40 on 7 x 8 at 2 CTAs/SM is 20% slower than 7 x 16 at one)
-    int cand[][2] = {{15, 16}, {11, 16}, {7, 16}, {7, 8}, {3, 8}, {3, 4}, {1, 4}};
-    if (const char* e = probe_env("CSB_RHS_TILE")) sscanf(e, "%d,%d", &cand[0][0], &cand[0][1]);
+    // TI x 16 tiles (256 threads cover the (TI + 1) x 16 faces up to TI = 15):
+    // the largest TI >= 7 that keeps 2 CTAs per SM (<= 104 KB), else the
+    // largest that fits one CTA, else the small fallbacks.  Measured at 1024^2:
+    // ns = 40 12 x 16 at 1 CTA/SM 2.55 ms (10 x 16 2.92, 8 x 16 3.07, 7 x 16
+    // 3.30; 7 x 8 at 2 CTAs/SM slower still), ns = 20 12 x 16 at 2 CTAs/SM
+    // 0.87 ms (11 x 16 0.92; 15 x 16 at 1 CTA/SM is 3x slower per cell than
+    // ns = 11).
+    auto fits = [&](int ti, int tj, size_t cap) {
+      const size_t ldP = (size_t)(ti + 4) * (tj + 4);
+      const size_t maxf = std::max((size_t)(ti + 1) * tj, (size_t)ti * (tj + 1));
+      smem = (ldP * nc + maxf * nv) * sizeof(double);
+      return smem <= cap;
+    };
+    TK = 1;
+    if (const char* e = probe_env("CSB_RHS_TILE")) {  // tuning probe
+      if (sscanf(e, "%d,%d", &TI, &TJ) == 2 && TI >= 1 && TJ >= 1 && (TI + 1) * TJ <= 1024 &&
+          fits(TI, TJ, budget))
+        return;
+    }
+    TJ = 16;
     for (int pass = 0; pass < 2; ++pass)
-      for (auto& c : cand) {
-        TI = c[0];
-        TJ = c[1];
-        TK = 1;
-        if (pass == 0 && TI * TJ < 112) break;
-        if (pass == 1 && TI == 11) continue;
-        const size_t ldP = (size_t)(TI + 4) * (TJ + 4);
-        const size_t maxf = std::max((size_t)(TI + 1) * TJ, (size_t)TI * (TJ + 1));
-        smem = (ldP * nc + maxf * nv) * sizeof(double);
-        if (smem <= (pass == 0 ? (size_t)104 * 1024 : budget)) return;
-      }
+      for (TI = 15; TI >= 7; --TI)
+        if (fits(TI, TJ, pass == 0 ? (size_t)104 * 1024 : budget)) return;
+    const int small[][2] = {{7, 8}, {3, 8}, {3, 4}, {1, 4}};
+    for (auto& c : small) {
+      TI = c[0];
+      TJ = c[1];
+      if (fits(TI, TJ, budget)) return;
+    }
   } else {
     const int cand[][3] = {{6, 8, 4}, {4, 4, 4}, {4, 4, 2}, {2, 4, 2}, {2, 2, 2}, {1, 2, 1}};
     for (auto& c : cand) {
