@@ -1,3 +1,8 @@
+"""Timing breakdown of the numpy drop-in calls at config 4 (assemble_residual,
+_implicit_step) and of the host <-> device copies under them.
+
+    python scripts/pyapi_prof.py
+"""
 import sys, time, os
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
