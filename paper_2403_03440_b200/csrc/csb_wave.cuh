@@ -1790,10 +1790,12 @@ CSB_DEV void epilogue_cell(const Model& m, int scheme, const double* __restrict_
       }
     double osum = 0.0;
     if (scheme == SCH_CS1) {
-      const double defect = d0 - dsum;
+      // (rho_s / sum rho_s) defect as rho_s (defect / sum rho_s): one division
+      // per cell instead of one per species (1-2 ulp of the correction term)
+      const double dfr = (d0 - dsum) / tot;
 #pragma unroll
       for (int sp = 0; sp < NSB; ++sp)
-        if (sp < ns) o[5 + sp] = o[5 + sp] + dd[(5 + sp) * DS] + (o[5 + sp] / tot) * defect;
+        if (sp < ns) o[5 + sp] = o[5 + sp] + dd[(5 + sp) * DS] + o[5 + sp] * dfr;
     } else {
       const double rnew = tot + d0;
       double rawsum = 0.0;
@@ -1803,9 +1805,10 @@ CSB_DEV void epilogue_cell(const Model& m, int scheme, const double* __restrict_
           o[5 + sp] = o[5 + sp] + dd[(5 + sp) * DS];
           rawsum += o[5 + sp];
         }
+      const double rsc = rnew / rawsum;
 #pragma unroll
       for (int sp = 0; sp < NSB; ++sp)
-        if (sp < ns) o[5 + sp] = rnew * o[5 + sp] / rawsum;
+        if (sp < ns) o[5 + sp] = o[5 + sp] * rsc;
     }
     o[0] = o[0] + d0;
 #pragma unroll
@@ -1833,12 +1836,12 @@ CSB_DEV void epilogue_cell(const Model& m, int scheme, const double* __restrict_
 // capped the kernel at 2 CTAs per SM with spills): every species pass
 // recomputes o_s from q (L1) and dq (shared memory) with pinned rounding
 // (__d*_rn), so every pass sees the value that was stored.
-CSB_DEV double closure_species(int scheme, double qs, double ds, double tot, double defect,
-                               double rnew, double rawsum) {
-  if (scheme == SCH_CS1)  // rho_s + drho_s + (rho_s / sum rho_s)(drho - sum drho_s)
-    return __dadd_rn(__dadd_rn(qs, ds), __dmul_rn(__ddiv_rn(qs, tot), defect));
-  if (scheme == SCH_CS2)  // (sum rho_s + drho)(rho_s + drho_s) / sum(rho_s + drho_s)
-    return __ddiv_rn(__dmul_rn(rnew, __dadd_rn(qs, ds)), rawsum);
+// dfr = (drho - sum drho_s) / sum rho_s, rsc = (sum rho_s + drho) / sum(rho_s + drho_s)
+CSB_DEV double closure_species(int scheme, double qs, double ds, double dfr, double rsc) {
+  if (scheme == SCH_CS1)  // rho_s + drho_s + rho_s (drho - sum drho_s) / sum rho_s
+    return __dadd_rn(__dadd_rn(qs, ds), __dmul_rn(qs, dfr));
+  if (scheme == SCH_CS2)  // (rho_s + drho_s)(sum rho_s + drho) / sum(rho_s + drho_s)
+    return __dmul_rn(__dadd_rn(qs, ds), rsc);
   return __dadd_rn(qs, ds);  // CI (the last species is reconstructed)
 }
 
@@ -1863,11 +1866,11 @@ CSB_DEV void epilogue_cell_streamed(const Model& m, int scheme, const double* __
     rawsum += qs + ds;
     if (sp < ns - 1) tail += __dadd_rn(qs, ds);
   }
-  const double defect = dd[0] - dsum, rnew = tot + dd[0];
+  const double dfr = (dd[0] - dsum) / tot, rsc = (tot + dd[0]) / rawsum;
   const double lastv = o[0] - tail;
   auto o_s = [&](int sp) {
     if (scheme == SCH_CI && sp == ns - 1) return lastv;
-    return closure_species(scheme, qc[(5 + sp) * N], dd[(5 + sp) * DS], tot, defect, rnew, rawsum);
+    return closure_species(scheme, qc[(5 + sp) * N], dd[(5 + sp) * DS], dfr, rsc);
   };
   // pass 2: store
   double osum = 0.0;
