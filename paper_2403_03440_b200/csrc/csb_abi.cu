@@ -334,6 +334,8 @@ int csb_set_model(csb_ctx* c, int ns, const double* M, const double* cp, const d
   m.ns = ns;
   m.Pr = Pr;
   m.Sc = Sc;
+  m.iPr = 1.0 / Pr;
+  m.iSc = 1.0 / Sc;
   for (int s = 0; s < ns; ++s) {
     m.M[s] = M[s];
     m.cp[s] = cp[s];

@@ -45,6 +45,7 @@ struct Model {
   int ns;
   int suth_shared;  // every species has the same (T_mu, S_mu): one Sutherland factor per state
   double Pr, Sc;
+  double iPr, iSc;  // 1 / Pr, 1 / Sc (fused 2-D face flux)
   double M[MAXNS], cp[MAXNS], Rs[MAXNS], bs[MAXNS];
   double mu_ref[MAXNS], T_mu[MAXNS], S_mu[MAXNS], TS[MAXNS];  // TS = T_mu + S_mu
   double inv_T_mu[MAXNS];                                      // 1 / T_mu

@@ -791,8 +791,8 @@ CSB_DEV bool face_flux2d(const Model& m, const double* sP, int ldP, int im, int 
       mu += (0.5 * (p[im] + p[ip])) * mu_species(m, sp, Tf);
     }
   }
-  const double kc = mu * cpf / m.Pr;
-  const double nrd = -(mu / m.Sc);  // -(rho D), D = mu / (rho Sc)
+  const double kc = (mu * cpf) * m.iPr;
+  const double nrd = -(mu * m.iSc);  // -(rho D), D = mu / (rho Sc)
   double UL = 0.0, UR = 0.0;
 #pragma unroll
   for (int x = 0; x < NX; ++x) {
