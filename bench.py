@@ -364,7 +364,7 @@ def e2e_python_api(run, case, K=2):
     dt = (time.perf_counter() - t0) / K
     return {"value": e.N / dt, "unit": UNIT, "ms_per_step": dt * 1e3, "steps": K,
             "call": "spatial.assemble_residual + driver._implicit_step, numpy AoS in/out "
-                    "(pageable host memory), wall clock"}
+                    "(pageable input, results in page-locked memory), wall clock"}
 
 
 def ncu_traffic(path=os.path.join(ROOT, "profiles", "ncu_traffic.json")):
