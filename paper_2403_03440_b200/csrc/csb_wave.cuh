@@ -576,6 +576,12 @@ __global__ void __launch_bounds__(256, NSB <= 8 ? 4 : 3) k_records2d(const Model
 //     diagonals, the four faces, and all record stores (256-byte rows).
 // Work unit = (chunk of L steps, strip), chunks outermost, so the strips of a
 // chunk run side by side (their halo rows hit L2).
+#ifndef CSB_REC_QFIRST
+#define CSB_REC_QFIRST 1  // measured at config 4: records 2.51 -> 2.28 ms (ns = 40: 1.34 -> 1.55, so up to 16 species)
+#endif
+#ifndef CSB_REC_RB
+#define CSB_REC_RB 8  // pass-through loads in flight per batch
+#endif
 template <int C>
 constexpr int rec_s_threads() { return (34 * C + 31) / 32 * 32; }
 constexpr int REC_S_NA = 11;  // A ring planes: u v w c nf nsp 1/V | lower-i Sx Sy, lower-j Sx Sy
@@ -643,17 +649,28 @@ __global__ void __launch_bounds__(rec_s_threads<C>(), C >= 16 ? 1 : (C >= 8 ? 2 
       const long long c = (long long)i * g.nj + j;
       const bool inner = r >= 0 && r < 32 && step >= tin;
       double* tp = TP + slot_t(inner ? step : 0) * 32 + (inner ? r : 0);
+      constexpr bool QF = CSB_REC_QFIRST && NSB <= 16;
+#if CSB_REC_QFIRST
+      // the decode's loads first: in flight while the pass-through inputs
+      // are copied
+      double qv[QF ? 5 + NSB : 1];
+      if constexpr (QF) {
+#pragma unroll
+        for (int k = 0; k < 5 + NSB; ++k) qv[k] = k < nv ? __ldg(q + c + (long long)k * N) : 0.0;
+      }
+#endif
       if (inner) {
         // (plain loads: a warp's 8-byte cp.async requests reach L2 one sector
         // per lane, measured 291 M L2 read sectors for 157 M requested)
         tp[5 * ST] = __ldg(g.S[2] + 2 * g.NF[2] + 2 * c);  // k-face z component (nk == 1)
 #pragma unroll
-        for (int k0 = 0; k0 < 5 + NSB; k0 += 8) {
-          double rv[8];
+        for (int k0 = 0; k0 < 5 + NSB; k0 += CSB_REC_RB) {
+          double rv[CSB_REC_RB];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) rv[k] = k0 + k < nv ? __ldg(R + (long long)(k0 + k) * N + c) : 0.0;
+          for (int k = 0; k < CSB_REC_RB; ++k)
+            rv[k] = k0 + k < nv ? __ldg(R + (long long)(k0 + k) * N + c) : 0.0;
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
+          for (int k = 0; k < CSB_REC_RB; ++k)
             if (k0 + k < 5 + NSB) tp[(T_RHS + k0 + k) * ST] = rv[k];
         }
         if (lamS) tp[T_LAMS * ST] = lamS[c];
@@ -662,7 +679,12 @@ __global__ void __launch_bounds__(rec_s_threads<C>(), C >= 16 ? 1 : (C >= 8 ? 2 
             tp[(T_DOM + sp) * ST] = domd[(long long)sp * dom_stride * N + c];
       }
       Cell<NSB> cs;
+#if CSB_REC_QFIRST
+      const bool ok = QF ? decode_from<NSB>(m, [&](int kq) { return qv[QF ? kq : 0]; }, cs)
+                         : decode_from<NSB>(m, [&](int kq) { return __ldg(q + c + kq * N); }, cs);
+#else
       const bool ok = decode_from<NSB>(m, [&](int kq) { return __ldg(q + c + kq * N); }, cs);
+#endif
       double mu, kc, D, nf, nsp, nu;
       transport<NSB>(m, cs.T, cs.Y, cs.rho, mu, kc, D);
       diffusivities(mu, kc, D, cs.rho, cs.cp - cs.R, nf, nsp, nu);
