@@ -3,6 +3,7 @@ for A/B comparison of library builds (load a variant with CSB_LIB_PATH).
 
     CSB_LIB_PATH=_variants/<tag>/libcsflow_b200.so python scripts/stage_times.py [cfg ...]
       cfg: c4 (4096x2048 O-grid ns=11), c3_<ns> (1024^2 box), c1 (512^2 air5)
+      CSB_SCHEME=0|1|2 picks CI / CS1 (default) / CS2
 """
 import ctypes
 import json
