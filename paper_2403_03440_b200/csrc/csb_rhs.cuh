@@ -1103,10 +1103,11 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
 #pragma unroll
       for (int x = 0; x < 3; ++x) u[x] = u[x] * ir;
       double sum = 0.0;
+      const double* qsp = qc + 5 * N;  // running pointer (one 64-bit add per component)
       for (int s0 = 0; s0 < ns; s0 += 8) {
         double v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = s0 + k < ns ? qc[(5 + s0 + k) * N] : 0.0;
+        for (int k = 0; k < 8; ++k, qsp += N) v[k] = s0 + k < ns ? *qsp : 0.0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           if (s0 + k >= ns) break;
@@ -1374,18 +1375,19 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
         }
       };
       if constexpr (stream_species<NSB>()) {
+        double* __restrict__ Rp = Rc;  // running pointer (one 64-bit add per component)
         for (int c0 = 0; c0 < nv; c0 += 8) {
           double pv[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k)
             pv[k] = (c0 + k >= nv || (PL && c0 + k == 3)) ? 0.0 : prev(c0 + k, PP(c0 + k));
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
+          for (int k = 0; k < 8; ++k, Rp += N) {
             const int c = c0 + k;
             if (c >= nv) break;
             double v = (PL && c == 3) ? 0.0 : pv[k] + (sFd[PP(c) * maxf + fhi] - sFd[PP(c) * maxf + flo]);
             if (chem && c >= 5) v = v - om[c - 5] * V;
-            Rc[c * N] = v;
+            *Rp = v;
             fold(c, v);
           }
         }
