@@ -1396,12 +1396,13 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
 #pragma unroll
         for (int c = 0; c < 5 + NSB; ++c)
           if (c < nv) rv[c] = (PL && c == 3) ? 0.0 : prev(c, PP(c));
+        double* __restrict__ Rp = Rc;
 #pragma unroll
-        for (int c = 0; c < 5 + NSB; ++c)
+        for (int c = 0; c < 5 + NSB; ++c, Rp += N)
           if (c < nv) {
             double v = (PL && c == 3) ? 0.0 : rv[c] + (sFd[PP(c) * maxf + fhi] - sFd[PP(c) * maxf + flo]);
             if (chem && c >= 5) v = v - om[c - 5] * V;
-            Rc[c * N] = v;
+            *Rp = v;
             fold(c, v);
           }
       }
