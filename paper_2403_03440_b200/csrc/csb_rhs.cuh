@@ -1322,27 +1322,30 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
       const double* sFd = (twobuf && d == 1) ? sF1 : sF;  // this direction's fluxes
       // twobuf: direction 0's flux difference of component plane pc
       const int flo0 = ii * TJ + jj, fhi0 = flo0 + TJ;
-      auto prev = [&](int c, int pc) {
+      // (Rl: the component's R word, a running pointer at the call sites)
+      auto prev = [&](int c, int pc, const double* Rl) {
         return twobuf ? sF[pc * maxf + fhi0] - sF[pc * maxf + flo0]
-                      : (sr_on ? sRc[c * ncell] : Rc[c * N]);
+                      : (sr_on ? sRc[c * ncell] : *Rl);
       };
       if (!last) {
         // first / middle direction: partial sums, loads of a group of 8
         // components issued before their stores
+        const double* Rl = Rc;  // running pointers: one 64-bit add per component
+        double* Rs = Rc;
         for (int c0 = 0; c0 < nv; c0 += 8) {
           double pv[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            pv[k] = (d == 0 || c0 + k >= nv) ? 0.0 : (sr_on ? sRc[(c0 + k) * ncell] : Rc[(c0 + k) * N]);
+          for (int k = 0; k < 8; ++k, Rl += N)
+            pv[k] = (d == 0 || c0 + k >= nv) ? 0.0 : (sr_on ? sRc[(c0 + k) * ncell] : *Rl);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
+          for (int k = 0; k < 8; ++k, Rs += N) {
             const int c = c0 + k;
             if (c >= nv) break;
             if (PL && c == 3) continue;  // (R_3 = 0 is written by the last direction)
             const double dR = sFd[PP(c) * maxf + fhi] - sFd[PP(c) * maxf + flo];
             const double v = d == 0 ? dR : pv[k] + dR;
             if (sr_on) sRc[c * ncell] = v;
-            else Rc[c * N] = v;
+            else *Rs = v;
           }
         }
         continue;
@@ -1375,12 +1378,13 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
         }
       };
       if constexpr (stream_species<NSB>()) {
-        double* __restrict__ Rp = Rc;  // running pointer (one 64-bit add per component)
+        double* __restrict__ Rp = Rc;  // running pointers (one 64-bit add per component)
+        const double* Rl = Rc;
         for (int c0 = 0; c0 < nv; c0 += 8) {
           double pv[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            pv[k] = (c0 + k >= nv || (PL && c0 + k == 3)) ? 0.0 : prev(c0 + k, PP(c0 + k));
+          for (int k = 0; k < 8; ++k, Rl += N)
+            pv[k] = (c0 + k >= nv || (PL && c0 + k == 3)) ? 0.0 : prev(c0 + k, PP(c0 + k), Rl);
 #pragma unroll
           for (int k = 0; k < 8; ++k, Rp += N) {
             const int c = c0 + k;
@@ -1395,7 +1399,7 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
         double rv[5 + NSB];
 #pragma unroll
         for (int c = 0; c < 5 + NSB; ++c)
-          if (c < nv) rv[c] = (PL && c == 3) ? 0.0 : prev(c, PP(c));
+          if (c < nv) rv[c] = (PL && c == 3) ? 0.0 : prev(c, PP(c), Rc + (long long)c * N);
         double* __restrict__ Rp = Rc;
 #pragma unroll
         for (int c = 0; c < 5 + NSB; ++c, Rp += N)
