@@ -1061,7 +1061,9 @@ __global__ void __launch_bounds__(256, CSB_RES_MINB) k_residual(const Model* __r
   const int i0 = ti * TI, j0 = tj * TJ, k0 = K2D ? 0 : tk * TK;
   const int ci = min(TI, g.ni - i0), cj = min(TJ, g.nj - j0), ck = K2D ? 1 : min(TK, g.nk - k0);
   double* sP = smem;
-  const int maxf = max(max((TI + 1) * TJ * TK, TI * (TJ + 1) * TK), TI * TJ * (K2D ? 1 : TK + 1));
+  // (K2D: one k layer, so a fixed tile makes maxf -- the flux plane stride -- a constant)
+  const int TKc = K2D ? 1 : TK;
+  const int maxf = max(max((TI + 1) * TJ * TKc, TI * (TJ + 1) * TKc), TI * TJ * (K2D ? 1 : TK + 1));
   // PL (planar, w == 0): the w plane of the staged primitives and the
   // w-momentum flux plane are not stored; PP maps a component to its plane
   constexpr int NPD = PL ? 1 : 0;
