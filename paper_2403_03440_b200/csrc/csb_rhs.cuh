@@ -1570,25 +1570,19 @@ cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, c
   size_t smem;
   pick_tile(ns, k2d, g.nk, TI, TJ, TK, smem, planar ? 1 : 0);
   // planar: both directions' fluxes resident (one difference pass) when the
-  // second buffer keeps the tile's CTAs per SM (static shared memory ~4.9 KB
-  // and the 1 KB system reservation per CTA come on top)
+  // second buffer keeps the tile's CTAs per SM (checked with the occupancy
+  // API below: static shared memory and the 1 KB system reservation per CTA
+  // come on top of the dynamic size)
 #ifndef CSB_RES_TWOBUF
 #define CSB_RES_TWOBUF 1
 #endif
-  int twobuf = 0;
+  const size_t smem1 = smem;  // one flux buffer
+  size_t smem2 = 0;
   if (planar && CSB_RES_TWOBUF) {
     const size_t maxf = std::max((size_t)(TI + 1) * TJ, (size_t)TI * (TJ + 1));
-    const size_t smem2 = smem + maxf * (4 + ns) * sizeof(double);
-    const size_t two = (227 * 1024) / 2 - 1024 - 5 * 1024, one = 200 * 1024;
-    if (smem2 <= (smem <= (size_t)104 * 1024 ? two : one)) {
-      twobuf = 1;
-      smem = smem2;
-    }
+    smem2 = smem1 + maxf * (4 + ns) * sizeof(double);
+    if (smem2 > (size_t)200 * 1024) smem2 = 0;
   }
-  size_t smem_sr;
-  const int sr_on =
-      !twobuf && residual_in_smem(smem, TI * TJ * TK, 5 + ns, smem_sr) ? 1 : 0;
-  if (sr_on) smem = smem_sr;
   const long long ntiles = (long long)((g.ni + TI - 1) / TI) * ((g.nj + TJ - 1) / TJ) *
                            (k2d ? 1 : (g.nk + TK - 1) / TK);
   // persistent grid: every resident CTA loops over the tiles (the model
@@ -1600,11 +1594,29 @@ cudaError_t CSB_BK(launch_residual)(const Model* mp, int ns, const GridDev& g, c
     auto kfn = !k2d    ? k_residual<NSB, false>
                : planar ? (fixed ? k_residual<NSB, true, 15, 16, true> : k_residual<NSB, true, 0, 0, true>)
                         : (fixed ? k_residual<NSB, true, 15, 16> : k_residual<NSB, true>);
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 256, smem) != cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
+    auto occ = [&](size_t bytes) {
+      int p = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, kfn, 256, bytes) != cudaSuccess) p = 0;
+      return p;
+    };
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max(smem1, smem2));
+    int twobuf = 0, sr_on = 0;
+    int per_sm = occ(smem1);
+    if (smem2 && occ(smem2) >= std::max(per_sm, 1)) {
+      twobuf = 1;
+      smem = smem2;
+    } else {
+      size_t smem_sr;
+      if (residual_in_smem(smem1, TI * TJ * TK, 5 + ns, smem_sr) && occ(smem_sr) >= std::max(per_sm, 1)) {
+        sr_on = 1;
+        smem = smem_sr;
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      } else {
+        smem = smem1;
+      }
+    }
+    if (per_sm < 1) per_sm = 1;
     const long long nblk = std::min<long long>(ntiles, (long long)per_sm * device_sms());
     if (!(nrm.out && nblk <= nrm.cap)) nrm.out = nullptr;
     if (fused) *fused = nrm.out != nullptr;
